@@ -1,0 +1,165 @@
+/*
+ * sparrow.h -- C-ABI of the B200-native Sparrow hot path (libsparrow.so).
+ *
+ * Plain pointers and sizes only; no torch types.  Device pointers are CUDA
+ * global-memory pointers on the handle's device; `stream` is a cudaStream_t
+ * (NULL = legacy default stream).  Every entry point returns an SpStatus; the
+ * thread-local message of the last failure is sp_last_error().
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/color_rl):
+ *
+ *   sp_cast_rays        kernels/__init__.py:62-76 -> kernels/_cy.pyx:19-106
+ *   sp_disc_collides    kernels/__init__.py:79-86 -> kernels/_cy.pyx:109-158
+ *   sp_env_create       vecenv.py:61-80 (VecEnv.__init__) + sim/core.py:47-110
+ *                       (SimBatch.__init__; map stacking core.py:62-71)
+ *   sp_env_reset_all    vecenv.py:84-92 (VecEnv.reset_all) -> core.py:114-161
+ *   sp_env_step         vecenv.py:94-116 (VecEnv.step_batch) -> core.py:165-219
+ *                       (SimBatch.step_all) incl. fused auto-reset core.py:114-161
+ *   sp_env_stats_*      vecenv.py:120-141 (snapshot_stats, first_episode_outcomes)
+ *   sp_env_read_state   sim/core.py:88-108 SoA attributes (read-only views)
+ *   sp_env_scan         sim/core.py:223-235 (SimBatch._scan) on caller poses
+ *   sp_rb_create        replay.py:31-43 (ReplayBuffer.__init__)
+ *   sp_rb_append        replay.py:48-67 (append_batch)
+ *   sp_rb_sample        replay.py:69-79 (sample)
+ *   sp_rb_size          replay.py:45-46 (__len__)
+ *   sp_rb_gather        replay.py:81-87 (snapshot: rows in storage order)
+ *   sp_random_actions   bench.py:97-105 (random policy actions), on device
+ */
+#ifndef SPARROW_H_
+#define SPARROW_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SP_OK = 0,
+  SP_EINVAL = 1,        /* ValueError: bad shape/config (core.py:56-59, vecenv.py:66-67) */
+  SP_EACTION = 2,       /* ValueError: action index out of range (core.py:169-170) */
+  SP_EEPISODE = 3,      /* EpisodeTerminated (core.py:35, 171-174) */
+  SP_EMAP = 4,          /* MapError: shapes differ / no spawn pose (core.py:63-66, 144-147) */
+  SP_ENOTREADY = 5,     /* BufferNotReady (replay.py:19, 73-75) */
+  SP_ECUDA = 6,         /* CUDA runtime failure */
+  SP_ENOMEM = 7
+} SpStatus;
+
+#define SP_MAX_ACTIONS 15 /* action codes are 4-bit; 15 marks the (0,0) delay filler */
+#define SP_MAX_DELAY 64   /* params.py:20 MAX_CONTROL_DELAY */
+
+/* EnvConfig + LidarConfig (sim/params.py:124-151) */
+typedef struct {
+  int32_t n_beams;             /* LidarConfig.n_beams */
+  double max_range_cm;         /* LidarConfig.max_range_cm */
+  double robot_radius_cm;      /* EnvConfig.robot_radius_cm */
+  int32_t timeout_steps;       /* EnvConfig.timeout_steps */
+  double proximity_cm;         /* EnvConfig.obstacle_penalty_range_cm */
+  int32_t n_actions;           /* len(EnvConfig.action_table) <= SP_MAX_ACTIONS */
+  double action_table[2 * SP_MAX_ACTIONS]; /* (v_linear, v_angular) pairs */
+  int32_t spawn_attempts;      /* EnvConfig.spawn_attempts */
+  int32_t auto_reset;          /* VecEnv(auto_reset=...) */
+  const double* beam_offsets;  /* host, n_beams: LidarConfig.beam_offsets() */
+} SpConfig;
+
+/* One occupancy map (sim/gridmap.py GridMap); all maps of an env share shape. */
+typedef struct {
+  int32_t n_rows, n_cols;      /* grid shape (H, W) */
+  double cell_cm;              /* cell_size_cm */
+  const uint8_t* occupancy;    /* host, H*W row-major [iy][ix], nonzero = occupied */
+  double goal_x, goal_y, goal_radius;
+  double spawn[4];             /* x0, y0, x1, y1 */
+  double planning_dist;        /* EnvConfig.planning_dist(map) */
+} SpMapDesc;
+
+/* DiversityRanges (params.py:55-121), one per lane or one shared. */
+typedef struct {
+  double k[2], dt[2];
+  int32_t delay[2];            /* inclusive */
+  double vmax_linear[2], vmax_angular[2], noise_std[2];
+} SpRanges;
+
+typedef struct SpEnv SpEnv;
+typedef struct SpReplay SpReplay;
+
+const char* sp_last_error(void);
+int sp_version(void);
+int sp_device_info(int device, int* n_sm, int* smem_optin_bytes, int* cc_major, int* cc_minor);
+
+/* ---- environment ------------------------------------------------------- */
+int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, int64_t n_envs,
+                  const int32_t* map_index /* host, n_envs, or NULL = (offset+i) % n_maps */,
+                  const SpRanges* ranges, int64_t n_ranges /* 1 or n_envs */,
+                  int64_t env_id_offset, int device, SpEnv** out);
+int sp_env_destroy(SpEnv* env);
+int sp_env_reset_all(SpEnv* env, uint64_t seed, float* states /* dev (N, 5+R) */, void* stream);
+int sp_env_step(SpEnv* env, const int64_t* actions /* dev (N) */, float* states,
+                float* store_states, double* rewards, uint8_t* dones, uint8_t* truncated,
+                int8_t* events, void* stream);
+/* Sticky device error word from the last step (SP_OK if none); syncs `stream`. */
+int sp_env_check(SpEnv* env, void* stream, int64_t* err_env);
+/* 1 if any lane waits for a reset (auto_reset=0 path; core.py:171-174); syncs. */
+int sp_env_any_needs_reset(SpEnv* env, void* stream, int* any);
+
+/* per-copy stats in external env order (host arrays of n_envs) */
+int sp_env_stats_read(SpEnv* env, int64_t* episodes, int64_t* arrivals, double* return_sum,
+                      int8_t* first_event, double* first_return, int64_t* first_steps,
+                      void* stream);
+/* last <=256 finished-episode returns in (step, env) order (vecenv.py:79,105) */
+int sp_env_recent_returns(SpEnv* env, double* out256, int32_t* n_out, void* stream);
+int sp_env_stats_reset(SpEnv* env, int clear_recent, void* stream);
+/* device totals {episodes, arrivals, return_sum} as 3 doubles (all-reduce payload) */
+int sp_env_stats_totals(SpEnv* env, double* dev_out3, void* stream);
+
+/* read one SoA field, external env order, into a host array of n_envs doubles.
+ * field: 0 x, 1 y, 2 heading, 3 v_linear, 4 v_angular, 5 start_x, 6 start_y,
+ * 7 k, 8 dt, 9 delay, 10 vmax_linear, 11 vmax_angular, 12 noise_std,
+ * 13 step_count, 14 needs_reset, 15 rng_ctr, 16 episode_return */
+int sp_env_read_state(SpEnv* env, int field, double* host_out, void* stream);
+int sp_env_map_info(SpEnv* env, int64_t* slot_of_env /* host n_envs, may be NULL */,
+                    int64_t* smem_bytes, int32_t* threads_per_cta, int32_t* ctas);
+
+/* LiDAR scan with the fused step's marcher on caller poses (no noise).
+ * Queries must be grouped by map: query q of map m lies in
+ * [query_offsets[m], query_offsets[m+1]).
+ * ranges[q*R + j], hit_cell[q*R + j] = iy*W+ix of the stopping occupied cell or -1. */
+int sp_env_scan(SpEnv* env, int64_t n,
+                const int64_t* query_offsets /* host n_maps+1; queries sorted by map */,
+                const double* x /* dev */, const double* y, const double* heading,
+                double* ranges /* dev n*R */, int32_t* hit_cell /* dev n*R or NULL */,
+                void* stream);
+
+/* ---- op-level plugin seam (kernels/_cy.pyx signature), device in/out ---- */
+int sp_cast_rays(const uint8_t* occ, const double* edt, int64_t n_maps, int64_t height,
+                 int64_t width, const int64_t* map_idx, const double* px, const double* py,
+                 const double* dirx, const double* diry, int64_t n, double cell,
+                 double max_range, double* out, void* stream);
+int sp_disc_collides(const uint8_t* occ, int64_t n_maps, int64_t height, int64_t width,
+                     const int64_t* map_idx, const double* px, const double* py,
+                     const double* radius, int64_t n, double cell, uint8_t* out, void* stream);
+
+/* ---- replay ring (replay.py) -------------------------------------------- */
+int sp_rb_create(int64_t capacity, int32_t state_dim, int device, SpReplay** out);
+int sp_rb_destroy(SpReplay* rb);
+/* rewards: reward_is_f64 ? double* : float*.  n <= capacity. */
+int sp_rb_append(SpReplay* rb, const float* states, const int64_t* actions, const void* rewards,
+                 int reward_is_f64, const float* next_states, const uint8_t* dones, int64_t n,
+                 void* stream);
+/* uniform with replacement over [0, size): idx_i = mulhi64(philox(seed, ctr+i, stream_id, 2), size) */
+int sp_rb_sample(SpReplay* rb, int64_t batch, uint64_t seed, uint32_t stream_id, uint64_t ctr,
+                 float* states, int64_t* actions, float* rewards, float* next_states,
+                 uint8_t* dones, int64_t* idx_out, void* stream);
+int sp_rb_size(SpReplay* rb, int64_t* size, int64_t* cursor);
+/* gather rows [0, size) in storage order */
+int sp_rb_gather(SpReplay* rb, float* states, int64_t* actions, float* rewards,
+                 float* next_states, uint8_t* dones, void* stream);
+
+/* ---- benchmark helpers ----------------------------------------------------- */
+/* actions[i] = integers(0, n_actions) from block `step` of (seed, env_id0 + i, tag 1) */
+int sp_random_actions(int64_t n, uint64_t seed, int64_t env_id0, int64_t step, int32_t n_actions,
+                      int64_t* actions, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARROW_H_ */

@@ -1,0 +1,764 @@
+// sp_capi.cu -- extern "C" implementation of include/sparrow.h.
+//
+// Host responsibilities: map preprocessing (bit-packing, 2x2-block free-box
+// table by an exact chessboard distance transform), map-major slot ordering,
+// device SoA allocation, launch geometry (one CTA per SM, shared memory =
+// one map's tables + per-warp scratch), error codes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "sp_env.cu"
+#include "sp_ops.cu"
+
+using namespace sp;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define SP_CUDA(expr)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(SP_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+constexpr int kMaxWarps = 24;  // 768 threads: keeps >= 85 registers per thread
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct DevDeviceGuard {
+  int prev = -1;
+  explicit DevDeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DevDeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// 2x2-block free-box table: 0 = block holds an occupied (or out-of-grid) cell,
+// else 1 + r with r = (chessboard distance to the nearest such block) - 1.
+void build_block_table(const uint8_t* occ, int H, int W, int Hb, int Wb, uint8_t* out) {
+  const int INF = 1 << 29;
+  std::vector<int> dist((size_t)Hb * Wb);
+  for (int by = 0; by < Hb; ++by)
+    for (int bx = 0; bx < Wb; ++bx) {
+      bool blocked = false;
+      for (int dy = 0; dy < 2 && !blocked; ++dy)
+        for (int dx = 0; dx < 2 && !blocked; ++dx) {
+          int iy = 2 * by + dy, ix = 2 * bx + dx;
+          if (iy >= H || ix >= W || occ[(size_t)iy * W + ix]) blocked = true;
+        }
+      // outside the block grid counts as blocked: distance to the border
+      int border = std::min(std::min(bx + 1, by + 1), std::min(Wb - bx, Hb - by));
+      dist[(size_t)by * Wb + bx] = blocked ? 0 : std::min(border, INF);
+    }
+  // two-pass chessboard distance transform (exact for the L-inf metric)
+  for (int by = 0; by < Hb; ++by)
+    for (int bx = 0; bx < Wb; ++bx) {
+      int& d = dist[(size_t)by * Wb + bx];
+      if (bx > 0) d = std::min(d, dist[(size_t)by * Wb + bx - 1] + 1);
+      if (by > 0) {
+        d = std::min(d, dist[(size_t)(by - 1) * Wb + bx] + 1);
+        if (bx > 0) d = std::min(d, dist[(size_t)(by - 1) * Wb + bx - 1] + 1);
+        if (bx + 1 < Wb) d = std::min(d, dist[(size_t)(by - 1) * Wb + bx + 1] + 1);
+      }
+    }
+  for (int by = Hb - 1; by >= 0; --by)
+    for (int bx = Wb - 1; bx >= 0; --bx) {
+      int& d = dist[(size_t)by * Wb + bx];
+      if (bx + 1 < Wb) d = std::min(d, dist[(size_t)by * Wb + bx + 1] + 1);
+      if (by + 1 < Hb) {
+        d = std::min(d, dist[(size_t)(by + 1) * Wb + bx] + 1);
+        if (bx + 1 < Wb) d = std::min(d, dist[(size_t)(by + 1) * Wb + bx + 1] + 1);
+        if (bx > 0) d = std::min(d, dist[(size_t)(by + 1) * Wb + bx - 1] + 1);
+      }
+    }
+  for (size_t i = 0; i < dist.size(); ++i) out[i] = (uint8_t)std::min(dist[i], 255);
+}
+
+}  // namespace
+
+struct SpEnv {
+  int device = 0;
+  EnvDev d{};
+  int64_t n = 0;
+  int R = 0, D = 0, n_maps = 0;
+  bool auto_reset = true;
+  uint64_t step_index = 0;
+  std::vector<int64_t> env_of_slot, slot_of_env, map_off;
+  std::vector<void*> allocs;
+  int grid = 0, threads = 0;
+  size_t smem = 0;
+  int n_sm = 0, smem_optin = 0;
+  int E_cap = 32;
+  int32_t* h_err = nullptr;  // pinned
+  std::mutex mu;
+
+  template <class T>
+  int alloc(T** p, size_t count, int fill_byte = 0) {
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, std::max<size_t>(count * sizeof(T), 16));
+    if (e != cudaSuccess) return fail(SP_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    cudaMemset(q, fill_byte, std::max<size_t>(count * sizeof(T), 16));
+    allocs.push_back(q);
+    *p = (T*)q;
+    return SP_OK;
+  }
+  ~SpEnv() {
+    for (void* p : allocs) cudaFree(p);
+    if (h_err) cudaFreeHost(h_err);
+  }
+};
+
+struct SpReplay {
+  int device = 0;
+  int64_t cap = 0, cursor = 0, size = 0;
+  int32_t dim = 0;
+  float *s = nullptr, *r = nullptr, *s2 = nullptr;
+  int64_t* a = nullptr;
+  uint8_t* dn = nullptr;
+  std::mutex mu;
+  ~SpReplay() {
+    cudaFree(s); cudaFree(r); cudaFree(s2); cudaFree(a); cudaFree(dn);
+  }
+};
+
+// geometry for a lane count with the env's tables
+static void plan_launch(SpEnv* env, int64_t lanes, int* grid, int* threads, int* E, size_t* smem,
+                        int* smem_maps) {
+  const EnvDev& d = env->d;
+  const size_t warp_bytes = align_up(1792 + (size_t)env->E_cap * d.D * 4, 16);
+  const size_t fixed = align_up((size_t)d.R * 16, 128) + 128;
+  const size_t budget = (size_t)env->smem_optin - 1024;
+  int use_smem = 1;
+  size_t map_bytes = align_up(d.map_bytes, 128);
+  int warps;
+  if (map_bytes + fixed + 8 * warp_bytes <= budget) {
+    warps = (int)std::min<size_t>(kMaxWarps, (budget - fixed - map_bytes) / warp_bytes);
+  } else {
+    use_smem = 0;  // map does not fit next to the warp scratch: read tables via L1/L2
+    map_bytes = 0;
+    warps = (int)std::min<size_t>(kMaxWarps, (budget - fixed) / warp_bytes);
+  }
+  warps = std::max(warps, 1);
+  int g = (int)std::min<int64_t>(env->n_sm, std::max<int64_t>(1, (lanes + 31) / 32));
+  int64_t per_cta = (lanes + g - 1) / g;
+  int e = (int)std::max<int64_t>(1, std::min<int64_t>(env->E_cap, (per_cta + warps - 1) / warps));
+  // shrink the CTA if fewer warps than available would do
+  int need_warps = (int)std::max<int64_t>(1, std::min<int64_t>(warps, (per_cta + e - 1) / e));
+  *grid = g;
+  *threads = need_warps * 32;
+  *E = e;
+  *smem = map_bytes + fixed + (size_t)need_warps * warp_bytes;
+  *smem_maps = use_smem;
+}
+
+static void set_geometry(SpEnv* env, EnvDev& d, size_t smem, int smem_maps, int E) {
+  const size_t map_region = smem_maps ? align_up(d.map_bytes, 128) : 0;
+  d.off_beam = (uint32_t)map_region;
+  d.off_bar = (uint32_t)(map_region + align_up((size_t)d.R * 16, 128));
+  d.off_warps = d.off_bar + 128;
+  d.warp_smem = (uint32_t)align_up(1792 + (size_t)env->E_cap * d.D * 4, 16);
+  d.smem_maps = smem_maps;
+  d.E = E;
+  (void)smem;
+}
+
+template <class T>
+static int d2h_slots(SpEnv* env, const T* dev, std::vector<T>& host, cudaStream_t st) {
+  host.resize(env->n);
+  SP_CUDA(cudaMemcpyAsync(host.data(), dev, sizeof(T) * env->n, cudaMemcpyDeviceToHost, st));
+  return SP_OK;
+}
+
+extern "C" {
+
+const char* sp_last_error(void) { return g_err.c_str(); }
+int sp_version(void) { return 1; }
+
+int sp_device_info(int device, int* n_sm, int* smem_optin, int* major, int* minor) {
+  cudaDeviceProp p;
+  SP_CUDA(cudaGetDeviceProperties(&p, device));
+  if (n_sm) *n_sm = p.multiProcessorCount;
+  if (smem_optin) *smem_optin = (int)p.sharedMemPerBlockOptin;
+  if (major) *major = p.major;
+  if (minor) *minor = p.minor;
+  return SP_OK;
+}
+
+int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, int64_t n_envs,
+                  const int32_t* map_index, const SpRanges* ranges, int64_t n_ranges,
+                  int64_t env_id_offset, int device, SpEnv** out) {
+  if (!cfg || !maps || !out || n_maps < 1) return fail(SP_EINVAL, "null argument");
+  if (n_envs < 1) return fail(SP_EINVAL, "need at least one copy");  // vecenv.py:66-67
+  if (cfg->n_beams < 1) return fail(SP_EINVAL, "n_beams must be >= 1");
+  if (cfg->n_actions < 1 || cfg->n_actions > SP_MAX_ACTIONS)
+    return fail(SP_EINVAL, "action table must have 1..15 entries");
+  if (n_ranges != 1 && n_ranges != n_envs)
+    return fail(SP_EINVAL, "need one DiversityRanges per lane");  // core.py:56-57
+  const int H = maps[0].n_rows, W = maps[0].n_cols;
+  const double cell = maps[0].cell_cm;
+  for (int m = 0; m < n_maps; ++m)
+    if (maps[m].n_rows != H || maps[m].n_cols != W || maps[m].cell_cm != cell)
+      return fail(SP_EMAP, "all maps in one batch must share grid shape and cell size");
+  if (H < 1 || W < 1 || H > (1 << 15) || W > (1 << 15)) return fail(SP_EINVAL, "bad grid shape");
+  for (int64_t i = 0; map_index && i < n_envs; ++i)
+    if (map_index[i] < 0 || map_index[i] >= n_maps)
+      return fail(SP_EINVAL, "map_index out of range");  // core.py:58-59
+  for (int64_t r = 0; r < n_ranges; ++r)
+    if (ranges[r].delay[0] < 0 || ranges[r].delay[1] > SP_MAX_DELAY ||
+        ranges[r].delay[0] > ranges[r].delay[1])
+      return fail(SP_EINVAL, "control delay range must lie in [0, 64]");
+
+  DevDeviceGuard guard(device);
+  SpEnv* env = new SpEnv();
+  env->device = device;
+  env->n = n_envs;
+  env->R = cfg->n_beams;
+  env->D = 5 + cfg->n_beams;
+  env->n_maps = n_maps;
+  env->auto_reset = cfg->auto_reset != 0;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+    delete env;
+    return fail(SP_ECUDA, "cudaGetDeviceProperties failed");
+  }
+  env->n_sm = prop.multiProcessorCount;
+  env->smem_optin = (int)prop.sharedMemPerBlockOptin;
+  env->E_cap = (int)std::max(1, std::min(32, 1024 / cfg->n_beams));
+
+  EnvDev& d = env->d;
+  d.n = n_envs;
+  d.R = env->R;
+  d.D = env->D;
+  d.H = H;
+  d.W = W;
+  d.Hb = (H + 1) / 2;
+  d.Wb = (W + 1) / 2;
+  d.WW = (W + 31) / 32;
+  d.n_maps = n_maps;
+  d.cell = cell;
+  d.inv_cell = 1.0 / cell;
+  d.max_range = cfg->max_range_cm;
+  d.radius = cfg->robot_radius_cm;
+  d.proximity = cfg->proximity_cm;
+  d.timeout = cfg->timeout_steps;
+  d.spawn_attempts = cfg->spawn_attempts;
+  d.auto_reset = cfg->auto_reset ? 1 : 0;
+  d.n_actions = cfg->n_actions;
+  {
+    const int K = (int)std::ceil(cfg->robot_radius_cm / cell);
+    d.need_r = (K + 1) / 2;
+  }
+  for (int c = 0; c <= SP_MAX_ACTIONS; ++c) {
+    d.action_v[c] = c < cfg->n_actions ? cfg->action_table[2 * c] : 0.0;
+    d.action_w[c] = c < cfg->n_actions ? cfg->action_table[2 * c + 1] : 0.0;
+  }
+  d.action_v[SP_MAX_ACTIONS] = 0.0;  // the (0, 0) delay filler (core.py:156)
+  d.action_w[SP_MAX_ACTIONS] = 0.0;
+  d.blk_bytes = (uint32_t)align_up((size_t)d.Hb * d.Wb, 16);
+  d.bits_bytes = (uint32_t)align_up((size_t)H * d.WW * 4, 16);
+  d.map_bytes = d.blk_bytes + d.bits_bytes;
+  d.env_id_offset = env_id_offset;
+
+  // slot order: stable sort by map (map-major)
+  std::vector<int32_t> midx(n_envs);
+  for (int64_t i = 0; i < n_envs; ++i)
+    midx[i] = map_index ? map_index[i] : (int32_t)((env_id_offset + i) % n_maps);
+  env->map_off.assign(n_maps + 1, 0);
+  for (int64_t i = 0; i < n_envs; ++i) env->map_off[midx[i] + 1]++;
+  for (int m = 0; m < n_maps; ++m) env->map_off[m + 1] += env->map_off[m];
+  env->env_of_slot.resize(n_envs);
+  env->slot_of_env.resize(n_envs);
+  {
+    std::vector<int64_t> fillp(env->map_off.begin(), env->map_off.end() - 1);
+    for (int64_t i = 0; i < n_envs; ++i) {
+      int64_t s = fillp[midx[i]]++;
+      env->env_of_slot[s] = i;
+      env->slot_of_env[i] = s;
+    }
+  }
+
+  // map tables + constants
+  std::vector<uint8_t> host_maps((size_t)n_maps * d.map_bytes, 0);
+  std::vector<MapConst> mconst(n_maps);
+  for (int m = 0; m < n_maps; ++m) {
+    uint8_t* base = host_maps.data() + (size_t)m * d.map_bytes;
+    build_block_table(maps[m].occupancy, H, W, d.Hb, d.Wb, base);
+    uint32_t* bits = (uint32_t*)(base + d.blk_bytes);
+    for (int iy = 0; iy < H; ++iy)
+      for (int ix = 0; ix < W; ++ix)
+        if (maps[m].occupancy[(size_t)iy * W + ix]) bits[(size_t)iy * d.WW + (ix >> 5)] |= 1u << (ix & 31);
+    mconst[m].goal_x = maps[m].goal_x;
+    mconst[m].goal_y = maps[m].goal_y;
+    mconst[m].goal_r = maps[m].goal_radius;
+    mconst[m].plan_dist = maps[m].planning_dist;
+    for (int k = 0; k < 4; ++k) mconst[m].spawn[k] = maps[m].spawn[k];
+  }
+  std::vector<double2> beam(env->R);
+  for (int j = 0; j < env->R; ++j) beam[j] = make_double2(std::cos(cfg->beam_offsets[j]), std::sin(cfg->beam_offsets[j]));
+  std::vector<double> rng_rows((size_t)(n_ranges == 1 ? 1 : n_envs) * 12);
+  for (int64_t s = 0; s < (n_ranges == 1 ? 1 : n_envs); ++s) {
+    const SpRanges& r = ranges[n_ranges == 1 ? 0 : env->env_of_slot[s]];
+    double* o = rng_rows.data() + 12 * s;
+    o[0] = r.k[0]; o[1] = r.k[1]; o[2] = r.dt[0]; o[3] = r.dt[1];
+    o[4] = r.delay[0]; o[5] = r.delay[1]; o[6] = r.vmax_linear[0]; o[7] = r.vmax_linear[1];
+    o[8] = r.vmax_angular[0]; o[9] = r.vmax_angular[1]; o[10] = r.noise_std[0]; o[11] = r.noise_std[1];
+  }
+  d.ranges_shared = n_ranges == 1;
+
+  int rc = SP_OK;
+  uint8_t* dmaps; MapConst* dmc; int64_t* dmoff; double2* dbeam; double* drng; int64_t* deos;
+#define TRY(x) do { rc = (x); if (rc) { delete env; return rc; } } while (0)
+  TRY(env->alloc(&dmaps, host_maps.size()));
+  TRY(env->alloc(&dmc, n_maps));
+  TRY(env->alloc(&dmoff, n_maps + 1));
+  TRY(env->alloc(&dbeam, env->R));
+  TRY(env->alloc(&drng, rng_rows.size()));
+  TRY(env->alloc(&deos, n_envs));
+  const size_t n = (size_t)n_envs;
+  double** f64s[] = {&d.x, &d.y, &d.h, &d.vl, &d.va, &d.ret, &d.sx, &d.sy, &d.c0, &d.s0,
+                     &d.pk, &d.pdt, &d.pvl, &d.pva, &d.psig, &d.return_sum, &d.first_ret};
+  for (double** p : f64s) TRY(env->alloc(p, n));
+  TRY(env->alloc(&d.hist, 4 * n, 0xff));
+  TRY(env->alloc(&d.ctr, n));
+  TRY(env->alloc(&d.step, n));
+  TRY(env->alloc(&d.delay, n));
+  TRY(env->alloc(&d.needs_reset, n, 1));
+  TRY(env->alloc(&d.episodes, n));
+  TRY(env->alloc(&d.arrivals, n));
+  TRY(env->alloc(&d.first_event, n, 0xff));
+  TRY(env->alloc(&d.first_steps, n));
+  d.rec_cap = (uint64_t)align_up(n + 256, 256);
+  TRY(env->alloc(&d.rec_ret, d.rec_cap));
+  TRY(env->alloc(&d.rec_key, d.rec_cap));
+  TRY(env->alloc(&d.rec_count, 1));
+  TRY(env->alloc(&d.err, 4));
+#undef TRY
+  if (cudaMallocHost(&env->h_err, 16) != cudaSuccess) { delete env; return fail(SP_ENOMEM, "pinned alloc"); }
+  cudaMemcpy(dmaps, host_maps.data(), host_maps.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(dmc, mconst.data(), sizeof(MapConst) * n_maps, cudaMemcpyHostToDevice);
+  cudaMemcpy(dmoff, env->map_off.data(), sizeof(int64_t) * (n_maps + 1), cudaMemcpyHostToDevice);
+  cudaMemcpy(dbeam, beam.data(), sizeof(double2) * env->R, cudaMemcpyHostToDevice);
+  cudaMemcpy(drng, rng_rows.data(), sizeof(double) * rng_rows.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(deos, env->env_of_slot.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice);
+  d.maps = dmaps;
+  d.mconst = dmc;
+  d.map_off = dmoff;
+  d.beam_cs = dbeam;
+  d.ranges = drng;
+  d.env_of_slot = deos;
+
+  int E, smem_maps;
+  plan_launch(env, n_envs, &env->grid, &env->threads, &E, &env->smem, &smem_maps);
+  set_geometry(env, d, env->smem, smem_maps, E);
+  cudaError_t e1 = cudaFuncSetAttribute(env_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        env->smem_optin);
+  cudaError_t e2 = cudaFuncSetAttribute(env_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        env->smem_optin);
+  cudaError_t e3 = cudaDeviceSynchronize();
+  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
+    delete env;
+    return fail(SP_ECUDA, std::string("env setup: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : (e2 != cudaSuccess ? e2 : e3)));
+  }
+  *out = env;
+  return SP_OK;
+}
+
+int sp_env_destroy(SpEnv* env) {
+  if (!env) return SP_OK;
+  DevDeviceGuard guard(env->device);
+  cudaDeviceSynchronize();
+  delete env;
+  return SP_OK;
+}
+
+static int launch_env(SpEnv* env, const StepArgs& a, cudaStream_t st) {
+  env_step_kernel<<<env->grid, env->threads, env->smem, st>>>(env->d, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(SP_ECUDA, std::string("env_step_kernel: ") + cudaGetErrorString(e));
+  return SP_OK;
+}
+
+int sp_env_reset_all(SpEnv* env, uint64_t seed, float* states, void* stream) {
+  if (!env || !states) return fail(SP_EINVAL, "null argument");
+  DevDeviceGuard guard(env->device);
+  std::lock_guard<std::mutex> lk(env->mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  env->d.seed = seed;
+  env->step_index = 0;
+  SP_CUDA(cudaMemsetAsync(env->d.ctr, 0, sizeof(uint64_t) * env->n, st));
+  SP_CUDA(cudaMemsetAsync(env->d.err, 0, 16, st));
+  StepArgs a{};
+  a.mode = MODE_RESET_ALL;
+  a.states = states;
+  return launch_env(env, a, st);
+}
+
+int sp_env_step(SpEnv* env, const int64_t* actions, float* states, float* store_states,
+                double* rewards, uint8_t* dones, uint8_t* truncated, int8_t* events,
+                void* stream) {
+  if (!env || !actions || !states || !store_states || !rewards || !dones || !truncated || !events)
+    return fail(SP_EINVAL, "null argument");
+  DevDeviceGuard guard(env->device);
+  std::lock_guard<std::mutex> lk(env->mu);
+  StepArgs a{};
+  a.mode = MODE_STEP;
+  a.step_index = ++env->step_index;
+  a.actions = actions;
+  a.states = states;
+  a.store_states = store_states;
+  a.rewards = rewards;
+  a.dones = dones;
+  a.truncated = truncated;
+  a.events = events;
+  return launch_env(env, a, (cudaStream_t)stream);
+}
+
+int sp_env_check(SpEnv* env, void* stream, int64_t* err_env) {
+  if (!env) return fail(SP_EINVAL, "null argument");
+  DevDeviceGuard guard(env->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  SP_CUDA(cudaMemcpyAsync(env->h_err, env->d.err, 8, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  if (err_env) *err_env = env->h_err[1];
+  int code = env->h_err[0];
+  if (code != SP_OK) {
+    cudaMemsetAsync(env->d.err, 0, 16, st);
+    cudaStreamSynchronize(st);
+    const char* what = code == SP_EACTION ? "action index out of range"
+                       : code == SP_EEPISODE ? "a lane finished its episode; reset before stepping"
+                       : code == SP_EMAP ? "no collision-free spawn pose found"
+                                         : "device error";
+    return fail(code, std::string(what) + " (env " + std::to_string(env->h_err[1]) + ")");
+  }
+  return SP_OK;
+}
+
+int sp_env_any_needs_reset(SpEnv* env, void* stream, int* any) {
+  if (!env || !any) return fail(SP_EINVAL, "null argument");
+  DevDeviceGuard guard(env->device);
+  std::vector<uint8_t> h(env->n);
+  cudaStream_t st = (cudaStream_t)stream;
+  SP_CUDA(cudaMemcpyAsync(h.data(), env->d.needs_reset, env->n, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  *any = 0;
+  for (int64_t s = 0; s < env->n; ++s)
+    if (h[s]) { *any = 1; break; }
+  return SP_OK;
+}
+
+int sp_env_stats_read(SpEnv* env, int64_t* episodes, int64_t* arrivals, double* return_sum,
+                      int8_t* first_event, double* first_return, int64_t* first_steps,
+                      void* stream) {
+  if (!env) return fail(SP_EINVAL, "null argument");
+  DevDeviceGuard guard(env->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<int64_t> e, a;
+  std::vector<double> r, fr;
+  std::vector<int8_t> fe;
+  std::vector<int32_t> fs;
+  int rc;
+  if ((rc = d2h_slots(env, env->d.episodes, e, st)) || (rc = d2h_slots(env, env->d.arrivals, a, st)) ||
+      (rc = d2h_slots(env, env->d.return_sum, r, st)) || (rc = d2h_slots(env, env->d.first_event, fe, st)) ||
+      (rc = d2h_slots(env, env->d.first_ret, fr, st)) || (rc = d2h_slots(env, env->d.first_steps, fs, st)))
+    return rc;
+  SP_CUDA(cudaStreamSynchronize(st));
+  for (int64_t i = 0; i < env->n; ++i) {
+    const int64_t s = env->slot_of_env[i];
+    if (episodes) episodes[i] = e[s];
+    if (arrivals) arrivals[i] = a[s];
+    if (return_sum) return_sum[i] = r[s];
+    if (first_event) first_event[i] = fe[s];
+    if (first_return) first_return[i] = fr[s];
+    if (first_steps) first_steps[i] = fs[s];
+  }
+  return SP_OK;
+}
+
+int sp_env_recent_returns(SpEnv* env, double* out256, int32_t* n_out, void* stream) {
+  if (!env || !out256 || !n_out) return fail(SP_EINVAL, "null argument");
+  DevDeviceGuard guard(env->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long count = 0;
+  SP_CUDA(cudaMemcpyAsync(&count, env->d.rec_count, 8, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  const uint64_t cap = env->d.rec_cap;
+  const uint64_t valid = std::min<uint64_t>(count, cap);
+  std::vector<double> ret(cap);
+  std::vector<uint64_t> key(cap);
+  SP_CUDA(cudaMemcpyAsync(ret.data(), env->d.rec_ret, 8 * cap, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaMemcpyAsync(key.data(), env->d.rec_key, 8 * cap, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  // entries written in the last `valid` reservations; order by (step, env)
+  std::vector<std::pair<uint64_t, double>> items;
+  items.reserve(valid);
+  for (uint64_t k = count - valid; k < count; ++k) items.emplace_back(key[k % cap], ret[k % cap]);
+  std::sort(items.begin(), items.end(),
+            [](const std::pair<uint64_t, double>& x, const std::pair<uint64_t, double>& y) {
+              return x.first < y.first;
+            });
+  const size_t take = std::min<size_t>(256, items.size());
+  for (size_t i = 0; i < take; ++i) out256[i] = items[items.size() - take + i].second;
+  *n_out = (int32_t)take;
+  return SP_OK;
+}
+
+int sp_env_stats_reset(SpEnv* env, int clear_recent, void* stream) {
+  if (!env) return fail(SP_EINVAL, "null argument");
+  DevDeviceGuard guard(env->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  SP_CUDA(cudaMemsetAsync(env->d.episodes, 0, 8 * env->n, st));
+  SP_CUDA(cudaMemsetAsync(env->d.arrivals, 0, 8 * env->n, st));
+  SP_CUDA(cudaMemsetAsync(env->d.return_sum, 0, 8 * env->n, st));
+  if (clear_recent) SP_CUDA(cudaMemsetAsync(env->d.rec_count, 0, 8, st));
+  return SP_OK;
+}
+
+int sp_env_stats_totals(SpEnv* env, double* dev_out3, void* stream) {
+  if (!env || !dev_out3) return fail(SP_EINVAL, "null argument");
+  DevDeviceGuard guard(env->device);
+  stats_totals_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(env->d.episodes, env->d.arrivals,
+                                                           env->d.return_sum, env->n, dev_out3);
+  SP_CUDA(cudaGetLastError());
+  return SP_OK;
+}
+
+int sp_env_read_state(SpEnv* env, int field, double* host_out, void* stream) {
+  if (!env || !host_out) return fail(SP_EINVAL, "null argument");
+  DevDeviceGuard guard(env->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const EnvDev& d = env->d;
+  std::vector<double> tmp(env->n);
+  const double* f64 = nullptr;
+  switch (field) {
+    case 0: f64 = d.x; break;
+    case 1: f64 = d.y; break;
+    case 2: f64 = d.h; break;
+    case 3: f64 = d.vl; break;
+    case 4: f64 = d.va; break;
+    case 5: f64 = d.sx; break;
+    case 6: f64 = d.sy; break;
+    case 7: f64 = d.pk; break;
+    case 8: f64 = d.pdt; break;
+    case 10: f64 = d.pvl; break;
+    case 11: f64 = d.pva; break;
+    case 12: f64 = d.psig; break;
+    case 16: f64 = d.ret; break;
+    default: break;
+  }
+  if (f64) {
+    SP_CUDA(cudaMemcpyAsync(tmp.data(), f64, 8 * env->n, cudaMemcpyDeviceToHost, st));
+  } else if (field == 9 || field == 13) {
+    std::vector<int32_t> v(env->n);
+    SP_CUDA(cudaMemcpyAsync(v.data(), field == 9 ? d.delay : d.step, 4 * env->n, cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaStreamSynchronize(st));
+    for (int64_t s = 0; s < env->n; ++s) tmp[s] = v[s];
+  } else if (field == 14) {
+    std::vector<uint8_t> v(env->n);
+    SP_CUDA(cudaMemcpyAsync(v.data(), d.needs_reset, env->n, cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaStreamSynchronize(st));
+    for (int64_t s = 0; s < env->n; ++s) tmp[s] = v[s];
+  } else if (field == 15) {
+    std::vector<uint64_t> v(env->n);
+    SP_CUDA(cudaMemcpyAsync(v.data(), d.ctr, 8 * env->n, cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaStreamSynchronize(st));
+    for (int64_t s = 0; s < env->n; ++s) tmp[s] = (double)v[s];
+  } else {
+    return fail(SP_EINVAL, "unknown state field");
+  }
+  SP_CUDA(cudaStreamSynchronize(st));
+  for (int64_t i = 0; i < env->n; ++i) host_out[i] = tmp[env->slot_of_env[i]];
+  return SP_OK;
+}
+
+int sp_env_map_info(SpEnv* env, int64_t* slot_of_env, int64_t* smem_bytes, int32_t* threads,
+                    int32_t* ctas) {
+  if (!env) return fail(SP_EINVAL, "null argument");
+  if (slot_of_env) std::memcpy(slot_of_env, env->slot_of_env.data(), 8 * env->n);
+  if (smem_bytes) *smem_bytes = (int64_t)env->smem;
+  if (threads) *threads = env->threads;
+  if (ctas) *ctas = env->grid;
+  return SP_OK;
+}
+
+int sp_env_scan(SpEnv* env, int64_t n, const int64_t* query_offsets, const double* x,
+                const double* y, const double* heading, double* ranges, int32_t* hit_cell,
+                void* stream) {
+  if (!env || !query_offsets || !x || !y || !heading || !ranges) return fail(SP_EINVAL, "null argument");
+  if (n < 1) return SP_OK;
+  if (query_offsets[0] != 0 || query_offsets[env->n_maps] != n)
+    return fail(SP_EINVAL, "query_offsets must span [0, n)");
+  DevDeviceGuard guard(env->device);
+  std::lock_guard<std::mutex> lk(env->mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t* dq = nullptr;
+  SP_CUDA(cudaMallocAsync((void**)&dq, 8 * (env->n_maps + 1), st));
+  SP_CUDA(cudaMemcpyAsync(dq, query_offsets, 8 * (env->n_maps + 1), cudaMemcpyHostToDevice, st));
+  int grid, threads, E, smem_maps;
+  size_t smem;
+  plan_launch(env, n, &grid, &threads, &E, &smem, &smem_maps);
+  EnvDev d = env->d;
+  set_geometry(env, d, smem, smem_maps, E);
+  ScanArgs q{n, dq, x, y, heading, ranges, hit_cell};
+  env_scan_kernel<<<grid, threads, smem, st>>>(d, q);
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(dq, st);
+  if (e != cudaSuccess) return fail(SP_ECUDA, std::string("env_scan_kernel: ") + cudaGetErrorString(e));
+  return SP_OK;
+}
+
+// ------------------------------------------------------------- op seam ----
+static int grid_for(int64_t n, int block) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + block - 1) / block, 148 * 16));
+}
+
+int sp_cast_rays(const uint8_t* occ, const double* edt, int64_t n_maps, int64_t height,
+                 int64_t width, const int64_t* map_idx, const double* px, const double* py,
+                 const double* dirx, const double* diry, int64_t n, double cell, double max_range,
+                 double* out, void* stream) {
+  if (n < 1) return SP_OK;
+  if (!occ || !edt || !map_idx || !px || !py || !dirx || !diry || !out || n_maps < 1)
+    return fail(SP_EINVAL, "null argument");
+  cast_rays_exact_kernel<<<grid_for(n, 128), 128, 0, (cudaStream_t)stream>>>(
+      occ, edt, height, width, map_idx, px, py, dirx, diry, n, cell, max_range, out);
+  SP_CUDA(cudaGetLastError());
+  return SP_OK;
+}
+
+int sp_disc_collides(const uint8_t* occ, int64_t n_maps, int64_t height, int64_t width,
+                     const int64_t* map_idx, const double* px, const double* py,
+                     const double* radius, int64_t n, double cell, uint8_t* out, void* stream) {
+  if (n < 1) return SP_OK;
+  if (!occ || !map_idx || !px || !py || !radius || !out || n_maps < 1)
+    return fail(SP_EINVAL, "null argument");
+  disc_collides_kernel<<<grid_for(n, 128), 128, 0, (cudaStream_t)stream>>>(
+      occ, height, width, map_idx, px, py, radius, n, cell, out);
+  SP_CUDA(cudaGetLastError());
+  return SP_OK;
+}
+
+// -------------------------------------------------------------- replay -----
+int sp_rb_create(int64_t capacity, int32_t state_dim, int device, SpReplay** out) {
+  if (capacity < 1) return fail(SP_EINVAL, "capacity must be positive");  // replay.py:33-34
+  if (state_dim < 1 || !out) return fail(SP_EINVAL, "bad state_dim");
+  DevDeviceGuard guard(device);
+  SpReplay* rb = new SpReplay();
+  rb->device = device;
+  rb->cap = capacity;
+  rb->dim = state_dim;
+  const size_t rows = (size_t)capacity;
+  if (cudaMalloc(&rb->s, rows * state_dim * 4) != cudaSuccess ||
+      cudaMalloc(&rb->s2, rows * state_dim * 4) != cudaSuccess ||
+      cudaMalloc(&rb->r, rows * 4) != cudaSuccess || cudaMalloc(&rb->a, rows * 8) != cudaSuccess ||
+      cudaMalloc(&rb->dn, rows) != cudaSuccess) {
+    delete rb;
+    return fail(SP_ENOMEM, "replay allocation failed");
+  }
+  cudaMemset(rb->s, 0, rows * state_dim * 4);
+  cudaMemset(rb->s2, 0, rows * state_dim * 4);
+  cudaMemset(rb->r, 0, rows * 4);
+  cudaMemset(rb->a, 0, rows * 8);
+  cudaMemset(rb->dn, 0, rows);
+  cudaDeviceSynchronize();
+  *out = rb;
+  return SP_OK;
+}
+
+int sp_rb_destroy(SpReplay* rb) {
+  if (!rb) return SP_OK;
+  DevDeviceGuard guard(rb->device);
+  cudaDeviceSynchronize();
+  delete rb;
+  return SP_OK;
+}
+
+int sp_rb_append(SpReplay* rb, const float* states, const int64_t* actions, const void* rewards,
+                 int reward_is_f64, const float* next_states, const uint8_t* dones, int64_t n,
+                 void* stream) {
+  if (!rb) return fail(SP_EINVAL, "null argument");
+  if (n > rb->cap)
+    return fail(SP_EINVAL, "batch of " + std::to_string(n) + " exceeds capacity " + std::to_string(rb->cap));
+  if (n < 1) return SP_OK;
+  if (!states || !actions || !rewards || !next_states || !dones) return fail(SP_EINVAL, "null argument");
+  DevDeviceGuard guard(rb->device);
+  std::lock_guard<std::mutex> lk(rb->mu);
+  const int64_t flat = n * rb->dim;
+  rb_append_kernel<<<grid_for(flat, 256), 256, 0, (cudaStream_t)stream>>>(
+      rb->s, rb->a, rb->r, rb->s2, rb->dn, rb->cap, rb->dim, rb->cursor, states, actions, rewards,
+      reward_is_f64, next_states, dones, n);
+  SP_CUDA(cudaGetLastError());
+  rb->cursor = (rb->cursor + n) % rb->cap;  // replay.py:66-67
+  rb->size = std::min(rb->size + n, rb->cap);
+  return SP_OK;
+}
+
+int sp_rb_sample(SpReplay* rb, int64_t batch, uint64_t seed, uint32_t stream_id, uint64_t ctr,
+                 float* states, int64_t* actions, float* rewards, float* next_states,
+                 uint8_t* dones, int64_t* idx_out, void* stream) {
+  if (!rb) return fail(SP_EINVAL, "null argument");
+  DevDeviceGuard guard(rb->device);
+  std::lock_guard<std::mutex> lk(rb->mu);
+  if (rb->size < batch)  // replay.py:73-75
+    return fail(SP_ENOTREADY, "buffer holds " + std::to_string(rb->size) + " transitions, need " +
+                                  std::to_string(batch));
+  if (batch < 1) return SP_OK;
+  if (!states || !actions || !rewards || !next_states || !dones) return fail(SP_EINVAL, "null argument");
+  const int blocks = (int)((batch + 255) / 256);
+  rb_sample_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+      rb->s, rb->a, rb->r, rb->s2, rb->dn, rb->dim, rb->size, batch, seed, stream_id, ctr, states,
+      actions, rewards, next_states, dones, idx_out);
+  SP_CUDA(cudaGetLastError());
+  return SP_OK;
+}
+
+int sp_rb_size(SpReplay* rb, int64_t* size, int64_t* cursor) {
+  if (!rb) return fail(SP_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(rb->mu);
+  if (size) *size = rb->size;
+  if (cursor) *cursor = rb->cursor;
+  return SP_OK;
+}
+
+int sp_rb_gather(SpReplay* rb, float* states, int64_t* actions, float* rewards, float* next_states,
+                 uint8_t* dones, void* stream) {
+  if (!rb) return fail(SP_EINVAL, "null argument");
+  DevDeviceGuard guard(rb->device);
+  std::lock_guard<std::mutex> lk(rb->mu);
+  if (rb->size < 1) return SP_OK;
+  const int64_t flat = rb->size * rb->dim;
+  rb_gather_kernel<<<grid_for(flat, 256), 256, 0, (cudaStream_t)stream>>>(
+      rb->s, rb->a, rb->r, rb->s2, rb->dn, rb->dim, rb->size, states, actions, rewards,
+      next_states, dones);
+  SP_CUDA(cudaGetLastError());
+  return SP_OK;
+}
+
+int sp_random_actions(int64_t n, uint64_t seed, int64_t env_id0, int64_t step, int32_t n_actions,
+                      int64_t* actions, void* stream) {
+  if (n < 1) return SP_OK;
+  if (!actions || n_actions < 1) return fail(SP_EINVAL, "bad arguments");
+  random_actions_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(n, seed, env_id0, step,
+                                                                           n_actions, actions);
+  SP_CUDA(cudaGetLastError());
+  return SP_OK;
+}
+
+}  // extern "C"

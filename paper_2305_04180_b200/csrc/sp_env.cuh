@@ -1,0 +1,82 @@
+// sp_env.cuh -- device-side data layout of one Sparrow environment batch.
+#pragma once
+#include "sp_common.cuh"
+
+namespace sp {
+
+// Per-map constants (gridmap.py GridMap fields used by core.py:81-86, 133).
+struct MapConst {
+  double goal_x, goal_y, goal_r, plan_dist;
+  double spawn[4];
+};
+
+// Everything the step kernel reads, by value (kernel parameter).
+struct EnvDev {
+  int64_t n;              // lanes (slots)
+  int32_t R, D;           // beams, obs dim = 5 + R
+  int32_t H, W, Hb, Wb, WW;  // grid, 2x2-block grid, 32-bit words per bitmap row
+  int32_t n_maps;
+  double cell, inv_cell, max_range, radius, proximity;
+  int32_t timeout, spawn_attempts, auto_reset, n_actions;
+  int32_t need_r;         // block-box radius that proves "no disc collision"
+  uint32_t blk_bytes;     // per-map block table bytes (16-byte padded)
+  uint32_t bits_bytes;    // per-map bitmap bytes
+  uint32_t map_bytes;     // blk_bytes + bits_bytes
+  double action_v[SP_MAX_ACTIONS + 1], action_w[SP_MAX_ACTIONS + 1];  // code 15 = (0, 0)
+  const uint8_t* maps;    // n_maps * map_bytes: [blk | bits]
+  const MapConst* mconst; // n_maps
+  const int64_t* map_off; // n_maps + 1 slot ranges (slots are map-major)
+  const double2* beam_cs; // R: (cos, sin) of LidarConfig.beam_offsets()
+  // SoA state, slot order (core.py:88-108)
+  double *x, *y, *h, *vl, *va, *ret;
+  double *sx, *sy, *c0, *s0, *pk, *pdt, *pvl, *pva, *psig;
+  uint64_t* hist;         // 4 words per lane: hist[w * n + s]; 4-bit action codes
+  uint64_t* ctr;          // Philox block counter per lane
+  int32_t *step, *delay;
+  uint8_t* needs_reset;
+  const double* ranges;   // 12 doubles per lane (or shared when ranges_shared)
+  int32_t ranges_shared;
+  const int64_t* env_of_slot;
+  int64_t env_id_offset;
+  uint64_t seed;
+  // per-copy stats (vecenv.py:33-41, 76-80), slot order
+  int64_t *episodes, *arrivals;
+  double* return_sum;
+  int8_t* first_event;
+  double* first_ret;
+  int32_t* first_steps;
+  double* rec_ret;        // recent-returns ring (vecenv.py:79)
+  uint64_t* rec_key;      // (step << 32) | env row, for deterministic ordering
+  unsigned long long* rec_count;
+  uint64_t rec_cap;
+  int32_t* err;           // [0] status, [1] env row
+  // launch geometry
+  int32_t E;              // lanes (envs) per warp batch, <= 32
+  uint32_t warp_smem;     // bytes of per-warp scratch
+  uint32_t off_beam, off_warps, off_bar;  // smem offsets
+  int32_t smem_maps;      // 1: tables staged in shared memory via TMA bulk copy
+};
+
+enum { MODE_STEP = 0, MODE_RESET_ALL = 1 };
+
+struct StepArgs {
+  int32_t mode;
+  uint64_t step_index;
+  const int64_t* actions;  // external order
+  float* states;           // (N, D) post-reset obs
+  float* store_states;     // (N, D) pre-reset s'
+  double* rewards;
+  uint8_t* dones;
+  uint8_t* truncated;
+  int8_t* events;
+};
+
+struct ScanArgs {
+  int64_t n;
+  const int64_t* qoff;          // n_maps + 1 query ranges (device copy)
+  const double *x, *y, *h;
+  double* ranges;
+  int32_t* hit_cell;
+};
+
+}  // namespace sp

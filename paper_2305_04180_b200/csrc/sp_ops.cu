@@ -1,0 +1,233 @@
+// sp_ops.cu -- op-level plugin kernels, the replay ring, benchmark helpers.
+//
+// * cast_rays_exact / disc_collides: the reference kernel seam
+//   (kernels/__init__.py:62-86) on device.  cast_rays_exact restates the
+//   reference algorithm itself (DDA + EDT jump, _cy.pyx:19-106) operation for
+//   operation in IEEE fp64 without contraction, so it is bit-identical to the
+//   Cython backend on any occupancy grid -- including grids without an
+//   occupied border, where the reference's jump may land outside the grid and
+//   report the landing distance.  Lane per ray; occ/edt read through L1/L2.
+// * Replay ring (replay.py:31-87): append = contiguous ring writes (the ring
+//   rows are contiguous, so a batch is one flat wrapped copy per column);
+//   sample = Philox index draw (replay.py:76) + row gather.
+#include "sp_common.cuh"
+
+namespace sp {
+
+__global__ void cast_rays_exact_kernel(const uint8_t* __restrict__ occ,
+                                       const double* __restrict__ edt, int64_t H, int64_t W,
+                                       const int64_t* __restrict__ map_idx,
+                                       const double* __restrict__ px,
+                                       const double* __restrict__ py,
+                                       const double* __restrict__ dirx,
+                                       const double* __restrict__ diry, int64_t n, double cell,
+                                       double max_range, double* __restrict__ out) {
+  const double INF = __longlong_as_double(0x7ff0000000000000ll);
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = map_idx[r];
+    const uint8_t* o = occ + m * H * W;
+    const double* e = edt + m * H * W;
+    const double x0 = px[r], y0 = py[r], dx = dirx[r], dy = diry[r];
+    int64_t ix = (int64_t)floor(ddiv(x0, cell));
+    int64_t iy = (int64_t)floor(ddiv(y0, cell));
+    if (ix < 0 || ix >= W || iy < 0 || iy >= H || o[iy * W + ix]) {  // :37-42
+      out[r] = 0.0;
+      continue;
+    }
+    const int64_t stepx = dx > 0 ? 1 : (dx < 0 ? -1 : 0);
+    const int64_t stepy = dy > 0 ? 1 : (dy < 0 ? -1 : 0);
+    const double tdx = dx != 0 ? ddiv(cell, fabs(dx)) : INF;
+    const double tdy = dy != 0 ? ddiv(cell, fabs(dy)) : INF;
+    double tmx = dx > 0 ? ddiv(dsub(dmul((double)(ix + 1), cell), x0), dx)
+                        : (dx < 0 ? ddiv(dsub(dmul((double)ix, cell), x0), dx) : INF);
+    double tmy = dy > 0 ? ddiv(dsub(dmul((double)(iy + 1), cell), y0), dy)
+                        : (dy < 0 ? ddiv(dsub(dmul((double)iy, cell), y0), dy) : INF);
+    double t = 0.0, res = max_range;
+    for (;;) {
+      const double clearance = e[iy * W + ix];
+      if (clearance > 2.5) {  // EDT jump, :62-88
+        const double tj = dadd(t, dmul(dsub(clearance, 1.5), cell));
+        const double qx = dadd(x0, dmul(tj, dx));
+        const double qy = dadd(y0, dmul(tj, dy));
+        ix = (int64_t)floor(ddiv(qx, cell));
+        iy = (int64_t)floor(ddiv(qy, cell));
+        tmx = dx > 0 ? dadd(ddiv(dsub(dmul((double)(ix + 1), cell), qx), dx), tj)
+                     : (dx < 0 ? dadd(ddiv(dsub(dmul((double)ix, cell), qx), dx), tj) : INF);
+        tmy = dy > 0 ? dadd(ddiv(dsub(dmul((double)(iy + 1), cell), qy), dy), tj)
+                     : (dy < 0 ? dadd(ddiv(dsub(dmul((double)iy, cell), qy), dy), tj) : INF);
+        t = tj;
+        if (t > max_range) { res = max_range; break; }
+        if (ix < 0 || ix >= W || iy < 0 || iy >= H) { res = t < max_range ? t : max_range; break; }
+        continue;
+      }
+      if (tmx <= tmy) {  // :89-96
+        t = tmx;
+        tmx = dadd(tmx, tdx);
+        ix += stepx;
+      } else {
+        t = tmy;
+        tmy = dadd(tmy, tdy);
+        iy += stepy;
+      }
+      if (t > max_range) { res = max_range; break; }
+      if (ix < 0 || ix >= W || iy < 0 || iy >= H) { res = t < max_range ? t : max_range; break; }
+      if (o[iy * W + ix]) { res = t < max_range ? t : max_range; break; }
+    }
+    out[r] = res;
+  }
+}
+
+__global__ void disc_collides_kernel(const uint8_t* __restrict__ occ, int64_t H, int64_t W,
+                                     const int64_t* __restrict__ map_idx,
+                                     const double* __restrict__ px, const double* __restrict__ py,
+                                     const double* __restrict__ radius, int64_t n, double cell,
+                                     uint8_t* __restrict__ out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const double x = px[k], y = py[k], r = radius[k];
+    if (x - r < 0.0 || y - r < 0.0 || x + r > (double)W * cell || y + r > (double)H * cell) {
+      out[k] = 1;  // :124-126
+      continue;
+    }
+    const uint8_t* o = occ + map_idx[k] * H * W;
+    int64_t ix0 = (int64_t)floor(ddiv(dsub(x, r), cell)); if (ix0 < 0) ix0 = 0;
+    int64_t ix1 = (int64_t)floor(ddiv(dadd(x, r), cell)); if (ix1 > W - 1) ix1 = W - 1;
+    int64_t iy0 = (int64_t)floor(ddiv(dsub(y, r), cell)); if (iy0 < 0) iy0 = 0;
+    int64_t iy1 = (int64_t)floor(ddiv(dadd(y, r), cell)); if (iy1 > H - 1) iy1 = H - 1;
+    const double r2 = dmul(r, r);
+    uint8_t hit = 0;
+    for (int64_t iy = iy0; iy <= iy1 && !hit; ++iy) {
+      for (int64_t ix = ix0; ix <= ix1; ++ix) {
+        if (!o[iy * W + ix]) continue;
+        double lo = dmul((double)ix, cell), hi = dadd(lo, cell);
+        double nx = x > lo ? x : lo;
+        if (nx > hi) nx = hi;
+        lo = dmul((double)iy, cell);
+        hi = dadd(lo, cell);
+        double ny = y > lo ? y : lo;
+        if (ny > hi) ny = hi;
+        const double ddx = dsub(x, nx), ddy = dsub(y, ny);
+        if (dadd(dmul(ddx, ddx), dmul(ddy, ddy)) <= r2) { hit = 1; break; }
+      }
+    }
+    out[k] = hit;
+  }
+}
+
+// ---------------------------------------------------------------- replay ---
+__global__ void rb_append_kernel(float* __restrict__ rs, int64_t* __restrict__ ra,
+                                 float* __restrict__ rr, float* __restrict__ rs2,
+                                 uint8_t* __restrict__ rd, int64_t cap, int32_t dim,
+                                 int64_t cursor, const float* __restrict__ s,
+                                 const int64_t* __restrict__ a, const void* __restrict__ r,
+                                 int r_f64, const float* __restrict__ s2,
+                                 const uint8_t* __restrict__ dn, int64_t n) {
+  const int64_t flat = n * dim, ring = cap * dim, base = cursor * dim;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < flat;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t dst = base + i;
+    if (dst >= ring) dst -= ring;
+    rs[dst] = s[i];
+    rs2[dst] = s2[i];
+    if (i < n) {
+      int64_t row = cursor + i;
+      if (row >= cap) row -= cap;
+      ra[row] = a[i];
+      rr[row] = r_f64 ? (float)((const double*)r)[i] : ((const float*)r)[i];  // replay.py:53
+      rd[row] = dn[i] ? 1 : 0;
+    }
+  }
+}
+
+__global__ void rb_sample_kernel(const float* __restrict__ rs, const int64_t* __restrict__ ra,
+                                 const float* __restrict__ rr, const float* __restrict__ rs2,
+                                 const uint8_t* __restrict__ rd, int32_t dim, int64_t size,
+                                 int64_t batch, uint64_t seed, uint32_t stream_id, uint64_t ctr,
+                                 float* __restrict__ s, int64_t* __restrict__ a,
+                                 float* __restrict__ r, float* __restrict__ s2,
+                                 uint8_t* __restrict__ dn, int64_t* __restrict__ idx_out) {
+  __shared__ int64_t idx[256];
+  const int64_t i0 = (int64_t)blockIdx.x * 256;
+  const int nb = (int)min((int64_t)256, batch - i0);
+  if ((int)threadIdx.x < nb) {
+    const int64_t i = i0 + threadIdx.x;
+    const Block4 b = stream_block(seed, stream_id, 2u, ctr + (uint64_t)i);
+    const int64_t k = draw_integer(b, 0, size);  // replay.py:76
+    idx[threadIdx.x] = k;
+    a[i] = ra[k];
+    r[i] = rr[k];
+    dn[i] = rd[k];
+    if (idx_out) idx_out[i] = k;
+  }
+  __syncthreads();
+  const int64_t flat = (int64_t)nb * dim;
+  for (int64_t f = threadIdx.x; f < flat; f += blockDim.x) {
+    const int64_t row = f / dim, c = f - row * dim;
+    const int64_t src = idx[row] * dim + c;
+    s[(i0 + row) * dim + c] = rs[src];
+    s2[(i0 + row) * dim + c] = rs2[src];
+  }
+}
+
+__global__ void rb_gather_kernel(const float* __restrict__ rs, const int64_t* __restrict__ ra,
+                                 const float* __restrict__ rr, const float* __restrict__ rs2,
+                                 const uint8_t* __restrict__ rd, int32_t dim, int64_t size,
+                                 float* __restrict__ s, int64_t* __restrict__ a,
+                                 float* __restrict__ r, float* __restrict__ s2,
+                                 uint8_t* __restrict__ dn) {
+  const int64_t flat = size * dim;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < flat;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    s[i] = rs[i];
+    s2[i] = rs2[i];
+    if (i < size) {
+      a[i] = ra[i];
+      r[i] = rr[i];
+      dn[i] = rd[i];
+    }
+  }
+}
+
+// --------------------------------------------------------------- bench ----
+__global__ void random_actions_kernel(int64_t n, uint64_t seed, int64_t env_id0, int64_t step,
+                                      int32_t n_actions, int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const Block4 b = stream_block(seed, (uint32_t)(env_id0 + i), 1u, (uint64_t)step);
+    out[i] = draw_integer(b, 0, n_actions);
+  }
+}
+
+// Deterministic single-CTA totals {episodes, arrivals, return_sum}.
+__global__ void stats_totals_kernel(const int64_t* __restrict__ eps,
+                                    const int64_t* __restrict__ arr,
+                                    const double* __restrict__ rsum, int64_t n,
+                                    double* __restrict__ out3) {
+  __shared__ double se[1024], sa[1024], sr[1024];
+  double e = 0, a = 0, r = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    e += (double)eps[i];
+    a += (double)arr[i];
+    r += rsum[i];
+  }
+  se[threadIdx.x] = e;
+  sa[threadIdx.x] = a;
+  sr[threadIdx.x] = r;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      se[threadIdx.x] += se[threadIdx.x + w];
+      sa[threadIdx.x] += sa[threadIdx.x + w];
+      sr[threadIdx.x] += sr[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out3[0] = se[0];
+    out3[1] = sa[0];
+    out3[2] = sr[0];
+  }
+}
+
+}  // namespace sp

@@ -1,0 +1,424 @@
+"""Drop-in ``VecEnv``: N lockstep Sparrow copies stepped by one CUDA launch.
+
+API of the reference ``color_rl.vecenv.VecEnv`` (``vecenv.py:61-145``):
+``reset_all(seed)``, ``step_batch(actions) -> StepBatch``,
+``snapshot_stats(reset)``, ``first_episode_outcomes()``,
+``all_first_episodes_done``, ``n_copies``, ``map_index``, ``sim``.
+
+Returned arrays are CUDA tensors (the paper's conversion-free data flow,
+``PAPER.md:237``) with the reference's dtypes: states/store_states float32
+``(N, 5+R)``, rewards float64, dones/truncated bool, events int8.  Each call
+returns fresh tensors.
+
+Randomness: lane i draws from the Philox stream (seed, env_id_offset + i)
+ instead of ``SeedSequence(seed).spawn(N)``; a
+shard of a larger run (``env_id_offset``) therefore reproduces exactly the
+lanes of a single-GPU run.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from typing import NamedTuple, Sequence
+
+import numpy as np
+
+from paper_2305_04180_b200 import _lib
+from paper_2305_04180_b200.sim import (
+    DiversityRanges,
+    EnvConfig,
+    Event,
+    EpisodeTerminated,
+    MapError,
+)
+
+
+class StepBatch(NamedTuple):  # vecenv.py:24-30
+    states: "torch.Tensor"        # (N, D) float32, post-reset rows for finished copies
+    rewards: "torch.Tensor"       # (N,) float64
+    dones: "torch.Tensor"         # (N,) bool; collision/arrival only
+    truncated: "torch.Tensor"     # (N,) bool; timeouts
+    store_states: "torch.Tensor"  # (N, D) float32; true s' rows
+    events: "torch.Tensor"        # (N,) int8 Event codes
+
+
+@dataclass
+class CopyStats:  # vecenv.py:33-41
+    episodes: int = 0
+    arrivals: int = 0
+    return_sum: float = 0.0
+
+    @property
+    def arrival_rate(self):
+        return self.arrivals / self.episodes if self.episodes else None
+
+
+@dataclass
+class StatsSnapshot:  # vecenv.py:44-58
+    per_copy: list
+    episodes: int
+    arrivals: int
+    return_sum: float
+    recent_returns: list = field(default_factory=list)
+
+    @property
+    def arrival_rate(self):
+        return self.arrivals / self.episodes if self.episodes else None
+
+    @property
+    def mean_return(self):
+        return self.return_sum / self.episodes if self.episodes else None
+
+
+def _map_desc(m, config) -> tuple:
+    occ = np.ascontiguousarray(np.asarray(m.occupancy, dtype=bool).astype(np.uint8))
+    desc = _lib.SpMapDesc()
+    desc.n_rows, desc.n_cols = occ.shape
+    desc.cell_cm = float(m.cell_size_cm)
+    desc.occupancy = occ.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
+    desc.goal_x, desc.goal_y = (float(v) for v in m.goal_center)
+    desc.goal_radius = float(m.goal_radius_cm)
+    for i, v in enumerate(m.spawn_region):
+        desc.spawn[i] = float(v)
+    pd = float(getattr(config, "max_planning_dist_cm", 0.0))
+    desc.planning_dist = pd if pd > 0 else math.hypot(m.width_cm, m.height_cm)
+    return desc, occ
+
+
+def _ranges_struct(r) -> "_lib.SpRanges":
+    s = _lib.SpRanges()
+    s.k[:] = [float(v) for v in r.k]
+    s.dt[:] = [float(v) for v in r.control_interval_s]
+    s.delay[:] = [int(v) for v in r.control_delay_steps]
+    s.vmax_linear[:] = [float(v) for v in r.v_linear_max_cm_s]
+    s.vmax_angular[:] = [float(v) for v in r.v_angular_max_rad_s]
+    s.noise_std[:] = [float(v) for v in r.lidar_noise_std_cm]
+    return s
+
+
+class SimView:
+    """Read-only view of the device SoA with the reference SimBatch attribute
+    names (``sim/core.py:81-108``).  Each attribute read copies to host."""
+
+    _FIELDS = {"x": 0, "y": 1, "heading": 2, "start_x": 5, "start_y": 6, "param_k": 7,
+               "param_dt": 8, "param_noise": 12, "rng_ctr": 15}
+
+    def __init__(self, env: "VecEnv"):
+        self._env = env
+        maps = env._maps
+        mi = env.map_index
+        self.goal_x = np.array([maps[i].goal_center[0] for i in mi])
+        self.goal_y = np.array([maps[i].goal_center[1] for i in mi])
+        self.goal_radius = np.array([maps[i].goal_radius_cm for i in mi])
+        self.planning_dist = np.array([env._plan_dist[i] for i in mi])
+        self.map_index = mi
+        self.n_lanes = env.n_copies
+        self.n_beams = env.n_beams
+        self.cell = float(maps[0].cell_size_cm)
+
+    def _read(self, field_id: int) -> np.ndarray:
+        return self._env._read_state(field_id)
+
+    def __getattr__(self, name):
+        fid = SimView._FIELDS.get(name)
+        if fid is None:
+            raise AttributeError(name)
+        return self._read(fid)
+
+    @property
+    def v(self) -> np.ndarray:
+        return np.stack([self._read(3), self._read(4)], axis=1)
+
+    @property
+    def param_vmax(self) -> np.ndarray:
+        return np.stack([self._read(10), self._read(11)], axis=1)
+
+    @property
+    def param_delay(self) -> np.ndarray:
+        return self._read(9).astype(np.int64)
+
+    @property
+    def step_count(self) -> np.ndarray:
+        return self._read(13).astype(np.int64)
+
+    @property
+    def needs_reset(self) -> np.ndarray:
+        return self._read(14).astype(bool)
+
+    @property
+    def episode_return(self) -> np.ndarray:
+        return self._read(16)
+
+
+class VecEnv:
+    def __init__(self, maps: Sequence, n_copies: int,
+                 ranges: DiversityRanges | Sequence[DiversityRanges] | None = None,
+                 config: EnvConfig | None = None, map_index: Sequence[int] | None = None,
+                 auto_reset: bool = True, kernel_backend=None, *, device=None,
+                 env_id_offset: int = 0, check_actions: bool = True):
+        if kernel_backend not in (None, "cuda", "auto", "active"):
+            raise ValueError(f"kernel backend {kernel_backend!r}: this build has only 'cuda'")
+        if n_copies < 1:
+            raise ValueError("need at least one copy")  # vecenv.py:66-67
+        import torch
+        self._torch = torch
+        self.device = _lib.require_cuda(device)
+        lib = _lib.load()
+        self._lib = lib
+        self.n_copies = int(n_copies)
+        self.auto_reset = bool(auto_reset)
+        self.check_actions = bool(check_actions)
+        self.config = config or EnvConfig()
+        self._maps = list(maps)
+        if not self._maps:
+            raise ValueError("need at least one map")
+        first = self._maps[0]
+        for m in self._maps:
+            if (np.asarray(m.occupancy).shape != np.asarray(first.occupancy).shape
+                    or m.cell_size_cm != first.cell_size_cm):
+                raise MapError("all maps in one batch must share grid shape and cell size")
+        if map_index is None:
+            map_index = [(env_id_offset + i) % len(self._maps) for i in range(self.n_copies)]
+        self.map_index = np.asarray(map_index, dtype=np.int64)
+        if self.map_index.shape != (self.n_copies,):
+            raise ValueError("need one map index per copy")
+        if self.map_index.min() < 0 or self.map_index.max() >= len(self._maps):
+            raise ValueError("map_index out of range")
+        if isinstance(ranges, (list, tuple)):
+            rl = list(ranges)
+            if len(rl) != self.n_copies:
+                raise ValueError("need one DiversityRanges per lane")
+        else:
+            rl = [ranges or DiversityRanges()]
+        lid = self.config.lidar
+        self.n_beams = int(lid.n_beams)
+        self.state_dim = 5 + self.n_beams
+        table = [tuple(p) for p in self.config.action_table]
+        self.n_actions = len(table)
+
+        cfg = _lib.SpConfig()
+        cfg.n_beams = self.n_beams
+        cfg.max_range_cm = float(lid.max_range_cm)
+        cfg.robot_radius_cm = float(self.config.robot_radius_cm)
+        cfg.timeout_steps = int(self.config.timeout_steps)
+        cfg.proximity_cm = float(self.config.obstacle_penalty_range_cm)
+        cfg.n_actions = self.n_actions
+        for i, (v, w) in enumerate(table):
+            cfg.action_table[2 * i] = float(v)
+            cfg.action_table[2 * i + 1] = float(w)
+        cfg.spawn_attempts = int(self.config.spawn_attempts)
+        cfg.auto_reset = 1 if self.auto_reset else 0
+        self._offsets = np.ascontiguousarray(lid.beam_offsets(), dtype=np.float64)
+        cfg.beam_offsets = self._offsets.ctypes.data_as(_lib.c_dp)
+
+        descs = (_lib.SpMapDesc * len(self._maps))()
+        keep = []
+        self._plan_dist = []
+        for i, m in enumerate(self._maps):
+            desc, occ = _map_desc(m, self.config)
+            descs[i] = desc
+            keep.append(occ)
+            self._plan_dist.append(desc.planning_dist)
+        rarr = (_lib.SpRanges * len(rl))(*[_ranges_struct(r) for r in rl])
+        midx = np.ascontiguousarray(self.map_index, dtype=np.int32)
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            rc = lib.sp_env_create(ctypes.byref(cfg), descs, len(self._maps), self.n_copies,
+                                   midx.ctypes.data_as(_lib.c_i32p), rarr, len(rl),
+                                   int(env_id_offset), self.device.index, ctypes.byref(handle))
+        _lib.check(rc, "sp_env_create")
+        self._h = handle
+        self.env_id_offset = int(env_id_offset)
+        self._sim = None
+        self._seeded = False
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                self._lib.sp_env_destroy(h)
+            except Exception:  # noqa: BLE001 (interpreter shutdown)
+                pass
+            self._h = None
+
+    # -- helpers --------------------------------------------------------------
+    def _stream(self) -> int:
+        return self._torch.cuda.current_stream(self.device).cuda_stream
+
+    def _read_state(self, field_id: int) -> np.ndarray:
+        out = np.empty(self.n_copies, dtype=np.float64)
+        _lib.check(self._lib.sp_env_read_state(self._h, field_id, out.ctypes.data_as(_lib.c_dp),
+                                               self._stream()), "read_state")
+        return out
+
+    def _actions_to_device(self, actions):
+        torch = self._torch
+        if isinstance(actions, torch.Tensor):
+            if actions.shape != (self.n_copies,):
+                raise ValueError(f"expected {self.n_copies} actions, got shape {tuple(actions.shape)}")
+            a = actions.to(device=self.device, dtype=torch.int64)
+            if self.check_actions and a.device.type == "cuda":
+                lo, hi = torch.aminmax(a)
+                if int(lo) < 0 or int(hi) >= self.n_actions:
+                    raise ValueError("action index out of range")
+            return a.contiguous()
+        a = np.asarray(actions, dtype=np.int64)
+        if a.shape != (self.n_copies,):
+            raise ValueError(f"expected {self.n_copies} actions, got shape {a.shape}")
+        if a.min() < 0 or a.max() >= self.n_actions:  # core.py:169-170
+            raise ValueError("action index out of range")
+        return torch.from_numpy(a).to(self.device, non_blocking=False)
+
+    def check(self) -> None:
+        """Raise any error a device-side step flagged (invalid device action,
+        missing spawn pose); synchronizes the current stream."""
+        err_env = ctypes.c_int64(0)
+        _lib.check(self._lib.sp_env_check(self._h, self._stream(), ctypes.byref(err_env)),
+                   "step")
+
+    # -- lifecycle ----------------------------------------------------------------
+    def reset_all(self, seed: int):
+        torch = self._torch
+        states = torch.empty((self.n_copies, self.state_dim), dtype=torch.float32,
+                             device=self.device)
+        _lib.check(self._lib.sp_env_reset_all(self._h, int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                              states.data_ptr(), self._stream()), "reset_all")
+        self._seeded = True
+        self.check()  # MapError if a lane found no spawn pose (core.py:144-147)
+        return states
+
+    def step_batch(self, actions, out: StepBatch | None = None) -> StepBatch:
+        if not self._seeded:
+            raise EpisodeTerminated("reset_all(seed) must be called before stepping")
+        torch = self._torch
+        a = self._actions_to_device(actions)
+        if not self.auto_reset:
+            flag = ctypes.c_int32(0)
+            _lib.check(self._lib.sp_env_any_needs_reset(self._h, self._stream(),
+                                                        ctypes.byref(flag)), "step")
+            if flag.value:
+                raise EpisodeTerminated("some lanes finished their episode; reset before stepping")
+        if out is None:
+            n, d = self.n_copies, self.state_dim
+            dev = self.device
+            out = StepBatch(
+                torch.empty((n, d), dtype=torch.float32, device=dev),
+                torch.empty(n, dtype=torch.float64, device=dev),
+                torch.empty(n, dtype=torch.bool, device=dev),
+                torch.empty(n, dtype=torch.bool, device=dev),
+                torch.empty((n, d), dtype=torch.float32, device=dev),
+                torch.empty(n, dtype=torch.int8, device=dev))
+        rc = self._lib.sp_env_step(self._h, a.data_ptr(), out.states.data_ptr(),
+                                   out.store_states.data_ptr(), out.rewards.data_ptr(),
+                                   out.dones.data_ptr(), out.truncated.data_ptr(),
+                                   out.events.data_ptr(), self._stream())
+        _lib.check(rc, "step")
+        return out
+
+    def step_device(self, actions_ptr: int, out: StepBatch) -> None:
+        """Raw launch on pre-validated device actions (benchmarks, CUDA graphs)."""
+        _lib.check(self._lib.sp_env_step(self._h, actions_ptr, out.states.data_ptr(),
+                                         out.store_states.data_ptr(), out.rewards.data_ptr(),
+                                         out.dones.data_ptr(), out.truncated.data_ptr(),
+                                         out.events.data_ptr(), self._stream()), "step")
+
+    # -- reporting -------------------------------------------------------------
+    def _per_copy_arrays(self) -> dict:
+        n = self.n_copies
+        eps = np.empty(n, np.int64)
+        arr = np.empty(n, np.int64)
+        rs = np.empty(n, np.float64)
+        fe = np.empty(n, np.int8)
+        fr = np.empty(n, np.float64)
+        fs = np.empty(n, np.int64)
+        _lib.check(self._lib.sp_env_stats_read(
+            self._h, eps.ctypes.data_as(_lib.c_i64p), arr.ctypes.data_as(_lib.c_i64p),
+            rs.ctypes.data_as(_lib.c_dp), fe.ctypes.data_as(_lib.c_i8p),
+            fr.ctypes.data_as(_lib.c_dp), fs.ctypes.data_as(_lib.c_i64p), self._stream()),
+            "stats")
+        return dict(episodes=eps, arrivals=arr, return_sum=rs, first_event=fe,
+                    first_return=fr, first_steps=fs)
+
+    def recent_returns(self) -> list:
+        buf = np.empty(256, np.float64)
+        n = ctypes.c_int32(0)
+        _lib.check(self._lib.sp_env_recent_returns(self._h, buf.ctypes.data_as(_lib.c_dp),
+                                                   ctypes.byref(n), self._stream()), "stats")
+        return buf[: n.value].tolist()
+
+    def snapshot_stats(self, reset: bool = False) -> StatsSnapshot:  # vecenv.py:120-132
+        self.check()
+        st = self._per_copy_arrays()
+        per_copy = [CopyStats(int(e), int(a), float(r))
+                    for e, a, r in zip(st["episodes"], st["arrivals"], st["return_sum"])]
+        snap = StatsSnapshot(per_copy=per_copy, episodes=int(st["episodes"].sum()),
+                             arrivals=int(st["arrivals"].sum()),
+                             return_sum=sum(c.return_sum for c in per_copy),
+                             recent_returns=self.recent_returns())
+        if reset:
+            _lib.check(self._lib.sp_env_stats_reset(self._h, 1, self._stream()), "stats")
+        return snap
+
+    def stats_totals(self):
+        """Device tensor [episodes, arrivals, return_sum] (float64) -- the
+        payload of the multi-GPU all-reduce (see paper_2305_04180_b200.dist)."""
+        out = self._torch.empty(3, dtype=self._torch.float64, device=self.device)
+        _lib.check(self._lib.sp_env_stats_totals(self._h, out.data_ptr(), self._stream()),
+                   "stats")
+        return out
+
+    def first_episode_outcomes(self) -> list:  # vecenv.py:134-137
+        st = self._per_copy_arrays()
+        return [None if e < 0 else (Event(int(e)), float(r), int(s))
+                for e, r, s in zip(st["first_event"], st["first_return"], st["first_steps"])]
+
+    @property
+    def all_first_episodes_done(self) -> bool:
+        return bool((self._per_copy_arrays()["first_event"] >= 0).all())
+
+    @property
+    def sim(self) -> SimView:
+        if self._sim is None:
+            self._sim = SimView(self)
+        return self._sim
+
+    def launch_info(self) -> dict:
+        smem = ctypes.c_int64(0)
+        thr = ctypes.c_int32(0)
+        ctas = ctypes.c_int32(0)
+        self._lib.sp_env_map_info(self._h, None, ctypes.byref(smem), ctypes.byref(thr),
+                                  ctypes.byref(ctas))
+        return {"smem_bytes": smem.value, "threads_per_cta": thr.value, "ctas": ctas.value}
+
+    def scan(self, x, y, heading, map_of_query=None, return_cells: bool = False):
+        """LiDAR ranges (no noise) from the fused step's marcher at caller poses:
+        (n, R) float64 [, (n, R) int32 hit cell iy*W+ix or -1]."""
+        torch = self._torch
+        x = torch.as_tensor(x, dtype=torch.float64, device=self.device).reshape(-1)
+        y = torch.as_tensor(y, dtype=torch.float64, device=self.device).reshape(-1)
+        h = torch.as_tensor(heading, dtype=torch.float64, device=self.device).reshape(-1)
+        n = x.numel()
+        if map_of_query is None:
+            mq = torch.zeros(n, dtype=torch.int64)
+        else:
+            mq = torch.as_tensor(np.asarray(map_of_query), dtype=torch.int64).reshape(-1)
+        order = torch.argsort(mq, stable=True)
+        counts = torch.bincount(mq, minlength=len(self._maps)).numpy()
+        qoff = np.zeros(len(self._maps) + 1, dtype=np.int64)
+        qoff[1:] = np.cumsum(counts)
+        od = order.to(self.device)
+        xs, ys, hs = x[od].contiguous(), y[od].contiguous(), h[od].contiguous()
+        R = self.n_beams
+        rng = torch.empty((n, R), dtype=torch.float64, device=self.device)
+        cells = torch.empty((n, R), dtype=torch.int32, device=self.device)
+        _lib.check(self._lib.sp_env_scan(self._h, n, qoff.ctypes.data_as(_lib.c_i64p),
+                                         xs.data_ptr(), ys.data_ptr(), hs.data_ptr(),
+                                         rng.data_ptr(), cells.data_ptr(), self._stream()),
+                   "scan")
+        out_r = torch.empty_like(rng)
+        out_c = torch.empty_like(cells)
+        out_r[od] = rng
+        out_c[od] = cells
+        return (out_r, out_c) if return_cells else out_r

@@ -1,0 +1,144 @@
+"""GPU parity: the fused CUDA step vs the reference (golden fixtures recorded
+from the unmodified reference) and vs the C oracle, on identical seeds.
+
+Bar (BASELINE north star): events/dones/truncated, RNG draw counts and
+episode counters bit-exact; poses, obs (incl. LiDAR ranges) and rewards
+within 1e-5 relative (+ fp32-resolution absolute floor, see helpers.py).
+"""
+
+import numpy as np
+import pytest
+
+from helpers import ATOL_OBS, ATOL_REWARD, assert_close, config, golden, load_maps, ranges
+from oracle.philox_shim import random_actions
+
+pytestmark = pytest.mark.gpu
+
+
+def _vec(maps, n, rg, cfg, **kw):
+    from paper_2305_04180_b200 import VecEnv
+    return VecEnv(maps, n, rg, cfg, **kw)
+
+
+def _replay_golden(name, maps, rg, n):
+    z = golden(name)
+    seed = int(z["seed"])
+    env = _vec(maps, n, rg, config(32))
+    s0 = env.reset_all(seed).cpu().numpy()
+    assert_close(s0, z["reset_states"], atol=ATOL_OBS, what="reset states")
+    steps = z["rewards"].shape[0]
+    obs_steps = list(z["obs_steps"])
+    k = 0
+    for t in range(steps):
+        b = env.step_batch(random_actions(seed, np.arange(n), t))
+        ev = b.events.cpu().numpy()
+        assert np.array_equal(ev, z["events"][t]), f"events differ at step {t}"
+        assert np.array_equal(b.dones.cpu().numpy(), z["dones"][t]), t
+        assert np.array_equal(b.truncated.cpu().numpy(), z["truncated"][t]), t
+        assert_close(b.rewards.cpu().numpy(), z["rewards"][t], atol=ATOL_REWARD,
+                     what=f"rewards step {t}")
+        if k < len(obs_steps) and obs_steps[k] == t:
+            assert_close(b.store_states.cpu().numpy(), z["store_states"][k], atol=ATOL_OBS,
+                         what=f"store_states step {t}")
+            assert_close(b.states.cpu().numpy(), z["states"][k], atol=ATOL_OBS,
+                         what=f"states step {t}")
+            k += 1
+    sim = env.sim
+    assert_close(sim.x, z["final_x"], what="x")
+    assert_close(sim.y, z["final_y"], what="y")
+    assert np.array_equal(sim.rng_ctr.astype(np.uint64), z["rng_ctr"]), "draw counts differ"
+    snap = env.snapshot_stats()
+    assert [c.episodes for c in snap.per_copy] == z["episodes"].tolist()
+    assert [c.arrivals for c in snap.per_copy] == z["arrivals"].tolist()
+    assert_close([c.return_sum for c in snap.per_copy], z["return_sum"], atol=1e-9,
+                 what="return_sum")
+    assert_close(snap.recent_returns, z["recent_returns"], atol=1e-9, what="recent returns")
+
+
+def test_cfg1_golden_1000_steps():
+    """cfg1: 16 envs, default map, 32 beams, 1000 random-action steps."""
+    _replay_golden("traj_cfg1.npz", load_maps(1), ranges(0.0), 16)
+
+
+def test_cfg2_golden_slice():
+    """cfg2 slice: 256 envs over 16 maps with +/-30 % diversity, 100 steps."""
+    _replay_golden("traj_cfg2.npz", load_maps(16), ranges(0.3), 256)
+
+
+@pytest.mark.parametrize("n,steps,div", [(4096, 60, 0.3), (1000, 40, 0.0)])
+def test_vs_oracle(n, steps, div):
+    from oracle.oracle import OracleVecEnv
+    maps = load_maps(16)
+    cfg = config(32)
+    seed = 4242
+    gpu = _vec(maps, n, ranges(div), cfg)
+    cpu = OracleVecEnv(maps, n, ranges(div), cfg)
+    assert_close(gpu.reset_all(seed).cpu().numpy(), cpu.reset_all(seed), atol=ATOL_OBS,
+                 what="reset")
+    for t in range(steps):
+        a = random_actions(seed, np.arange(n), t)
+        g = gpu.step_batch(a)
+        c = cpu.step_batch(a)
+        assert np.array_equal(g.events.cpu().numpy(), c.events), f"events step {t}"
+        assert np.array_equal(g.dones.cpu().numpy(), c.dones)
+        assert_close(g.rewards.cpu().numpy(), c.rewards, atol=ATOL_REWARD, what=f"reward {t}")
+        assert_close(g.store_states.cpu().numpy(), c.store_states, atol=ATOL_OBS,
+                     what=f"store {t}")
+        assert_close(g.states.cpu().numpy(), c.states, atol=ATOL_OBS, what=f"states {t}")
+    p = cpu.pose()
+    assert_close(gpu.sim.x, p["x"], what="x")
+    assert_close(gpu.sim.heading, p["heading"], atol=1e-12, what="heading")
+    assert np.array_equal(gpu.sim.rng_ctr.astype(np.uint64), p["rng_ctr"])
+
+
+@pytest.mark.parametrize("max_range", [150.0, 300.0, 500.0])
+def test_op_level_cast_rays_bit_identical(max_range):
+    """The plugin seam (kernels.cast_rays) reproduces the Cython backend
+    bit for bit (golden recorded from _cy.pyx)."""
+    from paper_2305_04180_b200 import kernels
+    from oracle.oracle import edt_cells
+    maps = load_maps(16)
+    z = golden("rays16.npz")
+    occ = np.stack([m.occupancy for m in maps]).astype(np.uint8)
+    edt = np.stack([edt_cells(m.occupancy) for m in maps])
+    ang = z["qh"][:, None] + config(32).lidar.beam_offsets()[None, :]
+    px, py = np.repeat(z["qx"], 32), np.repeat(z["qy"], 32)
+    got = kernels.cast_rays(occ, edt, np.repeat(z["qmap"], 32), px, py, np.cos(ang).ravel(),
+                            np.sin(ang).ravel(), 1.0, max_range)
+    assert np.array_equal(got, z[f"out_{int(max_range)}"])
+    disc = kernels.disc_collides(occ, z["qmap"], z["qx"], z["qy"], np.full(len(z["qx"]), 9.0),
+                                 1.0)
+    assert np.array_equal(disc, z["disc"])
+
+
+@pytest.mark.parametrize("n_beams", [32, 128, 256])
+@pytest.mark.parametrize("max_range", [150.0, 300.0, 500.0])
+def test_fast_marcher_hit_cells(n_beams, max_range):
+    """cfg4: the fused step's SMEM marcher stops in the reference's cell
+    (bit-exact hit cell) with the reference's range (1e-5 relative)."""
+    from oracle import oracle as O
+    maps = load_maps(16)
+    cfg = config(n_beams, lidar_kw={"max_range_cm": max_range})
+    env = _vec(maps, 16, ranges(0.0), cfg)
+    rng = np.random.default_rng(n_beams + int(max_range))
+    qx, qy, qh, qm = [], [], [], []
+    for m, gm in enumerate(maps):
+        free = np.argwhere(~gm.occupancy)
+        for iy, ix in free[rng.integers(0, len(free), 24)]:
+            qx.append(ix + rng.random()); qy.append(iy + rng.random())
+            qh.append(rng.uniform(-np.pi, np.pi)); qm.append(m)
+    qx, qy, qh, qm = map(np.array, (qx, qy, qh, qm))
+    got, cells = env.scan(qx, qy, qh, qm, return_cells=True)
+    got, cells = got.cpu().numpy(), cells.cpu().numpy()
+    occ = np.stack([m.occupancy for m in maps]).astype(np.uint8)
+    edt = np.stack([O.edt_cells(m.occupancy) for m in maps])
+    ang = qh[:, None] + cfg.lidar.beam_offsets()[None, :]
+    want, wcells = O.cast_rays(occ, edt, np.repeat(qm, n_beams), np.repeat(qx, n_beams),
+                               np.repeat(qy, n_beams), np.cos(ang).ravel(), np.sin(ang).ravel(),
+                               1.0, max_range, return_cells=True)
+    want = want.reshape(-1, n_beams)
+    wcells = wcells.reshape(-1, n_beams)
+    # hit cell: the reference reports the stopping occupied cell; both sides -1 otherwise
+    mism = cells != wcells
+    assert mism.sum() == 0, f"{mism.sum()} hit cells differ of {mism.size}"
+    assert_close(got, want, rtol=1e-9, atol=1e-9, what="ranges")
