@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -107,7 +108,6 @@ struct SpEnv {
   int grid = 0, threads = 0;
   size_t smem = 0;
   int n_sm = 0, smem_optin = 0;
-  int E_cap = 32;
   int32_t* h_err = nullptr;  // pinned
   std::mutex mu;
 
@@ -140,45 +140,92 @@ struct SpReplay {
   }
 };
 
-// geometry for a lane count with the env's tables
-static void plan_launch(SpEnv* env, int64_t lanes, int* grid, int* threads, int* E, size_t* smem,
-                        int* smem_maps) {
-  const EnvDev& d = env->d;
-  const size_t warp_bytes = align_up(1792 + (size_t)env->E_cap * d.D * 4, 16);
-  const size_t fixed = align_up((size_t)d.R * 16, 128) + 128;
-  const size_t budget = (size_t)env->smem_optin - 1024;
-  int use_smem = 1;
-  size_t map_bytes = align_up(d.map_bytes, 128);
-  int warps;
-  if (map_bytes + fixed + 8 * warp_bytes <= budget) {
-    warps = (int)std::min<size_t>(kMaxWarps, (budget - fixed - map_bytes) / warp_bytes);
-  } else {
-    use_smem = 0;  // map does not fit next to the warp scratch: read tables via L1/L2
-    map_bytes = 0;
-    warps = (int)std::min<size_t>(kMaxWarps, (budget - fixed) / warp_bytes);
+// Launch geometry shared by the step and scan kernels.
+struct Plan {
+  int grid = 1, threads = 768, chunk_cap = 1, smem_maps = 1;
+  size_t smem = 0;
+  std::vector<int64_t> cta_begin;  // grid + 1
+};
+
+// CTA slot ranges: every CTA stays inside one map when there are at most as
+// many non-empty maps as CTAs (CTAs per map proportional to its lanes,
+// largest remainder); otherwise equal contiguous splits.
+static std::vector<int64_t> cta_ranges(const std::vector<int64_t>& off, int G) {
+  const int M = (int)off.size() - 1;
+  const int64_t N = off[M] - off[0];
+  std::vector<int64_t> b;
+  int nonempty = 0;
+  for (int m = 0; m < M; ++m) nonempty += off[m + 1] > off[m];
+  if (N <= 0) return {off[0], off[0]};
+  if (nonempty > G || nonempty == 0) {
+    for (int c = 0; c <= G; ++c) b.push_back(off[0] + N * c / G);
+    return b;
   }
-  warps = std::max(warps, 1);
-  int g = (int)std::min<int64_t>(env->n_sm, std::max<int64_t>(1, (lanes + 31) / 32));
-  int64_t per_cta = (lanes + g - 1) / g;
-  int e = (int)std::max<int64_t>(1, std::min<int64_t>(env->E_cap, (per_cta + warps - 1) / warps));
-  // shrink the CTA if fewer warps than available would do
-  int need_warps = (int)std::max<int64_t>(1, std::min<int64_t>(warps, (per_cta + e - 1) / e));
-  *grid = g;
-  *threads = need_warps * 32;
-  *E = e;
-  *smem = map_bytes + fixed + (size_t)need_warps * warp_bytes;
-  *smem_maps = use_smem;
+  std::vector<int> g(M, 0);
+  int used = 0;
+  for (int m = 0; m < M; ++m) {
+    const int64_t nm = off[m + 1] - off[m];
+    if (nm == 0) continue;
+    g[m] = std::max<int>(1, (int)(nm * G / N));
+    used += g[m];
+  }
+  while (used > G) {  // too many after the min-1 rule: trim the best-served map
+    int best = -1;
+    for (int m = 0; m < M; ++m)
+      if (g[m] > 1 && (best < 0 || (off[m + 1] - off[m]) * g[best] < (off[best + 1] - off[best]) * g[m])) best = m;
+    if (best < 0) break;
+    --g[best];
+    --used;
+  }
+  while (used < G) {  // hand spare CTAs to the map with the most lanes per CTA
+    int best = -1;
+    for (int m = 0; m < M; ++m)
+      if (g[m] > 0 && (best < 0 || (off[m + 1] - off[m]) * g[best] > (off[best + 1] - off[best]) * g[m])) best = m;
+    const int64_t nm = off[best + 1] - off[best];
+    if (g[best] >= nm) break;
+    ++g[best];
+    ++used;
+  }
+  b.push_back(off[0]);
+  for (int m = 0; m < M; ++m) {
+    const int64_t nm = off[m + 1] - off[m];
+    for (int c = 1; c <= g[m]; ++c) b.push_back(off[m] + nm * c / g[m]);
+  }
+  return b;
 }
 
-static void set_geometry(SpEnv* env, EnvDev& d, size_t smem, int smem_maps, int E) {
-  const size_t map_region = smem_maps ? align_up(d.map_bytes, 128) : 0;
+static Plan plan_launch(SpEnv* env, const std::vector<int64_t>& off) {
+  const EnvDev& d = env->d;
+  Plan p;
+  const int64_t lanes = off.back() - off.front();
+  const size_t per_env = 6 * 8 + 4 + 2 + (size_t)d.D * 4;
+  const size_t fixed = align_up((size_t)d.R * 16, 128) + 128;
+  const size_t budget = (size_t)env->smem_optin - 1024;
+  size_t map_bytes = align_up(d.map_bytes, 128);
+  p.threads = kMaxWarps * 32;
+  size_t room = budget > fixed + map_bytes ? budget - fixed - map_bytes : 0;
+  if (room / per_env < 128) {  // map does not fit next to a useful chunk: read tables via L1/L2
+    p.smem_maps = 0;
+    map_bytes = 0;
+    room = budget - fixed;
+  }
+  p.chunk_cap = (int)std::max<size_t>(1, std::min<size_t>(p.threads, room / per_env));
+  p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(env->n_sm, (lanes + 15) / 16));
+  p.cta_begin = cta_ranges(off, p.grid);
+  p.grid = (int)p.cta_begin.size() - 1;
+  p.smem = map_bytes + fixed + 2 * align_up((size_t)p.chunk_cap, 16) +
+           align_up((size_t)p.chunk_cap * per_env + 16, 128);
+  return p;
+}
+
+static void apply_plan(const Plan& p, EnvDev& d) {
+  const size_t map_region = p.smem_maps ? align_up(d.map_bytes, 128) : 0;
   d.off_beam = (uint32_t)map_region;
   d.off_bar = (uint32_t)(map_region + align_up((size_t)d.R * 16, 128));
-  d.off_warps = d.off_bar + 128;
-  d.warp_smem = (uint32_t)align_up(1792 + (size_t)env->E_cap * d.D * 4, 16);
-  d.smem_maps = smem_maps;
-  d.E = E;
-  (void)smem;
+  d.off_flags = d.off_bar + 128;
+  d.off_chunk = (uint32_t)align_up(d.off_flags + 2 * align_up((size_t)p.chunk_cap, 16), 128);
+  d.chunk_cap = p.chunk_cap;
+  d.smem_maps = p.smem_maps;
 }
 
 template <class T>
@@ -242,7 +289,6 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   }
   env->n_sm = prop.multiProcessorCount;
   env->smem_optin = (int)prop.sharedMemPerBlockOptin;
-  env->E_cap = (int)std::max(1, std::min(32, 1024 / cfg->n_beams));
 
   EnvDev& d = env->d;
   d.n = n_envs;
@@ -366,13 +412,35 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   d.ranges = drng;
   d.env_of_slot = deos;
 
-  int E, smem_maps;
-  plan_launch(env, n_envs, &env->grid, &env->threads, &E, &env->smem, &smem_maps);
-  set_geometry(env, d, env->smem, smem_maps, E);
-  cudaError_t e1 = cudaFuncSetAttribute(env_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  {
+    const int R = env->R;
+    d.r_shift = (R & (R - 1)) == 0 ? __builtin_ctz((unsigned)R) : -1;
+    d.r_magic = (d.r_shift < 0 && R < 512) ? (((uint64_t)1 << 40) + R - 1) / R : 0;
+    const char* rm = std::getenv("SPARROW_REFILL_MIN");
+    d.refill_min = rm ? std::max(1, std::min(32, std::atoi(rm))) : 16;
+  }
+  Plan plan = plan_launch(env, env->map_off);
+  apply_plan(plan, d);
+  int64_t* dcta = nullptr;
+  {
+    int rc2 = env->alloc(&dcta, plan.cta_begin.size());
+    if (rc2) { delete env; return rc2; }
+    cudaMemcpy(dcta, plan.cta_begin.data(), 8 * plan.cta_begin.size(), cudaMemcpyHostToDevice);
+  }
+  d.cta_begin = dcta;
+  env->grid = plan.grid;
+  env->threads = plan.threads;
+  env->smem = plan.smem;
+  cudaError_t e1 = cudaFuncSetAttribute(env_step_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         env->smem_optin);
-  cudaError_t e2 = cudaFuncSetAttribute(env_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (e1 == cudaSuccess)
+    e1 = cudaFuncSetAttribute(env_step_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              env->smem_optin);
+  cudaError_t e2 = cudaFuncSetAttribute(env_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         env->smem_optin);
+  if (e2 == cudaSuccess)
+    e2 = cudaFuncSetAttribute(env_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              env->smem_optin);
   cudaError_t e3 = cudaDeviceSynchronize();
   if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
     delete env;
@@ -391,7 +459,10 @@ int sp_env_destroy(SpEnv* env) {
 }
 
 static int launch_env(SpEnv* env, const StepArgs& a, cudaStream_t st) {
-  env_step_kernel<<<env->grid, env->threads, env->smem, st>>>(env->d, a);
+  if (env->d.smem_maps)
+    env_step_kernel<true><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
+  else
+    env_step_kernel<false><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(SP_ECUDA, std::string("env_step_kernel: ") + cudaGetErrorString(e));
   return SP_OK;
@@ -609,16 +680,22 @@ int sp_env_scan(SpEnv* env, int64_t n, const int64_t* query_offsets, const doubl
   DevDeviceGuard guard(env->device);
   std::lock_guard<std::mutex> lk(env->mu);
   cudaStream_t st = (cudaStream_t)stream;
-  int64_t* dq = nullptr;
-  SP_CUDA(cudaMallocAsync((void**)&dq, 8 * (env->n_maps + 1), st));
-  SP_CUDA(cudaMemcpyAsync(dq, query_offsets, 8 * (env->n_maps + 1), cudaMemcpyHostToDevice, st));
-  int grid, threads, E, smem_maps;
-  size_t smem;
-  plan_launch(env, n, &grid, &threads, &E, &smem, &smem_maps);
+  std::vector<int64_t> off(query_offsets, query_offsets + env->n_maps + 1);
+  Plan plan = plan_launch(env, off);
   EnvDev d = env->d;
-  set_geometry(env, d, smem, smem_maps, E);
-  ScanArgs q{n, dq, x, y, heading, ranges, hit_cell};
-  env_scan_kernel<<<grid, threads, smem, st>>>(d, q);
+  apply_plan(plan, d);
+  const size_t nq = off.size(), nc = plan.cta_begin.size();
+  int64_t* dq = nullptr;
+  SP_CUDA(cudaMallocAsync((void**)&dq, 8 * (nq + nc), st));
+  SP_CUDA(cudaMemcpyAsync(dq, off.data(), 8 * nq, cudaMemcpyHostToDevice, st));
+  SP_CUDA(cudaMemcpyAsync(dq + nq, plan.cta_begin.data(), 8 * nc, cudaMemcpyHostToDevice, st));
+  ScanArgs q{n, dq + nq, dq, x, y, heading, ranges, hit_cell};
+  if (d.smem_maps)
+    env_scan_kernel<true><<<plan.grid, plan.threads, plan.smem, st>>>(d, q);
+  else
+    env_scan_kernel<false><<<plan.grid, plan.threads, plan.smem, st>>>(d, q);
+  // the copies above read pageable host memory: keep `off`/`plan` alive until they land
+  SP_CUDA(cudaStreamSynchronize(st));
   cudaError_t e = cudaGetLastError();
   cudaFreeAsync(dq, st);
   if (e != cudaSuccess) return fail(SP_ECUDA, std::string("env_scan_kernel: ") + cudaGetErrorString(e));

@@ -5,22 +5,29 @@
 //
 // * Lanes (env copies) are stored struct-of-arrays in MAP-MAJOR slot order;
 //   env_of_slot maps a slot back to the caller's row (outputs keep the
-//   reference row order).  Each CTA owns a contiguous slot range, so it needs
-//   one map (rarely two) at a time.
+//   reference row order).  The host gives every CTA a contiguous slot range
+//   that lies inside one map whenever the map count allows, so a CTA stages
+//   one map once per launch.
 // * Per map, two tables live in shared memory, staged by one TMA bulk copy
 //   (cp.async.bulk + mbarrier): a 1-bit occupancy bitmap (H x ceil(W/32) u32)
 //   and a 2x2-block "free box" table (u8: 0 = block holds an occupied cell,
 //   else 1 + r where the (2r+1)^2 blocks around it are all free).  366 x 366
 //   cells -> 17.6 KB + 33.5 KB.
-// * A warp takes a batch of E lanes.  Env math runs lane-per-env in fp64 with
-//   the reference's rounding order; LiDAR rays run from a per-warp ray queue
-//   (lane-per-ray, idle lanes refill by ballot) so divergent ray lengths do
-//   not idle the warp.  Noise is drawn lane-per-env into the staging row.
+// * A CTA walks its range in chunks of up to `chunk_cap` envs with CTA-wide
+//   phases separated by __syncthreads:
+//     A  thread-per-env physics, collision, events, shaped-reward partial,
+//        obs header and LiDAR noise (fp64 in the reference's rounding order);
+//     B  one CTA-wide LiDAR ray queue over chunk x R rays: warps take as many
+//        rays as they have idle lanes (one shared atomic), so ray-length
+//        divergence only idles lanes at the very end of the chunk;
+//     C  thread-per-env reward, outputs, VecEnv statistics; coalesced rows;
+//     D  auto-reset of the finished envs (resample, spawn rejection) and a
+//        fresh scan through the same ray queue, then the post-reset rows.
 // * The march visits the same cells as the reference DDA (_cy.pyx:89-105) but
 //   jumps over free boxes in one step: at cell (ix,iy) with free box B, the
 //   ray leaves B through the face with the smaller exit parameter (ties go to
-//   x, as tmx <= tmy does), re-entering the cell grid at the cell containing
-//   the exit point (clamped into B's span on the other axis).  Only free cells
+//   x, as tmx <= tmy does), re-entering the grid at the cell containing the
+//   exit point (clamped into B's span on the other axis).  Only free cells
 //   are skipped, so the first occupied cell is the reference's (up to
 //   exact-corner rounding, the same ambiguity the reference's own EDT jump
 //   has, _cy.pyx:62-88).
@@ -67,8 +74,8 @@ struct MapView {
   __device__ __forceinline__ uint32_t code(int ix, int iy) const {
     return blk[(iy >> 1) * Wb + (ix >> 1)];
   }
-  __device__ __forceinline__ bool occ(int ix, int iy) const {
-    return (bits[iy * WW + (ix >> 5)] >> (ix & 31)) & 1u;
+  __device__ __forceinline__ uint32_t word(int ix, int iy) const {
+    return bits[iy * WW + (ix >> 5)];
   }
 };
 
@@ -78,10 +85,9 @@ __device__ __forceinline__ bool disc_hits(const MapView& mv, const EnvDev& d, do
   const double r = d.radius, cell = d.cell;
   if (x - r < 0.0 || y - r < 0.0 || x + r > (double)d.W * cell || y + r > (double)d.H * cell)
     return true;  // :124-126
-  int cx = (int)floor(x * d.inv_cell), cy = (int)floor(y * d.inv_cell);
+  const int cx = (int)floor(x * d.inv_cell), cy = (int)floor(y * d.inv_cell);
   if (cx >= 0 && cx < d.W && cy >= 0 && cy < d.H) {
-    uint32_t c = mv.code(cx, cy);
-    if (c > (uint32_t)d.need_r) return false;  // free box covers the whole bbox
+    if (mv.code(cx, cy) > (uint32_t)d.need_r) return false;  // free box covers the bbox
   }
   int ix0 = (int)floor(ddiv(dsub(x, r), cell)); if (ix0 < 0) ix0 = 0;  // :128-135
   int ix1 = (int)floor(ddiv(dadd(x, r), cell)); if (ix1 > d.W - 1) ix1 = d.W - 1;
@@ -92,19 +98,19 @@ __device__ __forceinline__ bool disc_hits(const MapView& mv, const EnvDev& d, do
     const uint32_t* rowp = mv.bits + iy * mv.WW;
     for (int w = ix0 >> 5; w <= (ix1 >> 5); ++w) {
       uint32_t m = rowp[w];
-      int lo = w << 5;
+      const int lo = w << 5;
       if (ix0 > lo) m &= ~0u << (ix0 - lo);
       if (ix1 - lo < 31) m &= (2u << (ix1 - lo)) - 1u;
       while (m) {
-        int ix = lo + __ffs(m) - 1;
+        const int ix = lo + __ffs(m) - 1;
         m &= m - 1;
-        double clo = dmul((double)ix, cell), chi = dadd(clo, cell);  // :141-153
+        const double clo = dmul((double)ix, cell), chi = dadd(clo, cell);  // :141-153
         double nx = x > clo ? x : clo;
         if (nx > chi) nx = chi;
-        double rlo = dmul((double)iy, cell), rhi = dadd(rlo, cell);
+        const double rlo = dmul((double)iy, cell), rhi = dadd(rlo, cell);
         double ny = y > rlo ? y : rlo;
         if (ny > rhi) ny = rhi;
-        double ddx = dsub(x, nx), ddy = dsub(y, ny);
+        const double ddx = dsub(x, nx), ddy = dsub(y, ny);
         if (dadd(dmul(ddx, ddx), dmul(ddy, ddy)) <= r2) return true;
       }
     }
@@ -118,43 +124,47 @@ struct Ray {
   int ix, iy;
 };
 
-// One free-box step.  Returns true when the ray is finished (r.t = range).
+// 1/v to within an ulp: fp32 seed + two fp64 Newton steps (no DDIV).
+__device__ __forceinline__ double recip(double v) {
+  if (v == 0.0) return __longlong_as_double(0x7ff0000000000000ll);  // +inf: never exits this axis
+  if (fabs(v) < 1e-30) return 1.0 / v;
+  float f;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(f) : "f"((float)v));
+  double r = (double)f;
+  r = r * (2.0 - v * r);
+  r = r * (2.0 - v * r);
+  return r;
+}
+
+// One free-box step (branch-free up to the finishing tests).  Returns true
+// when the ray is finished; r.t is then the range.
 __device__ __forceinline__ bool ray_step(Ray& r, const MapView& mv, const EnvDev& d, int& hit) {
-  uint32_t code = mv.code(r.ix, r.iy);
-  int lox, hix, loy, hiy;
-  if (code == 0u) {
-    if (mv.occ(r.ix, r.iy)) {  // entered an occupied cell at r.t (<= max_range)
-      hit = r.iy * d.W + r.ix;
-      return true;
-    }
-    lox = hix = r.ix;
-    loy = hiy = r.iy;
-  } else {
-    int rr = (int)code - 1;
-    int bx = r.ix >> 1, by = r.iy >> 1;
-    lox = (bx - rr) << 1;
-    hix = ((bx + rr) << 1) + 1;
-    loy = (by - rr) << 1;
-    hiy = ((by + rr) << 1) + 1;
+  const uint32_t code = mv.code(r.ix, r.iy);
+  const uint32_t word = mv.word(r.ix, r.iy);
+  if (code == 0u && ((word >> (r.ix & 31)) & 1u)) {  // entered an occupied cell at r.t
+    hit = r.iy * d.W + r.ix;
+    return true;
   }
+  const int rr = (int)code - 1;
+  const int bx = r.ix >> 1, by = r.iy >> 1;
+  const bool box = code != 0u;
+  const int lox = box ? (bx - rr) << 1 : r.ix;
+  const int hix = box ? ((bx + rr) << 1) + 1 : r.ix;
+  const int loy = box ? (by - rr) << 1 : r.iy;
+  const int hiy = box ? ((by + rr) << 1) + 1 : r.iy;
   const bool px = r.dx >= 0.0, py = r.dy >= 0.0;
-  const double X = (double)(px ? hix + 1 : lox), Y = (double)(py ? hiy + 1 : loy);
-  const double tx = (X * d.cell - r.x0) * r.idx;
-  const double ty = (Y * d.cell - r.y0) * r.idy;
-  if (tx <= ty) {  // leave through the x face (tie -> x, as _cy.pyx:89)
-    r.t = tx;
+  const double tx = ((double)(px ? hix + 1 : lox) * d.cell - r.x0) * r.idx;
+  const double ty = ((double)(py ? hiy + 1 : loy) * d.cell - r.y0) * r.idy;
+  const bool xs = tx <= ty;  // leave through the x face on ties, as _cy.pyx:89
+  r.t = xs ? tx : ty;
+  // the cell on the other axis at the exit point, clamped into the box span
+  const int c = (int)floor((xs ? (r.y0 + tx * r.dy) : (r.x0 + ty * r.dx)) * d.inv_cell);
+  if (xs) {
     r.ix = px ? hix + 1 : lox - 1;
-    if (code != 0u) {
-      int c = (int)floor((r.y0 + tx * r.dy) * d.inv_cell);
-      r.iy = min(max(c, loy), hiy);
-    }
+    r.iy = min(max(c, loy), hiy);
   } else {
-    r.t = ty;
     r.iy = py ? hiy + 1 : loy - 1;
-    if (code != 0u) {
-      int c = (int)floor((r.x0 + ty * r.dx) * d.inv_cell);
-      r.ix = min(max(c, lox), hix);
-    }
+    r.ix = min(max(c, lox), hix);
   }
   if (r.t > d.max_range) {  // :97-99
     r.t = d.max_range;
@@ -175,8 +185,8 @@ __device__ __forceinline__ bool ray_setup(Ray& r, double x0, double y0, double c
   r.y0 = y0;
   r.dx = ch * cs.x - sh * cs.y;  // cos(h + o_j)
   r.dy = sh * cs.x + ch * cs.y;  // sin(h + o_j)
-  r.idx = r.dx != 0.0 ? 1.0 / r.dx : __longlong_as_double(0x7ff0000000000000ll);
-  r.idy = r.dy != 0.0 ? 1.0 / r.dy : __longlong_as_double(0x7ff0000000000000ll);
+  r.idx = recip(r.dx);
+  r.idy = recip(r.dy);
   r.t = 0.0;
   r.ix = (int)floor(x0 * d.inv_cell);
   r.iy = (int)floor(y0 * d.inv_cell);
@@ -187,63 +197,91 @@ __device__ __forceinline__ bool ray_setup(Ray& r, double x0, double y0, double c
   return false;
 }
 
-// Per-warp scratch (shared memory).
-struct WarpSmem {
+// Per-CTA chunk scratch (shared memory).
+struct Chunk {
   double *px, *py, *ch, *sh, *sig;
   unsigned long long* smin;
-  int32_t* list;  // batch-local env index per queue entry
-  float* stage;   // E x D staging rows
+  int32_t* list;   // chunk-local env of each group of R rays (queue order)
+  int* ctl;        // [0] ray-queue head, [1] list length
+  float* stage;    // chunk x D staging rows
 };
 
-__device__ __forceinline__ WarpSmem warp_smem(uint8_t* base, int D) {
-  WarpSmem w;
-  w.px = (double*)base;
-  w.py = w.px + 32;
-  w.ch = w.py + 32;
-  w.sh = w.ch + 32;
-  w.sig = w.sh + 32;
-  w.smin = (unsigned long long*)(w.sig + 32);
-  w.list = (int32_t*)(w.smin + 32);
-  w.stage = (float*)(w.list + 32);
-  (void)D;
-  return w;
+__device__ __forceinline__ Chunk chunk_smem(uint8_t* base, int cap) {
+  Chunk c;
+  c.px = (double*)base;
+  c.py = c.px + cap;
+  c.ch = c.py + cap;
+  c.sh = c.ch + cap;
+  c.sig = c.sh + cap;
+  c.smin = (unsigned long long*)(c.sig + cap);
+  c.list = (int32_t*)(c.smin + cap);
+  c.ctl = c.list + cap;
+  c.stage = (float*)(c.ctl + 4);
+  return c;
 }
 
-// Ray queue over n_env envs (ws.list) x R beams.  fin(e, j, t, hit).
+// q / R for 0 <= q < 2^31 (shift when R is a power of two, else magic number)
+__device__ __forceinline__ int div_r(int q, const EnvDev& d) {
+  if (d.r_shift >= 0) return q >> d.r_shift;
+  if (d.r_magic) return (int)(((uint64_t)(uint32_t)q * d.r_magic) >> 40);
+  return q / d.R;
+}
+
+// CTA-wide ray queue over n_env envs (c.list) x R beams.  fin(e, j, t, hit).
+// Every thread of the CTA must call it.  A warp refills only when at least
+// d.refill_min of its lanes are idle (or the queue is drained), and finished
+// rays are retired in the same branch, so per-ray setup/finish code runs at
+// high SIMT occupancy while the march keeps most lanes busy.
 template <bool kHit, class Fin>
-__device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, const WarpSmem& ws,
-                                          const double2* beam, int n_env, Fin fin) {
+__device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, const Chunk& c,
+                                          const double2* beam, int n_env, const Fin& fin) {
   const int R = d.R;
   const int total = n_env * R;
-  int next = 0;
-  bool active = false;
-  int e = 0, j = 0;
+  const int lane = threadIdx.x & 31;
+  bool active = false, done = false;
+  bool drained = total == 0;
+  int e = 0, j = 0, res_hit = -1;
+  double res_t = 0.0;
   Ray r;
   for (;;) {
-    const unsigned need = __ballot_sync(SP_FULL, !active);
-    if (need != 0u && next < total) {
-      const int my = next + __popc(need & lanemask_lt());
-      next += __popc(need);
-      if (!active && my < total) {
-        e = ws.list[my / R];
-        j = my - (my / R) * R;
-        int hit;
-        if (ray_setup(r, ws.px[e], ws.py[e], ws.ch[e], ws.sh[e], beam[j], d, hit)) {
-          fin(e, j, 0.0, hit);
-        } else {
-          active = true;
-        }
+    const unsigned idle = __ballot_sync(SP_FULL, !active);
+    const int n_idle = __popc(idle);
+    if (n_idle >= d.refill_min || drained) {
+      if (done) {
+        fin(e, j, res_t, res_hit);
+        done = false;
       }
-    }
-    if (!__any_sync(SP_FULL, active)) {
-      if (next >= total) break;
-      continue;
+      if (drained) {
+        if (idle == SP_FULL) break;
+      } else {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&c.ctl[0], n_idle);
+        base = __shfl_sync(SP_FULL, base, 0);
+        if (base + n_idle >= total) drained = true;
+        const int my = base + __popc(idle & lanemask_lt());
+        if (!active && my < total) {
+          const int g = div_r(my, d);
+          e = c.list[g];
+          j = my - g * R;
+          int hit;
+          if (ray_setup(r, c.px[e], c.py[e], c.ch[e], c.sh[e], beam[j], d, hit)) {
+            done = true;
+            res_t = 0.0;
+            res_hit = hit;
+          } else {
+            active = true;
+          }
+        }
+        continue;
+      }
     }
     if (active) {
       int hit;
       if (ray_step(r, mv, d, hit)) {
-        fin(e, j, r.t, kHit ? hit : -1);
         active = false;
+        done = true;
+        res_t = r.t;
+        res_hit = kHit ? hit : -1;
       }
     }
   }
@@ -253,12 +291,12 @@ __device__ __forceinline__ void set_error(const EnvDev& d, int code, int64_t row
   if (atomicCAS(d.err, 0, code) == 0) d.err[1] = (int32_t)row;
 }
 
-// Fill stage[5 .. 5+R) of one row with standard normals (core.py:240 draws).
+// Standard normals for one staging row (core.py:240 draws), stored as z.
 __device__ __forceinline__ void draw_noise_row(const EnvDev& d, uint32_t gid, uint64_t& ctr,
                                                float* row) {
   const int R = d.R;
   for (int j = 0; j < R; j += 4) {
-    Block4 b = stream_block(d.seed, gid, 0u, ctr++);
+    const Block4 b = stream_block(d.seed, gid, 0u, ctr++);
     float z[4];
     draw_normals4(b, z);
 #pragma unroll
@@ -276,292 +314,44 @@ __device__ __forceinline__ double bearing_error(double x, double y, double h, do
 // reward.py:40-52
 __device__ __forceinline__ double cross_track(double x, double y, double sx, double sy, double gx,
                                               double gy) {
-  double vx = dsub(gx, sx), vy = dsub(gy, sy);
-  double len2 = dadd(dmul(vx, vx), dmul(vy, vy));
-  double safe = len2 > 0.0 ? len2 : 1.0;
+  const double vx = dsub(gx, sx), vy = dsub(gy, sy);
+  const double len2 = dadd(dmul(vx, vx), dmul(vy, vy));
+  const double safe = len2 > 0.0 ? len2 : 1.0;
   double t = dclip(ddiv(dadd(dmul(dsub(x, sx), vx), dmul(dsub(y, sy), vy)), safe), 0.0, 1.0);
   if (!(len2 > 0.0)) t = 0.0;
-  double ex = dsub(x, dadd(sx, dmul(t, vx))), ey = dsub(y, dadd(sy, dmul(t, vy)));
+  const double ex = dsub(x, dadd(sx, dmul(t, vx))), ey = dsub(y, dadd(sy, dmul(t, vy)));
   return __dsqrt_rn(dadd(dmul(ex, ex), dmul(ey, ey)));
 }
 
-// Lane state carried through one warp batch.
-struct Lane {
-  double x, y, h, vl, va, ret, sx, sy, c0, s0, k, dt, vml, vma, sig;
-  uint64_t hist0, ctr;
-  int32_t step, delay;
+// core.py:243-258 columns 0..4 (LiDAR columns come from the ray phase)
+__device__ __forceinline__ void header_row(const MapConst& mc, double x, double y, double alpha,
+                                           double c0, double s0, double vl, double va, double vml,
+                                           double vma, float* row) {
+  const double rx = dsub(mc.goal_x, x), ry = dsub(mc.goal_y, y);
+  row[0] = (float)ddiv(dadd(dmul(c0, rx), dmul(s0, ry)), mc.plan_dist);
+  row[1] = (float)ddiv(dadd(dmul(-s0, rx), dmul(c0, ry)), mc.plan_dist);
+  row[2] = (float)ddiv(alpha, SP_PI);
+  row[3] = (float)ddiv(vl, vml);
+  row[4] = (float)ddiv(va, vma);
+}
+
+// Finish functor of the step/reset ray phases: noisy normalized obs into the
+// staging row (core.py:237-241, 257) and the noise-free minimum (core.py:205).
+struct FinObs {
+  Chunk c;
+  int D;
+  double max_range;
+  __device__ __forceinline__ void operator()(int e, int j, double t, int) const {
+    float* rowp = c.stage + e * D;
+    const double z = (double)rowp[5 + j];
+    const double v = dclip(dadd(t, dadd(0.0, dmul(c.sig[e], z))), 0.0, max_range);
+    rowp[5 + j] = (float)ddiv(v, max_range);
+    atomicMin(&c.smin[e], (unsigned long long)__double_as_longlong(t + 0.0));
+  }
 };
 
-__device__ __forceinline__ void header_row(const EnvDev& d, const MapConst& mc, const Lane& L,
-                                           float* row) {
-  // core.py:243-258 (columns 0..4; LiDAR columns are written by the ray phase)
-  double rx = dsub(mc.goal_x, L.x), ry = dsub(mc.goal_y, L.y);
-  double alpha = bearing_error(L.x, L.y, L.h, mc.goal_x, mc.goal_y);
-  row[0] = (float)ddiv(dadd(dmul(L.c0, rx), dmul(L.s0, ry)), mc.plan_dist);
-  row[1] = (float)ddiv(dadd(dmul(-L.s0, rx), dmul(L.c0, ry)), mc.plan_dist);
-  row[2] = (float)ddiv(alpha, SP_PI);
-  row[3] = (float)ddiv(L.vl, L.vml);
-  row[4] = (float)ddiv(L.va, L.vma);
-}
-
-// core.py:114-156 for one lane (stream already bound).  false = no spawn.
-__device__ __forceinline__ bool reset_lane(const EnvDev& d, const MapView& mv, const MapConst& mc,
-                                           int64_t s, uint32_t gid, Lane& L) {
-  const double* rg = d.ranges + (d.ranges_shared ? 0 : 12 * s);
-  // DiversityRanges.sample (params.py:112-121): U U I U U U
-  L.k = draw_uniform(stream_block(d.seed, gid, 0u, L.ctr++), rg[0], rg[1]);
-  L.dt = draw_uniform(stream_block(d.seed, gid, 0u, L.ctr++), rg[2], rg[3]);
-  L.delay = (int32_t)draw_integer(stream_block(d.seed, gid, 0u, L.ctr++), (int64_t)rg[4],
-                                  (int64_t)rg[5] + 1);
-  L.vml = draw_uniform(stream_block(d.seed, gid, 0u, L.ctr++), rg[6], rg[7]);
-  L.vma = draw_uniform(stream_block(d.seed, gid, 0u, L.ctr++), rg[8], rg[9]);
-  L.sig = draw_uniform(stream_block(d.seed, gid, 0u, L.ctr++), rg[10], rg[11]);
-  // spawn rejection (core.py:135-147)
-  bool ok = false;
-  double x = 0, y = 0, th = 0;
-  for (int a = 0; a < d.spawn_attempts; ++a) {
-    x = draw_uniform(stream_block(d.seed, gid, 0u, L.ctr++), mc.spawn[0], mc.spawn[2]);
-    y = draw_uniform(stream_block(d.seed, gid, 0u, L.ctr++), mc.spawn[1], mc.spawn[3]);
-    th = draw_uniform(stream_block(d.seed, gid, 0u, L.ctr++), -SP_PI, SP_PI);
-    if (!disc_hits(mv, d, x, y)) {
-      ok = true;
-      break;
-    }
-  }
-  if (!ok) return false;
-  L.x = x; L.y = y; L.h = th;  // core.py:149-156
-  L.sx = x; L.sy = y;
-  L.c0 = cos(th);
-  L.s0 = sin(th);
-  L.vl = 0.0; L.va = 0.0;
-  L.step = 0;
-  L.hist0 = ~0ull;  // d x (0, 0): 4-bit code 15 everywhere
-  return true;
-}
-
-// ------------------------------------------------------------ the batch ---
-__device__ __noinline__ void env_batch(const EnvDev& d, const StepArgs& a, const MapView& mv,
-                                       const MapConst& mc, const double2* beam, const WarpSmem& ws,
-                                       int64_t s0, int E, int lane) {
-  const int D = d.D;
-  const bool act = lane < E;
-  const int64_t s = s0 + lane;
-  const int64_t row = act ? d.env_of_slot[s] : 0;
-  const uint32_t gid = (uint32_t)(d.env_id_offset + row);
-  float* my_stage = ws.stage + lane * D;
-  Lane L;
-  bool live = false;  // this lane takes part in the step
-  bool ended = false;
-  int8_t ev = 0;
-  bool coll = false, arrived = false, timed_out = false;
-  double d1 = 0.0;
-
-  if (act) {
-    L.x = d.x[s]; L.y = d.y[s]; L.h = d.h[s]; L.vl = d.vl[s]; L.va = d.va[s]; L.ret = d.ret[s];
-    L.sx = d.sx[s]; L.sy = d.sy[s]; L.c0 = d.c0[s]; L.s0 = d.s0[s];
-    L.k = d.pk[s]; L.dt = d.pdt[s]; L.vml = d.pvl[s]; L.vma = d.pva[s]; L.sig = d.psig[s];
-    L.ctr = d.ctr[s]; L.step = d.step[s]; L.delay = d.delay[s];
-    L.hist0 = L.delay > 0 ? d.hist[s] : 0ull;
-    ws.list[lane] = lane;
-  }
-  if (a.mode == MODE_STEP && act) {
-    const int64_t av = a.actions[row];
-    if (av < 0 || av >= d.n_actions) {
-      set_error(d, SP_EACTION, row);
-    } else if (d.needs_reset[s]) {
-      set_error(d, SP_EEPISODE, row);
-    } else {
-      live = true;
-      // delay queue (core.py:176-182): matured = action from `delay` steps ago
-      uint32_t code;
-      if (L.delay == 0) {
-        code = (uint32_t)av;
-      } else {
-        const int q = L.delay - 1;
-        uint64_t w = q < 16 ? L.hist0 : d.hist[(int64_t)(q >> 4) * d.n + s];
-        code = (uint32_t)(w >> (4 * (q & 15))) & 15u;
-        // push av: shift the 4-bit history by one entry across the used words
-        const int nw = (L.delay + 15) >> 4;
-        uint64_t carry = (uint64_t)av;
-        for (int wi = 0; wi < nw; ++wi) {
-          uint64_t cur = wi == 0 ? L.hist0 : d.hist[(int64_t)wi * d.n + s];
-          uint64_t nxt = (cur << 4) | carry;
-          carry = cur >> 60;
-          if (wi == 0) L.hist0 = nxt;
-          else d.hist[(int64_t)wi * d.n + s] = nxt;
-        }
-      }
-      const double mv_ = d.action_v[code], mw_ = d.action_w[code];
-      // apply_kinematics (kinematics.py:22-36)
-      double v0 = dadd(dmul(L.k, L.vl), dmul(dsub(1.0, L.k), mv_));
-      double v1 = dadd(dmul(L.k, L.va), dmul(dsub(1.0, L.k), mw_));
-      v0 = dclip(v0, -L.vml, L.vml);
-      v1 = dclip(v1, -L.vma, L.vma);
-      L.vl = v0; L.va = v1;
-      // integrate_unicycle (kinematics.py:39-63)
-      double sin0, cos0, sin1, cos1;
-      sincos(L.h, &sin0, &cos0);
-      const double h1 = dadd(L.h, dmul(v1, L.dt));
-      sincos(h1, &sin1, &cos1);
-      double ddx, ddy;
-      if (fabs(v1) >= 1e-6) {
-        const double radius = ddiv(v0, v1);
-        ddx = dmul(radius, dsub(sin1, sin0));
-        ddy = dmul(-radius, dsub(cos1, cos0));
-      } else {
-        ddx = dmul(dmul(v0, cos0), L.dt);
-        ddy = dmul(dmul(v0, sin0), L.dt);
-      }
-      L.x = dadd(L.x, ddx);
-      L.y = dadd(L.y, ddy);
-      L.h = wrap_angle(h1);
-      // events (core.py:189-201)
-      coll = disc_hits(mv, d, L.x, L.y);
-      const double gdx = dsub(mc.goal_x, L.x), gdy = dsub(mc.goal_y, L.y);
-      d1 = __dsqrt_rn(dadd(dmul(gdx, gdx), dmul(gdy, gdy)));
-      arrived = !coll && d1 <= mc.goal_r;
-      L.step += 1;
-      timed_out = !coll && !arrived && L.step >= d.timeout;
-      ev = coll ? 1 : (arrived ? 2 : (timed_out ? 3 : 0));
-      ended = coll || arrived || timed_out;
-      // noise for this step's scan (core.py:237-241), staged as z
-      draw_noise_row(d, gid, L.ctr, my_stage);
-      double sh_, ch_;
-      sincos(L.h, &sh_, &ch_);
-      ws.px[lane] = L.x; ws.py[lane] = L.y; ws.ch[lane] = ch_; ws.sh[lane] = sh_;
-      ws.sig[lane] = L.sig;
-      ws.smin[lane] = 0x7ff0000000000000ull;  // +inf
-    }
-  }
-
-  const double max_range = d.max_range;
-  auto fin_obs = [&](int e, int j, double t, int) {
-    float* rowp = ws.stage + e * D;
-    const double z = (double)rowp[5 + j];
-    const double v = dclip(dadd(t, dadd(0.0, dmul(ws.sig[e], z))), 0.0, max_range);
-    rowp[5 + j] = (float)ddiv(v, max_range);
-    atomicMin(&ws.smin[e], (unsigned long long)__double_as_longlong(t + 0.0));
-  };
-
-  if (a.mode == MODE_STEP) {
-    const unsigned live_mask = __ballot_sync(SP_FULL, live);
-    // compact the live lanes into the queue list
-    if (live) ws.list[__popc(live_mask & lanemask_lt())] = lane;
-    __syncwarp();
-    ray_phase<false>(mv, d, ws, beam, __popc(live_mask), fin_obs);
-    __syncwarp();
-    if (live) {
-      const double smin = __longlong_as_double((long long)ws.smin[lane]);
-      // reward (reward.py:55-83)
-      double rew;
-      if (ev == 1) {
-        rew = -10.0;
-      } else if (ev == 2) {
-        rew = 75.0;
-      } else {
-        const double alpha = bearing_error(L.x, L.y, L.h, mc.goal_x, mc.goal_y);
-        const double d2 = cross_track(L.x, L.y, L.sx, L.sy, mc.goal_x, mc.goal_y);
-        const double r_d1 = dclip(dsub(1.0, ddiv(d1, mc.plan_dist)), 0.0, 1.0);
-        const double r_d2 = dclip(dsub(1.0, ddiv(d2, mc.plan_dist)), 0.0, 1.0);
-        const double r_v = L.vl > ddiv(L.vml, 2.0) ? 1.0 : 0.0;
-        const double r_a = dclip(dsub(1.0, ddiv(dmul(2.0, fabs(alpha)), SP_PI)), -1.0, 1.0);
-        const double r_p = smin < d.proximity ? -1.0 : 0.0;
-        rew = dadd(dadd(dadd(dadd(dmul(0.3, r_d1), dmul(0.1, r_d2)), dmul(0.3, r_v)),
-                        dmul(0.3, r_a)),
-                   dmul(0.1, r_p));
-      }
-      header_row(d, mc, L, my_stage);
-      a.rewards[row] = rew;
-      a.dones[row] = (uint8_t)(coll || arrived);
-      a.truncated[row] = (uint8_t)timed_out;
-      a.events[row] = ev;
-      // VecEnv bookkeeping (vecenv.py:96-112)
-      L.ret = dadd(L.ret, rew);
-      if (ended) {
-        d.episodes[s] += 1;
-        d.return_sum[s] = dadd(d.return_sum[s], L.ret);
-        if (ev == 2) d.arrivals[s] += 1;
-        const unsigned long long k = atomicAdd(d.rec_count, 1ull);
-        const uint64_t slot = k % d.rec_cap;
-        d.rec_ret[slot] = L.ret;
-        d.rec_key[slot] = (a.step_index << 32) | (uint64_t)row;
-        if (d.first_event[s] < 0) {
-          d.first_event[s] = ev;
-          d.first_ret[s] = L.ret;
-          d.first_steps[s] = L.step;
-        }
-        L.ret = 0.0;
-      }
-    }
-    __syncwarp();
-    // write s' rows (store_states) and, for lanes that keep running, states
-    const unsigned live_mask2 = __ballot_sync(SP_FULL, live);
-    const unsigned end_mask = __ballot_sync(SP_FULL, live && ended);
-    for (int e = 0; e < E; ++e) {
-      if (!((live_mask2 >> e) & 1u)) continue;
-      const int64_t rr = d.env_of_slot[s0 + e];
-      const float* src = ws.stage + e * D;
-      const bool keep = !((end_mask >> e) & 1u) || !d.auto_reset;
-      for (int c = lane; c < D; c += 32) {
-        const float v = src[c];
-        a.store_states[rr * D + c] = v;
-        if (keep) a.states[rr * D + c] = v;
-      }
-    }
-    __syncwarp();
-  }
-
-  // ---- resets: auto-reset of ended lanes, or reset_all ------------------
-  bool do_reset = (a.mode == MODE_RESET_ALL) ? act : (live && ended && d.auto_reset);
-  bool spawned = false;
-  if (do_reset) {
-    spawned = reset_lane(d, mv, mc, s, gid, L);
-    if (!spawned) set_error(d, SP_EMAP, row);
-  }
-  const unsigned reset_mask = __ballot_sync(SP_FULL, spawned);
-  if (reset_mask != 0u) {
-    if (spawned) {
-      draw_noise_row(d, gid, L.ctr, my_stage);  // core.py:159-160
-      ws.px[lane] = L.x; ws.py[lane] = L.y; ws.ch[lane] = L.c0; ws.sh[lane] = L.s0;
-      ws.sig[lane] = L.sig;
-      ws.smin[lane] = 0x7ff0000000000000ull;
-      ws.list[__popc(reset_mask & lanemask_lt())] = lane;
-    }
-    __syncwarp();
-    ray_phase<false>(mv, d, ws, beam, __popc(reset_mask), fin_obs);
-    __syncwarp();
-    if (spawned) header_row(d, mc, L, my_stage);
-    __syncwarp();
-    for (int e = 0; e < E; ++e) {
-      if (!((reset_mask >> e) & 1u)) continue;
-      const int64_t rr = d.env_of_slot[s0 + e];
-      const float* src = ws.stage + e * D;
-      for (int c = lane; c < D; c += 32) a.states[rr * D + c] = src[c];
-    }
-    __syncwarp();
-  }
-
-  // ---- write back the SoA state --------------------------------------------
-  if (live || spawned) {
-    d.x[s] = L.x; d.y[s] = L.y; d.h[s] = L.h; d.vl[s] = L.vl; d.va[s] = L.va;
-    d.ret[s] = (a.mode == MODE_RESET_ALL) ? 0.0 : L.ret;
-    d.ctr[s] = L.ctr;
-    d.step[s] = L.step;
-    if (L.delay > 0) d.hist[s] = L.hist0;
-    d.needs_reset[s] = (uint8_t)(spawned ? 0 : (ended ? 1 : 0));
-    if (spawned) {
-      d.sx[s] = L.sx; d.sy[s] = L.sy; d.c0[s] = L.c0; d.s0[s] = L.s0;
-      d.pk[s] = L.k; d.pdt[s] = L.dt; d.pvl[s] = L.vml; d.pva[s] = L.vma; d.psig[s] = L.sig;
-      d.delay[s] = L.delay;
-      for (int wi = 1; wi < ((L.delay + 15) >> 4); ++wi) d.hist[(int64_t)wi * d.n + s] = ~0ull;
-      if (a.mode == MODE_RESET_ALL) d.first_event[s] = -1;
-    }
-  } else if (do_reset && !spawned && act) {
-    d.ctr[s] = L.ctr;
-  }
-}
-
 // Load map m's tables (TMA bulk copy into shared memory) -- or point at HBM.
+template <bool kSmem>
 __device__ __forceinline__ MapView bind_map(const EnvDev& d, int m, uint8_t* smem_maps,
                                             uint64_t* bar, uint32_t& phase) {
   const uint8_t* src = d.maps + (size_t)m * d.map_bytes;
@@ -570,7 +360,7 @@ __device__ __forceinline__ MapView bind_map(const EnvDev& d, int m, uint8_t* sme
   mv.H = d.H;
   mv.Wb = d.Wb;
   mv.WW = d.WW;
-  if (d.smem_maps) {
+  if constexpr (kSmem) {
     __syncthreads();  // everyone is done with the previous map
     if (threadIdx.x == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -588,79 +378,327 @@ __device__ __forceinline__ MapView bind_map(const EnvDev& d, int m, uint8_t* sme
   return mv;
 }
 
-__global__ void __launch_bounds__(768, 1) env_step_kernel(const __grid_constant__ EnvDev d, const __grid_constant__ StepArgs a) {
+// core.py:114-156 for one lane (stream bound to gid); writes the episode SoA
+// fields, the obs header and the scan inputs.  false = no spawn pose.
+__device__ __forceinline__ bool reset_env(const EnvDev& d, const MapView& mv, const MapConst& mc,
+                                          int64_t s, uint32_t gid, uint64_t& ctr, const Chunk& c,
+                                          int e) {
+  const double* rg = d.ranges + (d.ranges_shared ? 0 : 12 * s);
+  // DiversityRanges.sample (params.py:112-121): U U I U U U
+  const double k = draw_uniform(stream_block(d.seed, gid, 0u, ctr++), rg[0], rg[1]);
+  const double dt = draw_uniform(stream_block(d.seed, gid, 0u, ctr++), rg[2], rg[3]);
+  const int32_t delay = (int32_t)draw_integer(stream_block(d.seed, gid, 0u, ctr++),
+                                              (int64_t)rg[4], (int64_t)rg[5] + 1);
+  const double vml = draw_uniform(stream_block(d.seed, gid, 0u, ctr++), rg[6], rg[7]);
+  const double vma = draw_uniform(stream_block(d.seed, gid, 0u, ctr++), rg[8], rg[9]);
+  const double sig = draw_uniform(stream_block(d.seed, gid, 0u, ctr++), rg[10], rg[11]);
+  // spawn rejection (core.py:135-147)
+  bool ok = false;
+  double x = 0, y = 0, th = 0;
+  for (int at = 0; at < d.spawn_attempts; ++at) {
+    x = draw_uniform(stream_block(d.seed, gid, 0u, ctr++), mc.spawn[0], mc.spawn[2]);
+    y = draw_uniform(stream_block(d.seed, gid, 0u, ctr++), mc.spawn[1], mc.spawn[3]);
+    th = draw_uniform(stream_block(d.seed, gid, 0u, ctr++), -SP_PI, SP_PI);
+    if (!disc_hits(mv, d, x, y)) {
+      ok = true;
+      break;
+    }
+  }
+  if (!ok) return false;
+  const double c0 = cos(th), s0 = sin(th);  // core.py:151-152
+  d.x[s] = x; d.y[s] = y; d.h[s] = th; d.vl[s] = 0.0; d.va[s] = 0.0;
+  d.sx[s] = x; d.sy[s] = y; d.c0[s] = c0; d.s0[s] = s0;
+  d.pk[s] = k; d.pdt[s] = dt; d.pvl[s] = vml; d.pva[s] = vma; d.psig[s] = sig;
+  d.delay[s] = delay;
+  d.step[s] = 0;
+  d.needs_reset[s] = 0;
+  for (int wi = 0; wi < ((delay + 15) >> 4); ++wi) d.hist[(int64_t)wi * d.n + s] = ~0ull;
+  float* row = c.stage + e * d.D;
+  draw_noise_row(d, gid, ctr, row);  // core.py:159-160
+  header_row(mc, x, y, bearing_error(x, y, th, mc.goal_x, mc.goal_y), c0, s0, 0.0, 0.0, vml, vma,
+             row);
+  c.px[e] = x; c.py[e] = y; c.ch[e] = c0; c.sh[e] = s0; c.sig[e] = sig;
+  c.smin[e] = 0x7ff0000000000000ull;
+  return true;
+}
+
+// Coalesced copy of staged rows (one warp per row) to (N, D) outputs:
+// out_a gets rows with sel_a[e] (all when null), out_b rows with sel_b[e].
+__device__ __forceinline__ void write_rows(const EnvDev& d, const Chunk& c, int64_t s0, int n,
+                                           const uint8_t* sel_a, float* out_a,
+                                           const uint8_t* sel_b, float* out_b) {
+  const int D = d.D;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int e = warp; e < n; e += nw) {
+    const bool wa = out_a != nullptr && (sel_a == nullptr || sel_a[e]);
+    const bool wb = out_b != nullptr && (sel_b == nullptr || sel_b[e]);
+    if (!wa && !wb) continue;
+    const int64_t rr = d.env_of_slot[s0 + e];
+    const float* src = c.stage + e * D;
+    for (int k = lane; k < D; k += 32) {
+      const float v = src[k];
+      if (wa) out_a[rr * D + k] = v;
+      if (wb) out_b[rr * D + k] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------ the kernel ---
+template <bool kSmem>
+__global__ void __launch_bounds__(768, 1)
+    env_step_kernel(const __grid_constant__ EnvDev d, const __grid_constant__ StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   double2* beam = (double2*)(smem + d.off_beam);
   uint64_t* bar = (uint64_t*)(smem + d.off_bar);
+  uint8_t* reset_flag = smem + d.off_flags;        // chunk_cap: env resets this chunk
+  uint8_t* keep_flag = reset_flag + d.chunk_cap;   // chunk_cap: post-step row == s' row
+  const Chunk c = chunk_smem(smem + d.off_chunk, d.chunk_cap);
   for (int j = threadIdx.x; j < d.R; j += blockDim.x) beam[j] = d.beam_cs[j];
-  if (threadIdx.x == 0 && d.smem_maps) mbar_init(bar, 1);
+  if (threadIdx.x == 0 && kSmem) mbar_init(bar, 1);
   __syncthreads();
-  const WarpSmem ws = warp_smem(smem + d.off_warps + (size_t)warp * d.warp_smem, d.D);
   uint32_t phase = 0;
-  const int64_t sb = (int64_t)blockIdx.x * d.n / gridDim.x;
-  const int64_t se = (int64_t)(blockIdx.x + 1) * d.n / gridDim.x;
-  int64_t s = sb;
-  int m = 0;
-  while (s < se) {
-    while (d.map_off[m + 1] <= s) ++m;
-    const int64_t seg_end = min(se, d.map_off[m + 1]);
-    const MapView mv = bind_map(d, m, smem, bar, phase);
-    const MapConst mc = d.mconst[m];
-    const int64_t nb = (seg_end - s + d.E - 1) / d.E;
-    for (int64_t b = warp; b < nb; b += nwarps) {
-      const int64_t s0 = s + b * d.E;
-      const int E = (int)min((int64_t)d.E, seg_end - s0);
-      env_batch(d, a, mv, mc, beam, ws, s0, E, lane);
+  const int64_t sb = d.cta_begin[blockIdx.x], se = d.cta_begin[blockIdx.x + 1];
+  const int D = d.D;
+  const FinObs fin{c, D, d.max_range};
+  int m = 0, cur_map = -1;
+  MapView mv{};
+  for (int64_t s0 = sb; s0 < se;) {
+    while (d.map_off[m + 1] <= s0) ++m;
+    if (m != cur_map) {
+      mv = bind_map<kSmem>(d, m, smem, bar, phase);
+      cur_map = m;
     }
-    s = seg_end;
+    const MapConst mc = d.mconst[m];
+    const int n = (int)min((int64_t)d.chunk_cap, min(se, d.map_off[m + 1]) - s0);
+    const int e = threadIdx.x;
+    const bool act = e < n;
+    const int64_t s = s0 + e;
+    const int64_t row = act ? d.env_of_slot[s] : 0;
+    const uint32_t gid = (uint32_t)(d.env_id_offset + row);
+    uint64_t ctr = act ? d.ctr[s] : 0;
+    __syncthreads();  // the previous chunk is fully written out
+    if (threadIdx.x == 0) {
+      c.ctl[0] = 0;
+      c.ctl[1] = 0;
+    }
+    if (act) {
+      reset_flag[e] = 0;
+      keep_flag[e] = 0;
+    }
+    __syncthreads();
+
+    if (a.mode == MODE_STEP) {
+      // ---- A: physics, collision, events, noise -------------------------
+      bool live = false, ended = false;
+      int8_t ev = 0;
+      double partial = 0.0;
+      if (act) {
+        const int64_t av = a.actions[row];
+        if (av < 0 || av >= d.n_actions) {
+          set_error(d, SP_EACTION, row);
+        } else if (d.needs_reset[s]) {
+          set_error(d, SP_EEPISODE, row);
+        } else {
+          live = true;
+          double x = d.x[s], y = d.y[s], h = d.h[s], vl = d.vl[s], va = d.va[s];
+          const double k = d.pk[s], dt = d.pdt[s], vml = d.pvl[s], vma = d.pva[s];
+          const int32_t delay = d.delay[s];
+          int32_t step = d.step[s];
+          // delay queue (core.py:176-182): matured = action issued `delay` steps ago
+          uint32_t code = (uint32_t)av;
+          if (delay > 0) {
+            const int q = delay - 1;
+            const uint64_t h0 = d.hist[s];
+            const uint64_t w = q < 16 ? h0 : d.hist[(int64_t)(q >> 4) * d.n + s];
+            code = (uint32_t)(w >> (4 * (q & 15))) & 15u;
+            const int nw = (delay + 15) >> 4;
+            uint64_t carry = (uint64_t)av;
+            for (int wi = 0; wi < nw; ++wi) {
+              const uint64_t cur = wi == 0 ? h0 : d.hist[(int64_t)wi * d.n + s];
+              d.hist[(int64_t)wi * d.n + s] = (cur << 4) | carry;
+              carry = cur >> 60;
+            }
+          }
+          const double mv_ = d.action_v[code], mw_ = d.action_w[code];
+          // apply_kinematics (kinematics.py:22-36)
+          const double omk = dsub(1.0, k);
+          vl = dclip(dadd(dmul(k, vl), dmul(omk, mv_)), -vml, vml);
+          va = dclip(dadd(dmul(k, va), dmul(omk, mw_)), -vma, vma);
+          // integrate_unicycle (kinematics.py:39-63)
+          double sin0, cos0, sin1, cos1;
+          sincos(h, &sin0, &cos0);
+          const double h1 = dadd(h, dmul(va, dt));
+          sincos(h1, &sin1, &cos1);
+          double ddx, ddy;
+          if (fabs(va) >= 1e-6) {
+            const double radius = ddiv(vl, va);
+            ddx = dmul(radius, dsub(sin1, sin0));
+            ddy = dmul(-radius, dsub(cos1, cos0));
+          } else {
+            ddx = dmul(dmul(vl, cos0), dt);
+            ddy = dmul(dmul(vl, sin0), dt);
+          }
+          x = dadd(x, ddx);
+          y = dadd(y, ddy);
+          h = wrap_angle(h1);
+          // events (core.py:189-201)
+          const bool coll = disc_hits(mv, d, x, y);
+          const double gdx = dsub(mc.goal_x, x), gdy = dsub(mc.goal_y, y);
+          const double d1 = __dsqrt_rn(dadd(dmul(gdx, gdx), dmul(gdy, gdy)));
+          const bool arrived = !coll && d1 <= mc.goal_r;
+          step += 1;
+          const bool timed_out = !coll && !arrived && step >= d.timeout;
+          ev = coll ? 1 : (arrived ? 2 : (timed_out ? 3 : 0));
+          ended = coll || arrived || timed_out;
+          // shaped reward minus the proximity term (reward.py:55-73) + obs header
+          const double alpha = bearing_error(x, y, h, mc.goal_x, mc.goal_y);
+          if (ev == 0 || ev == 3) {
+            const double d2 = cross_track(x, y, d.sx[s], d.sy[s], mc.goal_x, mc.goal_y);
+            const double r_d1 = dclip(dsub(1.0, ddiv(d1, mc.plan_dist)), 0.0, 1.0);
+            const double r_d2 = dclip(dsub(1.0, ddiv(d2, mc.plan_dist)), 0.0, 1.0);
+            const double r_v = vl > ddiv(vml, 2.0) ? 1.0 : 0.0;
+            const double r_a = dclip(dsub(1.0, ddiv(dmul(2.0, fabs(alpha)), SP_PI)), -1.0, 1.0);
+            partial = dadd(dadd(dadd(dmul(0.3, r_d1), dmul(0.1, r_d2)), dmul(0.3, r_v)),
+                           dmul(0.3, r_a));
+          }
+          float* rowp = c.stage + e * D;
+          header_row(mc, x, y, alpha, d.c0[s], d.s0[s], vl, va, vml, vma, rowp);
+          draw_noise_row(d, gid, ctr, rowp);  // core.py:237-241
+          double sh_, ch_;
+          sincos(h, &sh_, &ch_);
+          c.px[e] = x; c.py[e] = y; c.ch[e] = ch_; c.sh[e] = sh_; c.sig[e] = d.psig[s];
+          c.smin[e] = 0x7ff0000000000000ull;  // +inf
+          c.list[atomicAdd(&c.ctl[1], 1)] = e;
+          d.x[s] = x; d.y[s] = y; d.h[s] = h; d.vl[s] = vl; d.va[s] = va;
+          d.step[s] = step;
+        }
+      }
+      __syncthreads();
+      // ---- B: LiDAR rays ---------------------------------------------------
+      ray_phase<false>(mv, d, c, beam, c.ctl[1], fin);
+      __syncthreads();
+      // ---- C: reward, outputs, statistics ------------------------------------
+      if (live) {
+        const double smin = __longlong_as_double((long long)c.smin[e]);
+        const double rew = ev == 1 ? -10.0
+                         : ev == 2 ? 75.0
+                                   : dadd(partial, dmul(0.1, smin < d.proximity ? -1.0 : 0.0));
+        a.rewards[row] = rew;
+        a.dones[row] = (uint8_t)(ev == 1 || ev == 2);
+        a.truncated[row] = (uint8_t)(ev == 3);
+        a.events[row] = ev;
+        double ret = dadd(d.ret[s], rew);  // vecenv.py:96-112
+        if (ended) {
+          d.episodes[s] += 1;
+          d.return_sum[s] = dadd(d.return_sum[s], ret);
+          if (ev == 2) d.arrivals[s] += 1;
+          const unsigned long long k = atomicAdd(d.rec_count, 1ull);
+          d.rec_ret[k % d.rec_cap] = ret;
+          d.rec_key[k % d.rec_cap] = (a.step_index << 32) | (uint64_t)row;
+          if (d.first_event[s] < 0) {
+            d.first_event[s] = ev;
+            d.first_ret[s] = ret;
+            d.first_steps[s] = d.step[s];
+          }
+          ret = 0.0;
+          d.needs_reset[s] = 1;
+          if (d.auto_reset) reset_flag[e] = 1;
+        }
+        keep_flag[e] = !(ended && d.auto_reset);
+        d.ret[s] = ret;
+      }
+      const int n_reset = __syncthreads_count(act && reset_flag[e]);
+      // s' rows of every live env; post-step rows of the ones that keep running
+      write_rows(d, c, s0, n, keep_flag, a.states, keep_flag, a.store_states);
+      write_rows(d, c, s0, n, reset_flag, a.store_states, nullptr, nullptr);
+      if (n_reset == 0) {
+        if (act) d.ctr[s] = ctr;
+        s0 += n;
+        continue;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        c.ctl[0] = 0;
+        c.ctl[1] = 0;
+      }
+      __syncthreads();
+    } else if (act) {
+      reset_flag[e] = 1;  // reset_all: every env
+    }
+
+    // ---- D: resets (auto-reset of finished envs, or reset_all) -------------
+    if (act && reset_flag[e]) {
+      if (reset_env(d, mv, mc, s, gid, ctr, c, e)) {
+        c.list[atomicAdd(&c.ctl[1], 1)] = e;
+        if (a.mode == MODE_RESET_ALL) {
+          d.ret[s] = 0.0;
+          d.first_event[s] = -1;
+        }
+      } else {
+        set_error(d, SP_EMAP, row);
+        reset_flag[e] = 0;
+      }
+    }
+    if (act) d.ctr[s] = ctr;
+    __syncthreads();
+    ray_phase<false>(mv, d, c, beam, c.ctl[1], fin);
+    __syncthreads();
+    write_rows(d, c, s0, n, reset_flag, a.states, nullptr, nullptr);
+    s0 += n;
   }
 }
 
 // Standalone LiDAR scan on caller poses (cfg4): the same marcher, no noise.
-__global__ void __launch_bounds__(768, 1) env_scan_kernel(const __grid_constant__ EnvDev d, const __grid_constant__ ScanArgs q) {
+struct FinScan {
+  double* ranges;
+  int32_t* hit_cell;
+  int64_t s0;
+  int R;
+  __device__ __forceinline__ void operator()(int e, int j, double t, int hit) const {
+    const int64_t o = (s0 + e) * R + j;
+    ranges[o] = t;
+    if (hit_cell) hit_cell[o] = hit;
+  }
+};
+
+template <bool kSmem>
+__global__ void __launch_bounds__(768, 1)
+    env_scan_kernel(const __grid_constant__ EnvDev d, const __grid_constant__ ScanArgs q) {
   extern __shared__ __align__(128) uint8_t smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   double2* beam = (double2*)(smem + d.off_beam);
   uint64_t* bar = (uint64_t*)(smem + d.off_bar);
+  const Chunk c = chunk_smem(smem + d.off_chunk, d.chunk_cap);
   for (int j = threadIdx.x; j < d.R; j += blockDim.x) beam[j] = d.beam_cs[j];
-  if (threadIdx.x == 0 && d.smem_maps) mbar_init(bar, 1);
+  if (threadIdx.x == 0 && kSmem) mbar_init(bar, 1);
   __syncthreads();
-  const WarpSmem ws = warp_smem(smem + d.off_warps + (size_t)warp * d.warp_smem, d.D);
   uint32_t phase = 0;
-  const int64_t sb = (int64_t)blockIdx.x * q.n / gridDim.x;
-  const int64_t se = (int64_t)(blockIdx.x + 1) * q.n / gridDim.x;
-  int64_t s = sb;
-  int m = 0;
-  const int R = d.R;
-  while (s < se) {
-    while (q.qoff[m + 1] <= s) ++m;
-    const int64_t seg_end = min(se, q.qoff[m + 1]);
-    const MapView mv = bind_map(d, m, smem, bar, phase);
-    const int64_t nb = (seg_end - s + d.E - 1) / d.E;
-    for (int64_t b = warp; b < nb; b += nwarps) {
-      const int64_t s0 = s + b * d.E;
-      const int E = (int)min((int64_t)d.E, seg_end - s0);
-      if (lane < E) {
-        double sh_, ch_;
-        sincos(q.h[s0 + lane], &sh_, &ch_);
-        ws.px[lane] = q.x[s0 + lane];
-        ws.py[lane] = q.y[s0 + lane];
-        ws.ch[lane] = ch_;
-        ws.sh[lane] = sh_;
-        ws.list[lane] = lane;
-      }
-      __syncwarp();
-      auto fin = [&](int e, int j, double t, int hit) {
-        const int64_t o = (s0 + e) * R + j;
-        q.ranges[o] = t;
-        if (q.hit_cell) q.hit_cell[o] = hit;
-      };
-      ray_phase<true>(mv, d, ws, beam, E, fin);
-      __syncwarp();
+  const int64_t sb = q.cta_begin[blockIdx.x], se = q.cta_begin[blockIdx.x + 1];
+  int m = 0, cur_map = -1;
+  MapView mv{};
+  for (int64_t s0 = sb; s0 < se;) {
+    while (q.qoff[m + 1] <= s0) ++m;
+    if (m != cur_map) {
+      mv = bind_map<kSmem>(d, m, smem, bar, phase);
+      cur_map = m;
     }
-    s = seg_end;
+    const int n = (int)min((int64_t)d.chunk_cap, min(se, q.qoff[m + 1]) - s0);
+    __syncthreads();
+    if (threadIdx.x == 0) c.ctl[0] = 0;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+      double sh_, ch_;
+      sincos(q.h[s0 + e], &sh_, &ch_);
+      c.px[e] = q.x[s0 + e];
+      c.py[e] = q.y[s0 + e];
+      c.ch[e] = ch_;
+      c.sh[e] = sh_;
+      c.list[e] = e;
+    }
+    __syncthreads();
+    const FinScan fin{q.ranges, q.hit_cell, s0, d.R};
+    ray_phase<true>(mv, d, c, beam, n, fin);
+    s0 += n;
   }
 }
 
 }  // namespace sp
+

@@ -51,10 +51,13 @@ struct EnvDev {
   uint64_t rec_cap;
   int32_t* err;           // [0] status, [1] env row
   // launch geometry
-  int32_t E;              // lanes (envs) per warp batch, <= 32
-  uint32_t warp_smem;     // bytes of per-warp scratch
-  uint32_t off_beam, off_warps, off_bar;  // smem offsets
+  const int64_t* cta_begin;  // grid + 1 slot boundaries (map-aligned when possible)
+  int32_t chunk_cap;      // envs per CTA chunk (<= threads per CTA)
+  uint32_t off_beam, off_bar, off_flags, off_chunk;  // smem offsets
   int32_t smem_maps;      // 1: tables staged in shared memory via TMA bulk copy
+  int32_t refill_min;     // ray queue: refill a warp once this many lanes idle
+  int32_t r_shift;        // q / R: shift when R is a power of two, else -1
+  uint64_t r_magic;       // ceil(2^40 / R) for R < 512 (else 0: plain division)
 };
 
 enum { MODE_STEP = 0, MODE_RESET_ALL = 1 };
@@ -73,6 +76,7 @@ struct StepArgs {
 
 struct ScanArgs {
   int64_t n;
+  const int64_t* cta_begin;     // grid + 1 query boundaries
   const int64_t* qoff;          // n_maps + 1 query ranges (device copy)
   const double *x, *y, *h;
   double* ranges;
