@@ -109,6 +109,9 @@ struct SpEnv {
   size_t smem = 0;
   int n_sm = 0, smem_optin = 0;
   int32_t* h_err = nullptr;  // pinned
+  int64_t* h_scan = nullptr;  // pinned staging for scan offsets (n_maps + 1 + n_sm + 1)
+  int64_t* d_scan = nullptr;
+  cudaEvent_t scan_copied = nullptr;
   std::mutex mu;
 
   template <class T>
@@ -124,6 +127,8 @@ struct SpEnv {
   ~SpEnv() {
     for (void* p : allocs) cudaFree(p);
     if (h_err) cudaFreeHost(h_err);
+    if (h_scan) cudaFreeHost(h_scan);
+    if (scan_copied) cudaEventDestroy(scan_copied);
   }
 };
 
@@ -142,7 +147,7 @@ struct SpReplay {
 
 // Launch geometry shared by the step and scan kernels.
 struct Plan {
-  int grid = 1, threads = 768, chunk_cap = 1, smem_maps = 1;
+  int grid = 1, threads = 768, chunk_cap = 1, slot_cap = 33, smem_maps = 1;
   size_t smem = 0;
   std::vector<int64_t> cta_begin;  // grid + 1
 };
@@ -194,27 +199,34 @@ static std::vector<int64_t> cta_ranges(const std::vector<int64_t>& off, int G) {
   return b;
 }
 
-static Plan plan_launch(SpEnv* env, const std::vector<int64_t>& off) {
+// shared-memory bytes of a chunk with `cap` envs (layout of chunk_smem)
+static size_t chunk_bytes(int cap, int D) {
+  const size_t slots = (size_t)cap + std::max(32, cap / 8);
+  return slots * (57 + 4 * (size_t)D) + 5 * (size_t)cap + 16;
+}
+
+static Plan plan_launch(SpEnv* env, const std::vector<int64_t>& off, bool staging = true) {
   const EnvDev& d = env->d;
+  const int D = staging ? d.D : 0;  // the scan kernel stages nothing
   Plan p;
   const int64_t lanes = off.back() - off.front();
-  const size_t per_env = 6 * 8 + 4 + 2 + (size_t)d.D * 4;
   const size_t fixed = align_up((size_t)d.R * 16, 128) + 128;
   const size_t budget = (size_t)env->smem_optin - 1024;
   size_t map_bytes = align_up(d.map_bytes, 128);
   p.threads = kMaxWarps * 32;
-  size_t room = budget > fixed + map_bytes ? budget - fixed - map_bytes : 0;
-  if (room / per_env < 128) {  // map does not fit next to a useful chunk: read tables via L1/L2
-    p.smem_maps = 0;
+  if (map_bytes + fixed + chunk_bytes(128, D) + 128 > budget) {
+    p.smem_maps = 0;  // map does not fit next to a useful chunk: read tables via L1/L2
     map_bytes = 0;
-    room = budget - fixed;
   }
-  p.chunk_cap = (int)std::max<size_t>(1, std::min<size_t>(p.threads, room / per_env));
+  const size_t room = budget - fixed - map_bytes - 128;
+  int cap = p.threads;
+  while (cap > 1 && chunk_bytes(cap, D) > room) cap -= 16;
+  p.chunk_cap = std::max(1, cap);
+  p.slot_cap = p.chunk_cap + std::max(32, p.chunk_cap / 8);
   p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(env->n_sm, (lanes + 15) / 16));
   p.cta_begin = cta_ranges(off, p.grid);
   p.grid = (int)p.cta_begin.size() - 1;
-  p.smem = map_bytes + fixed + 2 * align_up((size_t)p.chunk_cap, 16) +
-           align_up((size_t)p.chunk_cap * per_env + 16, 128);
+  p.smem = map_bytes + fixed + align_up(chunk_bytes(p.chunk_cap, D), 128);
   return p;
 }
 
@@ -222,9 +234,9 @@ static void apply_plan(const Plan& p, EnvDev& d) {
   const size_t map_region = p.smem_maps ? align_up(d.map_bytes, 128) : 0;
   d.off_beam = (uint32_t)map_region;
   d.off_bar = (uint32_t)(map_region + align_up((size_t)d.R * 16, 128));
-  d.off_flags = d.off_bar + 128;
-  d.off_chunk = (uint32_t)align_up(d.off_flags + 2 * align_up((size_t)p.chunk_cap, 16), 128);
+  d.off_chunk = d.off_bar + 128;
   d.chunk_cap = p.chunk_cap;
+  d.slot_cap = p.slot_cap;
   d.smem_maps = p.smem_maps;
 }
 
@@ -398,7 +410,13 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   TRY(env->alloc(&d.rec_count, 1));
   TRY(env->alloc(&d.err, 4));
 #undef TRY
-  if (cudaMallocHost(&env->h_err, 16) != cudaSuccess) { delete env; return fail(SP_ENOMEM, "pinned alloc"); }
+  if (cudaMallocHost(&env->h_err, 16) != cudaSuccess ||
+      cudaMallocHost(&env->h_scan, 8 * (size_t)(n_maps + env->n_sm + 2)) != cudaSuccess ||
+      env->alloc(&env->d_scan, (size_t)(n_maps + env->n_sm + 2)) != SP_OK ||
+      cudaEventCreateWithFlags(&env->scan_copied, cudaEventDisableTiming) != cudaSuccess) {
+    delete env;
+    return fail(SP_ENOMEM, "pinned alloc");
+  }
   cudaMemcpy(dmaps, host_maps.data(), host_maps.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(dmc, mconst.data(), sizeof(MapConst) * n_maps, cudaMemcpyHostToDevice);
   cudaMemcpy(dmoff, env->map_off.data(), sizeof(int64_t) * (n_maps + 1), cudaMemcpyHostToDevice);
@@ -416,6 +434,9 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
     const int R = env->R;
     d.r_shift = (R & (R - 1)) == 0 ? __builtin_ctz((unsigned)R) : -1;
     d.r_magic = (d.r_shift < 0 && R < 512) ? (((uint64_t)1 << 40) + R - 1) / R : 0;
+    d.nb = (R + 3) / 4;
+    d.nb_shift = (d.nb & (d.nb - 1)) == 0 ? __builtin_ctz((unsigned)d.nb) : -1;
+    d.inv_max_range = 1.0 / cfg->max_range_cm;
     const char* rm = std::getenv("SPARROW_REFILL_MIN");
     d.refill_min = rm ? std::max(1, std::min(32, std::atoi(rm))) : 16;
   }
@@ -681,23 +702,23 @@ int sp_env_scan(SpEnv* env, int64_t n, const int64_t* query_offsets, const doubl
   std::lock_guard<std::mutex> lk(env->mu);
   cudaStream_t st = (cudaStream_t)stream;
   std::vector<int64_t> off(query_offsets, query_offsets + env->n_maps + 1);
-  Plan plan = plan_launch(env, off);
+  Plan plan = plan_launch(env, off, false);
   EnvDev d = env->d;
   apply_plan(plan, d);
+  d.D = 0;  // chunk layout without staging rows
   const size_t nq = off.size(), nc = plan.cta_begin.size();
-  int64_t* dq = nullptr;
-  SP_CUDA(cudaMallocAsync((void**)&dq, 8 * (nq + nc), st));
-  SP_CUDA(cudaMemcpyAsync(dq, off.data(), 8 * nq, cudaMemcpyHostToDevice, st));
-  SP_CUDA(cudaMemcpyAsync(dq + nq, plan.cta_begin.data(), 8 * nc, cudaMemcpyHostToDevice, st));
-  ScanArgs q{n, dq + nq, dq, x, y, heading, ranges, hit_cell};
+  // stage the offsets through pinned memory; wait only for the previous copy
+  SP_CUDA(cudaEventSynchronize(env->scan_copied));
+  std::memcpy(env->h_scan, off.data(), 8 * nq);
+  std::memcpy(env->h_scan + nq, plan.cta_begin.data(), 8 * nc);
+  SP_CUDA(cudaMemcpyAsync(env->d_scan, env->h_scan, 8 * (nq + nc), cudaMemcpyHostToDevice, st));
+  SP_CUDA(cudaEventRecord(env->scan_copied, st));
+  ScanArgs q{n, env->d_scan + nq, env->d_scan, x, y, heading, ranges, hit_cell};
   if (d.smem_maps)
     env_scan_kernel<true><<<plan.grid, plan.threads, plan.smem, st>>>(d, q);
   else
     env_scan_kernel<false><<<plan.grid, plan.threads, plan.smem, st>>>(d, q);
-  // the copies above read pageable host memory: keep `off`/`plan` alive until they land
-  SP_CUDA(cudaStreamSynchronize(st));
   cudaError_t e = cudaGetLastError();
-  cudaFreeAsync(dq, st);
   if (e != cudaSuccess) return fail(SP_ECUDA, std::string("env_scan_kernel: ") + cudaGetErrorString(e));
   return SP_OK;
 }

@@ -197,26 +197,36 @@ __device__ __forceinline__ bool ray_setup(Ray& r, double x0, double y0, double c
   return false;
 }
 
-// Per-CTA chunk scratch (shared memory).
+// Per-CTA chunk scratch (shared memory).  A chunk holds up to `cap` envs;
+// its scans use "slots": slot e (< cap) is env e's post-step scan, slots
+// cap .. cap+extra-1 are post-reset scans of envs that finished this step.
 struct Chunk {
-  double *px, *py, *ch, *sh, *sig;
-  unsigned long long* smin;
-  int32_t* list;   // chunk-local env of each group of R rays (queue order)
-  int* ctl;        // [0] ray-queue head, [1] list length
-  float* stage;    // chunk x D staging rows
+  double *px, *py, *ch, *sh, *sig;  // per slot: scan origin, heading cos/sin, noise std
+  uint64_t* nctr;  // per slot: first Philox block of the slot's LiDAR noise
+  uint32_t* gid;   // per slot: the env's stream lane (global env id)
+  int32_t* list;   // queue order: slot of each group of R rays
+  int32_t* xslot;  // per env: post-reset slot, -1 if none
+  uint8_t* wmode;  // per env: which rows to write (see kernel)
+  uint8_t* prox;   // per slot: some ray ended closer than the proximity range
+  int* ctl;        // [0] ray-queue head [1] slots listed [2] extra slots used [3] overflow
+  float* stage;    // slots x D staging rows
 };
 
-__device__ __forceinline__ Chunk chunk_smem(uint8_t* base, int cap) {
+__device__ __forceinline__ Chunk chunk_smem(uint8_t* base, int cap, int slots, int D) {
   Chunk c;
   c.px = (double*)base;
-  c.py = c.px + cap;
-  c.ch = c.py + cap;
-  c.sh = c.ch + cap;
-  c.sig = c.sh + cap;
-  c.smin = (unsigned long long*)(c.sig + cap);
-  c.list = (int32_t*)(c.smin + cap);
-  c.ctl = c.list + cap;
-  c.stage = (float*)(c.ctl + 4);
+  c.py = c.px + slots;
+  c.ch = c.py + slots;
+  c.sh = c.ch + slots;
+  c.sig = c.sh + slots;
+  c.nctr = (uint64_t*)(c.sig + slots);
+  c.stage = (float*)(c.nctr + slots);
+  c.gid = (uint32_t*)(c.stage + (size_t)slots * D);
+  c.list = (int32_t*)(c.gid + slots);
+  c.xslot = c.list + slots;
+  c.ctl = c.xslot + cap;
+  c.wmode = (uint8_t*)(c.ctl + 4);
+  c.prox = c.wmode + cap;
   return c;
 }
 
@@ -291,17 +301,23 @@ __device__ __forceinline__ void set_error(const EnvDev& d, int code, int64_t row
   if (atomicCAS(d.err, 0, code) == 0) d.err[1] = (int32_t)row;
 }
 
-// Standard normals for one staging row (core.py:240 draws), stored as z.
-__device__ __forceinline__ void draw_noise_row(const EnvDev& d, uint32_t gid, uint64_t& ctr,
-                                               float* row) {
-  const int R = d.R;
-  for (int j = 0; j < R; j += 4) {
-    const Block4 b = stream_block(d.seed, gid, 0u, ctr++);
+// LiDAR noise (core.py:237-241): every listed slot needs R standard normals
+// from blocks nctr[slot] .. nctr[slot]+nb-1 of its stream.  One work item per
+// Philox block, spread over the whole CTA; z is staged in the obs row.
+__device__ __forceinline__ void noise_phase(const EnvDev& d, const Chunk& c, int n_slots) {
+  const int nb = d.nb, R = d.R, D = d.D;
+  const int items = n_slots * nb;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int k = d.nb_shift >= 0 ? (it >> d.nb_shift) : it / nb;
+    const int b = it - k * nb;
+    const int slot = c.list[k];
+    const Block4 blk = stream_block(d.seed, c.gid[slot], 0u, c.nctr[slot] + (uint64_t)b);
     float z[4];
-    draw_normals4(b, z);
+    draw_normals4(blk, z);
+    float* row = c.stage + slot * D + 5 + 4 * b;
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (j + u < R) row[5 + j + u] = z[u];
+      if (4 * b + u < R) row[u] = z[u];
   }
 }
 
@@ -335,18 +351,27 @@ __device__ __forceinline__ void header_row(const MapConst& mc, double x, double 
   row[4] = (float)ddiv(va, vma);
 }
 
-// Finish functor of the step/reset ray phases: noisy normalized obs into the
-// staging row (core.py:237-241, 257) and the noise-free minimum (core.py:205).
+// v / m for v in [0, m] from the reciprocal plus one exact-residual correction
+// (Markstein): the correctly rounded quotient without a DDIV.
+__device__ __forceinline__ double div_by(double v, double m, double inv_m) {
+  const double q = v * inv_m;
+  const double r = fma(-q, m, v);
+  return fma(r, inv_m, q);
+}
+
+// Finish functor of the ray phase: noisy normalized obs into the staging row
+// (core.py:237-241, 257) and the proximity flag (reward.py:70: scan_min < 30
+// is "some ray < 30", core.py:205).
 struct FinObs {
   Chunk c;
   int D;
-  double max_range;
-  __device__ __forceinline__ void operator()(int e, int j, double t, int) const {
-    float* rowp = c.stage + e * D;
+  double max_range, inv_max_range, proximity;
+  __device__ __forceinline__ void operator()(int slot, int j, double t, int) const {
+    float* rowp = c.stage + slot * D;
     const double z = (double)rowp[5 + j];
-    const double v = dclip(dadd(t, dadd(0.0, dmul(c.sig[e], z))), 0.0, max_range);
-    rowp[5 + j] = (float)ddiv(v, max_range);
-    atomicMin(&c.smin[e], (unsigned long long)__double_as_longlong(t + 0.0));
+    const double v = dclip(dadd(t, dadd(0.0, dmul(c.sig[slot], z))), 0.0, max_range);
+    rowp[5 + j] = (float)div_by(v, max_range, inv_max_range);
+    if (t < proximity) c.prox[slot] = 1;
   }
 };
 
@@ -378,11 +403,22 @@ __device__ __forceinline__ MapView bind_map(const EnvDev& d, int m, uint8_t* sme
   return mv;
 }
 
-// core.py:114-156 for one lane (stream bound to gid); writes the episode SoA
-// fields, the obs header and the scan inputs.  false = no spawn pose.
+// Register a scan slot: origin, heading, noise stream position; queue it.
+__device__ __forceinline__ void add_slot(const Chunk& c, int slot, double x, double y, double ch,
+                                         double sh, double sig, uint32_t gid, uint64_t nctr) {
+  c.px[slot] = x; c.py[slot] = y; c.ch[slot] = ch; c.sh[slot] = sh; c.sig[slot] = sig;
+  c.gid[slot] = gid;
+  c.nctr[slot] = nctr;
+  c.prox[slot] = 0;
+  c.list[atomicAdd(&c.ctl[1], 1)] = slot;
+}
+
+// core.py:114-156 for one lane (stream bound to gid): resample, spawn, write
+// the episode SoA fields and the obs header of `slot`, queue its scan (the
+// noise blocks follow the reset draws, core.py:159-160).  false = no spawn.
 __device__ __forceinline__ bool reset_env(const EnvDev& d, const MapView& mv, const MapConst& mc,
                                           int64_t s, uint32_t gid, uint64_t& ctr, const Chunk& c,
-                                          int e) {
+                                          int slot) {
   const double* rg = d.ranges + (d.ranges_shared ? 0 : 12 * s);
   // DiversityRanges.sample (params.py:112-121): U U I U U U
   const double k = draw_uniform(stream_block(d.seed, gid, 0u, ctr++), rg[0], rg[1]);
@@ -405,7 +441,8 @@ __device__ __forceinline__ bool reset_env(const EnvDev& d, const MapView& mv, co
     }
   }
   if (!ok) return false;
-  const double c0 = cos(th), s0 = sin(th);  // core.py:151-152
+  double s0, c0;
+  sincos(th, &s0, &c0);  // core.py:151-152
   d.x[s] = x; d.y[s] = y; d.h[s] = th; d.vl[s] = 0.0; d.va[s] = 0.0;
   d.sx[s] = x; d.sy[s] = y; d.c0[s] = c0; d.s0[s] = s0;
   d.pk[s] = k; d.pdt[s] = dt; d.pvl[s] = vml; d.pva[s] = vma; d.psig[s] = sig;
@@ -413,32 +450,38 @@ __device__ __forceinline__ bool reset_env(const EnvDev& d, const MapView& mv, co
   d.step[s] = 0;
   d.needs_reset[s] = 0;
   for (int wi = 0; wi < ((delay + 15) >> 4); ++wi) d.hist[(int64_t)wi * d.n + s] = ~0ull;
-  float* row = c.stage + e * d.D;
-  draw_noise_row(d, gid, ctr, row);  // core.py:159-160
   header_row(mc, x, y, bearing_error(x, y, th, mc.goal_x, mc.goal_y), c0, s0, 0.0, 0.0, vml, vma,
-             row);
-  c.px[e] = x; c.py[e] = y; c.ch[e] = c0; c.sh[e] = s0; c.sig[e] = sig;
-  c.smin[e] = 0x7ff0000000000000ull;
+             c.stage + slot * d.D);
+  add_slot(c, slot, x, y, c0, s0, sig, gid, ctr);
+  ctr += d.nb;
   return true;
 }
 
-// Coalesced copy of staged rows (one warp per row) to (N, D) outputs:
-// out_a gets rows with sel_a[e] (all when null), out_b rows with sel_b[e].
-__device__ __forceinline__ void write_rows(const EnvDev& d, const Chunk& c, int64_t s0, int n,
-                                           const uint8_t* sel_a, float* out_a,
-                                           const uint8_t* sel_b, float* out_b) {
+// Row write modes (per env, Chunk::wmode)
+enum : uint8_t {
+  W_NONE = 0,      // no output (invalid action / waiting for a reset)
+  W_KEEP = 1,      // s' row == post-step row: stage[e] -> store_states, states
+  W_RESET_X = 2,   // stage[e] -> store_states, stage[xslot[e]] -> states
+  W_RESET_OV = 3,  // stage[e] -> store_states; states after the overflow pass
+  W_STATE = 4      // stage[e] -> states only (reset_all, overflow pass)
+};
+
+// Coalesced row writes, one warp per env row.
+__device__ __forceinline__ void write_rows(const EnvDev& d, const StepArgs& a, const Chunk& c,
+                                           int64_t s0, int n) {
   const int D = d.D;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int e = warp; e < n; e += nw) {
-    const bool wa = out_a != nullptr && (sel_a == nullptr || sel_a[e]);
-    const bool wb = out_b != nullptr && (sel_b == nullptr || sel_b[e]);
-    if (!wa && !wb) continue;
+    const uint8_t w = c.wmode[e];
+    if (w == W_NONE) continue;
     const int64_t rr = d.env_of_slot[s0 + e];
-    const float* src = c.stage + e * D;
+    const float* own = c.stage + e * D;
+    const float* post = w == W_RESET_X ? c.stage + c.xslot[e] * D : own;
+    float* st = a.states + rr * D;
+    float* ss = a.store_states + rr * D;
     for (int k = lane; k < D; k += 32) {
-      const float v = src[k];
-      if (wa) out_a[rr * D + k] = v;
-      if (wb) out_b[rr * D + k] = v;
+      if (w != W_STATE) ss[k] = own[k];
+      if (w != W_RESET_OV) st[k] = post[k];
     }
   }
 }
@@ -450,16 +493,14 @@ __global__ void __launch_bounds__(768, 1)
   extern __shared__ __align__(128) uint8_t smem[];
   double2* beam = (double2*)(smem + d.off_beam);
   uint64_t* bar = (uint64_t*)(smem + d.off_bar);
-  uint8_t* reset_flag = smem + d.off_flags;        // chunk_cap: env resets this chunk
-  uint8_t* keep_flag = reset_flag + d.chunk_cap;   // chunk_cap: post-step row == s' row
-  const Chunk c = chunk_smem(smem + d.off_chunk, d.chunk_cap);
+  const Chunk c = chunk_smem(smem + d.off_chunk, d.chunk_cap, d.slot_cap, d.D);
   for (int j = threadIdx.x; j < d.R; j += blockDim.x) beam[j] = d.beam_cs[j];
   if (threadIdx.x == 0 && kSmem) mbar_init(bar, 1);
   __syncthreads();
   uint32_t phase = 0;
   const int64_t sb = d.cta_begin[blockIdx.x], se = d.cta_begin[blockIdx.x + 1];
   const int D = d.D;
-  const FinObs fin{c, D, d.max_range};
+  const FinObs fin{c, D, d.max_range, d.inv_max_range, d.proximity};
   int m = 0, cur_map = -1;
   MapView mv{};
   for (int64_t s0 = sb; s0 < se;) {
@@ -477,173 +518,182 @@ __global__ void __launch_bounds__(768, 1)
     const uint32_t gid = (uint32_t)(d.env_id_offset + row);
     uint64_t ctr = act ? d.ctr[s] : 0;
     __syncthreads();  // the previous chunk is fully written out
-    if (threadIdx.x == 0) {
-      c.ctl[0] = 0;
-      c.ctl[1] = 0;
-    }
-    if (act) {
-      reset_flag[e] = 0;
-      keep_flag[e] = 0;
-    }
+    if (threadIdx.x < 4) c.ctl[threadIdx.x] = 0;
     __syncthreads();
 
-    if (a.mode == MODE_STEP) {
-      // ---- A: physics, collision, events, noise -------------------------
-      bool live = false, ended = false;
-      int8_t ev = 0;
-      double partial = 0.0;
-      if (act) {
-        const int64_t av = a.actions[row];
-        if (av < 0 || av >= d.n_actions) {
-          set_error(d, SP_EACTION, row);
-        } else if (d.needs_reset[s]) {
-          set_error(d, SP_EEPISODE, row);
-        } else {
-          live = true;
-          double x = d.x[s], y = d.y[s], h = d.h[s], vl = d.vl[s], va = d.va[s];
-          const double k = d.pk[s], dt = d.pdt[s], vml = d.pvl[s], vma = d.pva[s];
-          const int32_t delay = d.delay[s];
-          int32_t step = d.step[s];
-          // delay queue (core.py:176-182): matured = action issued `delay` steps ago
-          uint32_t code = (uint32_t)av;
-          if (delay > 0) {
-            const int q = delay - 1;
-            const uint64_t h0 = d.hist[s];
-            const uint64_t w = q < 16 ? h0 : d.hist[(int64_t)(q >> 4) * d.n + s];
-            code = (uint32_t)(w >> (4 * (q & 15))) & 15u;
-            const int nw = (delay + 15) >> 4;
-            uint64_t carry = (uint64_t)av;
-            for (int wi = 0; wi < nw; ++wi) {
-              const uint64_t cur = wi == 0 ? h0 : d.hist[(int64_t)wi * d.n + s];
-              d.hist[(int64_t)wi * d.n + s] = (cur << 4) | carry;
-              carry = cur >> 60;
-            }
-          }
-          const double mv_ = d.action_v[code], mw_ = d.action_w[code];
-          // apply_kinematics (kinematics.py:22-36)
-          const double omk = dsub(1.0, k);
-          vl = dclip(dadd(dmul(k, vl), dmul(omk, mv_)), -vml, vml);
-          va = dclip(dadd(dmul(k, va), dmul(omk, mw_)), -vma, vma);
-          // integrate_unicycle (kinematics.py:39-63)
-          double sin0, cos0, sin1, cos1;
-          sincos(h, &sin0, &cos0);
-          const double h1 = dadd(h, dmul(va, dt));
-          sincos(h1, &sin1, &cos1);
-          double ddx, ddy;
-          if (fabs(va) >= 1e-6) {
-            const double radius = ddiv(vl, va);
-            ddx = dmul(radius, dsub(sin1, sin0));
-            ddy = dmul(-radius, dsub(cos1, cos0));
-          } else {
-            ddx = dmul(dmul(vl, cos0), dt);
-            ddy = dmul(dmul(vl, sin0), dt);
-          }
-          x = dadd(x, ddx);
-          y = dadd(y, ddy);
-          h = wrap_angle(h1);
-          // events (core.py:189-201)
-          const bool coll = disc_hits(mv, d, x, y);
-          const double gdx = dsub(mc.goal_x, x), gdy = dsub(mc.goal_y, y);
-          const double d1 = __dsqrt_rn(dadd(dmul(gdx, gdx), dmul(gdy, gdy)));
-          const bool arrived = !coll && d1 <= mc.goal_r;
-          step += 1;
-          const bool timed_out = !coll && !arrived && step >= d.timeout;
-          ev = coll ? 1 : (arrived ? 2 : (timed_out ? 3 : 0));
-          ended = coll || arrived || timed_out;
-          // shaped reward minus the proximity term (reward.py:55-73) + obs header
-          const double alpha = bearing_error(x, y, h, mc.goal_x, mc.goal_y);
-          if (ev == 0 || ev == 3) {
-            const double d2 = cross_track(x, y, d.sx[s], d.sy[s], mc.goal_x, mc.goal_y);
-            const double r_d1 = dclip(dsub(1.0, ddiv(d1, mc.plan_dist)), 0.0, 1.0);
-            const double r_d2 = dclip(dsub(1.0, ddiv(d2, mc.plan_dist)), 0.0, 1.0);
-            const double r_v = vl > ddiv(vml, 2.0) ? 1.0 : 0.0;
-            const double r_a = dclip(dsub(1.0, ddiv(dmul(2.0, fabs(alpha)), SP_PI)), -1.0, 1.0);
-            partial = dadd(dadd(dadd(dmul(0.3, r_d1), dmul(0.1, r_d2)), dmul(0.3, r_v)),
-                           dmul(0.3, r_a));
-          }
-          float* rowp = c.stage + e * D;
-          header_row(mc, x, y, alpha, d.c0[s], d.s0[s], vl, va, vml, vma, rowp);
-          draw_noise_row(d, gid, ctr, rowp);  // core.py:237-241
-          double sh_, ch_;
-          sincos(h, &sh_, &ch_);
-          c.px[e] = x; c.py[e] = y; c.ch[e] = ch_; c.sh[e] = sh_; c.sig[e] = d.psig[s];
-          c.smin[e] = 0x7ff0000000000000ull;  // +inf
-          c.list[atomicAdd(&c.ctl[1], 1)] = e;
-          d.x[s] = x; d.y[s] = y; d.h[s] = h; d.vl[s] = vl; d.va[s] = va;
-          d.step[s] = step;
-        }
-      }
-      __syncthreads();
-      // ---- B: LiDAR rays ---------------------------------------------------
-      ray_phase<false>(mv, d, c, beam, c.ctl[1], fin);
-      __syncthreads();
-      // ---- C: reward, outputs, statistics ------------------------------------
-      if (live) {
-        const double smin = __longlong_as_double((long long)c.smin[e]);
-        const double rew = ev == 1 ? -10.0
-                         : ev == 2 ? 75.0
-                                   : dadd(partial, dmul(0.1, smin < d.proximity ? -1.0 : 0.0));
-        a.rewards[row] = rew;
-        a.dones[row] = (uint8_t)(ev == 1 || ev == 2);
-        a.truncated[row] = (uint8_t)(ev == 3);
-        a.events[row] = ev;
-        double ret = dadd(d.ret[s], rew);  // vecenv.py:96-112
-        if (ended) {
-          d.episodes[s] += 1;
-          d.return_sum[s] = dadd(d.return_sum[s], ret);
-          if (ev == 2) d.arrivals[s] += 1;
-          const unsigned long long k = atomicAdd(d.rec_count, 1ull);
-          d.rec_ret[k % d.rec_cap] = ret;
-          d.rec_key[k % d.rec_cap] = (a.step_index << 32) | (uint64_t)row;
-          if (d.first_event[s] < 0) {
-            d.first_event[s] = ev;
-            d.first_ret[s] = ret;
-            d.first_steps[s] = d.step[s];
-          }
-          ret = 0.0;
-          d.needs_reset[s] = 1;
-          if (d.auto_reset) reset_flag[e] = 1;
-        }
-        keep_flag[e] = !(ended && d.auto_reset);
-        d.ret[s] = ret;
-      }
-      const int n_reset = __syncthreads_count(act && reset_flag[e]);
-      // s' rows of every live env; post-step rows of the ones that keep running
-      write_rows(d, c, s0, n, keep_flag, a.states, keep_flag, a.store_states);
-      write_rows(d, c, s0, n, reset_flag, a.store_states, nullptr, nullptr);
-      if (n_reset == 0) {
-        if (act) d.ctr[s] = ctr;
-        s0 += n;
-        continue;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        c.ctl[0] = 0;
-        c.ctl[1] = 0;
-      }
-      __syncthreads();
-    } else if (act) {
-      reset_flag[e] = 1;  // reset_all: every env
+    // ---- A: physics, collision, events, reward partial, resets -----------
+    bool live = false, ended = false;
+    int8_t ev = 0;
+    double partial = 0.0;
+    if (act) {
+      c.xslot[e] = -1;
+      c.wmode[e] = W_NONE;
     }
-
-    // ---- D: resets (auto-reset of finished envs, or reset_all) -------------
-    if (act && reset_flag[e]) {
-      if (reset_env(d, mv, mc, s, gid, ctr, c, e)) {
-        c.list[atomicAdd(&c.ctl[1], 1)] = e;
-        if (a.mode == MODE_RESET_ALL) {
+    if (a.mode == MODE_RESET_ALL) {
+      if (act) {
+        if (reset_env(d, mv, mc, s, gid, ctr, c, e)) {
+          c.wmode[e] = W_STATE;
           d.ret[s] = 0.0;
           d.first_event[s] = -1;
+        } else {
+          set_error(d, SP_EMAP, row);
         }
-      } else {
-        set_error(d, SP_EMAP, row);
-        reset_flag[e] = 0;
+        d.ctr[s] = ctr;
       }
+    } else if (act) {
+      const int64_t av = a.actions[row];
+      if (av < 0 || av >= d.n_actions) {
+        set_error(d, SP_EACTION, row);
+      } else if (d.needs_reset[s]) {
+        set_error(d, SP_EEPISODE, row);
+      } else {
+        live = true;
+        double x = d.x[s], y = d.y[s], h = d.h[s], vl = d.vl[s], va = d.va[s];
+        const double k = d.pk[s], dt = d.pdt[s], vml = d.pvl[s], vma = d.pva[s];
+        const int32_t delay = d.delay[s];
+        int32_t step = d.step[s];
+        // delay queue (core.py:176-182): matured = action issued `delay` steps ago
+        uint32_t code = (uint32_t)av;
+        if (delay > 0) {
+          const int q = delay - 1;
+          const uint64_t h0 = d.hist[s];
+          const uint64_t w = q < 16 ? h0 : d.hist[(int64_t)(q >> 4) * d.n + s];
+          code = (uint32_t)(w >> (4 * (q & 15))) & 15u;
+          const int nw = (delay + 15) >> 4;
+          uint64_t carry = (uint64_t)av;
+          for (int wi = 0; wi < nw; ++wi) {
+            const uint64_t cur = wi == 0 ? h0 : d.hist[(int64_t)wi * d.n + s];
+            d.hist[(int64_t)wi * d.n + s] = (cur << 4) | carry;
+            carry = cur >> 60;
+          }
+        }
+        const double mv_ = d.action_v[code], mw_ = d.action_w[code];
+        // apply_kinematics (kinematics.py:22-36)
+        const double omk = dsub(1.0, k);
+        vl = dclip(dadd(dmul(k, vl), dmul(omk, mv_)), -vml, vml);
+        va = dclip(dadd(dmul(k, va), dmul(omk, mw_)), -vma, vma);
+        // integrate_unicycle (kinematics.py:39-63)
+        double sin0, cos0, sin1, cos1;
+        sincos(h, &sin0, &cos0);
+        const double h1 = dadd(h, dmul(va, dt));
+        sincos(h1, &sin1, &cos1);
+        double ddx, ddy;
+        if (fabs(va) >= 1e-6) {
+          const double radius = ddiv(vl, va);
+          ddx = dmul(radius, dsub(sin1, sin0));
+          ddy = dmul(-radius, dsub(cos1, cos0));
+        } else {
+          ddx = dmul(dmul(vl, cos0), dt);
+          ddy = dmul(dmul(vl, sin0), dt);
+        }
+        x = dadd(x, ddx);
+        y = dadd(y, ddy);
+        h = wrap_angle(h1);
+        // events (core.py:189-201)
+        const bool coll = disc_hits(mv, d, x, y);
+        const double gdx = dsub(mc.goal_x, x), gdy = dsub(mc.goal_y, y);
+        const double d1 = __dsqrt_rn(dadd(dmul(gdx, gdx), dmul(gdy, gdy)));
+        const bool arrived = !coll && d1 <= mc.goal_r;
+        step += 1;
+        const bool timed_out = !coll && !arrived && step >= d.timeout;
+        ev = coll ? 1 : (arrived ? 2 : (timed_out ? 3 : 0));
+        ended = coll || arrived || timed_out;
+        // shaped reward without the proximity term (reward.py:55-73) + obs header
+        const double alpha = bearing_error(x, y, h, mc.goal_x, mc.goal_y);
+        if (ev == 0 || ev == 3) {
+          const double d2 = cross_track(x, y, d.sx[s], d.sy[s], mc.goal_x, mc.goal_y);
+          const double r_d1 = dclip(dsub(1.0, ddiv(d1, mc.plan_dist)), 0.0, 1.0);
+          const double r_d2 = dclip(dsub(1.0, ddiv(d2, mc.plan_dist)), 0.0, 1.0);
+          const double r_v = vl > ddiv(vml, 2.0) ? 1.0 : 0.0;
+          const double r_a = dclip(dsub(1.0, ddiv(dmul(2.0, fabs(alpha)), SP_PI)), -1.0, 1.0);
+          partial = dadd(dadd(dadd(dmul(0.3, r_d1), dmul(0.1, r_d2)), dmul(0.3, r_v)),
+                         dmul(0.3, r_a));
+        }
+        header_row(mc, x, y, alpha, d.c0[s], d.s0[s], vl, va, vml, vma, c.stage + e * D);
+        // the post-step scan (core.py:203-206); cos/sin of h1 == of wrap(h1)
+        add_slot(c, e, x, y, cos1, sin1, d.psig[s], gid, ctr);
+        ctr += d.nb;
+        d.x[s] = x; d.y[s] = y; d.h[s] = h; d.vl[s] = vl; d.va[s] = va;
+        d.step[s] = step;
+        c.wmode[e] = W_KEEP;
+        if (ended && d.auto_reset) {  // fused auto-reset (vecenv.py:113-114)
+          const int k2 = atomicAdd(&c.ctl[2], 1);
+          if (k2 < d.slot_cap - d.chunk_cap) {
+            const int xs = d.chunk_cap + k2;
+            if (reset_env(d, mv, mc, s, gid, ctr, c, xs)) {
+              c.xslot[e] = xs;
+              c.wmode[e] = W_RESET_X;
+            } else {
+              set_error(d, SP_EMAP, row);
+            }
+          } else {
+            c.wmode[e] = W_RESET_OV;  // extra slots exhausted: second pass below
+            atomicAdd(&c.ctl[3], 1);
+          }
+        }
+      }
+      d.ctr[s] = ctr;
     }
-    if (act) d.ctr[s] = ctr;
     __syncthreads();
-    ray_phase<false>(mv, d, c, beam, c.ctl[1], fin);
+    const int n_slots = c.ctl[1];
+    // ---- N: LiDAR noise; B: LiDAR rays --------------------------------------
+    noise_phase(d, c, n_slots);
     __syncthreads();
-    write_rows(d, c, s0, n, reset_flag, a.states, nullptr, nullptr);
+    ray_phase<false>(mv, d, c, beam, n_slots, fin);
+    __syncthreads();
+    // ---- C: reward, outputs, statistics ------------------------------------
+    if (live) {
+      const double rew = ev == 1 ? -10.0
+                       : ev == 2 ? 75.0
+                                 : dadd(partial, dmul(0.1, c.prox[e] ? -1.0 : 0.0));
+      a.rewards[row] = rew;
+      a.dones[row] = (uint8_t)(ev == 1 || ev == 2);
+      a.truncated[row] = (uint8_t)(ev == 3);
+      a.events[row] = ev;
+      double ret = dadd(d.ret[s], rew);  // vecenv.py:96-112
+      if (ended) {
+        d.episodes[s] += 1;
+        d.return_sum[s] = dadd(d.return_sum[s], ret);
+        if (ev == 2) d.arrivals[s] += 1;
+        const unsigned long long kk = atomicAdd(d.rec_count, 1ull);
+        d.rec_ret[kk % d.rec_cap] = ret;
+        d.rec_key[kk % d.rec_cap] = (a.step_index << 32) | (uint64_t)row;
+        if (d.first_event[s] < 0) {
+          d.first_event[s] = ev;
+          d.first_ret[s] = ret;
+          d.first_steps[s] = d.step[s];
+        }
+        ret = 0.0;
+        if (!d.auto_reset || c.wmode[e] == W_RESET_OV) d.needs_reset[s] = 1;
+      }
+      d.ret[s] = ret;
+    }
+    write_rows(d, a, c, s0, n);
+    // ---- overflow pass: resets that did not fit the extra slots (rare) -----
+    if (a.mode == MODE_STEP && c.ctl[3] > 0) {
+      __syncthreads();
+      if (threadIdx.x < 2) c.ctl[threadIdx.x] = 0;
+      __syncthreads();
+      if (act && c.wmode[e] == W_RESET_OV) {
+        uint64_t ctr2 = d.ctr[s];
+        if (reset_env(d, mv, mc, s, gid, ctr2, c, e)) {
+          c.wmode[e] = W_STATE;
+        } else {
+          set_error(d, SP_EMAP, row);
+          c.wmode[e] = W_NONE;
+        }
+        d.ctr[s] = ctr2;
+      } else if (act) {
+        c.wmode[e] = W_NONE;
+      }
+      __syncthreads();
+      const int n2 = c.ctl[1];
+      noise_phase(d, c, n2);
+      __syncthreads();
+      ray_phase<false>(mv, d, c, beam, n2, fin);
+      __syncthreads();
+      write_rows(d, a, c, s0, n);
+    }
     s0 += n;
   }
 }
@@ -667,7 +717,7 @@ __global__ void __launch_bounds__(768, 1)
   extern __shared__ __align__(128) uint8_t smem[];
   double2* beam = (double2*)(smem + d.off_beam);
   uint64_t* bar = (uint64_t*)(smem + d.off_bar);
-  const Chunk c = chunk_smem(smem + d.off_chunk, d.chunk_cap);
+  const Chunk c = chunk_smem(smem + d.off_chunk, d.chunk_cap, d.slot_cap, d.D);
   for (int j = threadIdx.x; j < d.R; j += blockDim.x) beam[j] = d.beam_cs[j];
   if (threadIdx.x == 0 && kSmem) mbar_init(bar, 1);
   __syncthreads();

