@@ -1,0 +1,126 @@
+"""Host-side logic of the drop-in (no GPU): map text format, parameter
+ranges, beam offsets, sharding.  Mirrors the reference's test_gridmap.py /
+params checks and is cross-checked against the reference where built."""
+
+import math
+
+import numpy as np
+import pytest
+
+from helpers import load_maps, make_map
+from oracle import oracle as O
+from paper_2305_04180_b200 import dist
+from paper_2305_04180_b200.sim import (
+    DiversityRanges,
+    EnvConfig,
+    GridMap,
+    LidarConfig,
+    MapError,
+    SimParams,
+)
+
+MAP_TEXT = """\
+8 8 1
+########
+#....GG#
+#....GG#
+#......#
+#......#
+#SS....#
+#SS....#
+########
+"""
+
+
+def test_from_text_goal_and_spawn():
+    m = GridMap.from_text(MAP_TEXT)
+    assert (m.width_cm, m.height_cm, m.cell_size_cm) == (8, 8, 1)
+    assert m.goal_center == (6.0, 6.0)
+    assert m.goal_radius_cm == pytest.approx(math.hypot(0.5, 0.5) + 0.5)
+    assert m.spawn_region == (1.0, 1.0, 3.0, 3.0)
+    assert m.occupancy[0].all() and not m.occupancy[3, 3]
+
+
+def test_text_round_trip_and_row_order():
+    m = GridMap.from_text(MAP_TEXT)
+    m2 = GridMap.from_text(m.to_text())
+    assert np.array_equal(m.occupancy, m2.occupancy)
+    assert m2.goal_center == m.goal_center and m2.spawn_region == m.spawn_region
+    t = GridMap.from_text("4 4 1\n####\n#.G#\n#S.#\n####\n")
+    assert t.spawn_region == (1.0, 1.0, 2.0, 2.0) and t.goal_center == (2.5, 2.5)
+    c = GridMap.from_text("20 20 5\n####\n#.G#\n#S.#\n####\n")
+    assert c.goal_center == (12.5, 12.5) and c.spawn_region == (5.0, 5.0, 10.0, 10.0)
+
+
+@pytest.mark.parametrize("bad", [
+    "not a header\n", "8 8 3\n", MAP_TEXT.replace("G", "."), MAP_TEXT.replace("S", "."),
+    MAP_TEXT.replace(".", "?", 1), "\n".join(MAP_TEXT.splitlines()[:-1]) + "\n"])
+def test_rejects_malformed_text(bad):
+    with pytest.raises(MapError):
+        GridMap.from_text(bad)
+
+
+def test_constructor_invariants():
+    occ = np.zeros((10, 10), dtype=bool)
+    occ[0, :] = occ[-1, :] = occ[:, 0] = occ[:, -1] = True
+    with pytest.raises(MapError):
+        GridMap(10, 10, 3, occ, (5, 5), 1.0, (1, 1, 3, 3))
+    bad = occ.copy()
+    bad[0, 4] = False
+    with pytest.raises(MapError):
+        GridMap(10, 10, 1, bad, (5, 5), 1.0, (1, 1, 3, 3))
+    with pytest.raises(MapError):
+        GridMap(10, 10, 1, occ, (15, 5), 1.0, (1, 1, 3, 3))
+    with pytest.raises(MapError):
+        GridMap(10, 10, 1, occ, (0.5, 0.5), 1.0, (1, 1, 3, 3))
+    with pytest.raises(MapError):
+        GridMap(10, 10, 1, occ, (5, 5), 1.0, (1, 1, 30, 3))
+
+
+@pytest.mark.skipif(not O.reference_available(), reason="oracle/_ref not built")
+def test_gridmap_and_params_equal_reference():
+    O.import_reference()
+    from color_rl.sim.gridmap import GridMap as RG
+    from color_rl.sim.params import DiversityRanges as RD, LidarConfig as RL, SimParams as RS
+    for m in load_maps(16):
+        t = m.to_text()
+        a, b = RG.from_text(t), GridMap.from_text(t)
+        assert a.to_text() == b.to_text()
+        assert (a.goal_center, a.goal_radius_cm, a.spawn_region) == \
+               (b.goal_center, b.goal_radius_cm, b.spawn_region)
+    for frac in (0.0, 0.1, 0.3, 0.5):
+        for d in (0, 1, 3, 40):
+            nom = SimParams(control_delay_steps=d)
+            rnom = RS(control_delay_steps=d)
+            assert DiversityRanges.around(nom, frac).__dict__ == RD.around(rnom, frac).__dict__
+    for n in (1, 27, 32, 128, 256):
+        assert np.array_equal(LidarConfig(n_beams=n).beam_offsets(), RL(n_beams=n).beam_offsets())
+
+
+def test_params_validation():
+    with pytest.raises(ValueError):
+        SimParams(k=1.0)
+    with pytest.raises(ValueError):
+        SimParams(control_delay_steps=65)
+    with pytest.raises(ValueError):
+        DiversityRanges(k=(0.7, 0.6))
+    with pytest.raises(ValueError):
+        DiversityRanges.around(SimParams(), -0.1)
+    r = DiversityRanges.around(SimParams(), 0.3)
+    assert r.control_delay_steps == (0, 2)
+
+
+def test_config_planning_distance():
+    m = make_map(40)
+    assert EnvConfig().planning_dist(m) == pytest.approx(math.hypot(40, 40))
+    assert EnvConfig(max_planning_dist_cm=100.0).planning_dist(m) == 100.0
+    assert LidarConfig(n_beams=32).state_dim == 37
+
+
+def test_shard_partitions_global_ids():
+    for total, world in ((65536 * 8, 8), (1000, 3), (5, 8)):
+        parts = [dist.shard(total, r, world) for r in range(world)]
+        ids = [i for off, n in parts for i in range(off, off + n)]
+        assert ids == list(range(total))
+    with pytest.raises(ValueError):
+        dist.shard(10, 3, 3)
