@@ -17,6 +17,8 @@
  *                       (SimBatch.step_all) incl. fused auto-reset core.py:114-161
  *   sp_env_stats_*      vecenv.py:120-141 (snapshot_stats, first_episode_outcomes)
  *   sp_env_read_state   sim/core.py:88-108 SoA attributes (read-only views)
+ *   sp_env_write_state  test-only pose placement (tests/test_env.py:37-42 place())
+ *   sp_env_reset_lanes  sim/core.py:114-161 (SimBatch.reset_lane, stream kept)
  *   sp_env_scan         sim/core.py:223-235 (SimBatch._scan) on caller poses
  *   sp_rb_create        replay.py:31-43 (ReplayBuffer.__init__)
  *   sp_rb_append        replay.py:48-67 (append_batch)
@@ -116,6 +118,12 @@ int sp_env_stats_totals(SpEnv* env, double* dev_out3, void* stream);
  * 7 k, 8 dt, 9 delay, 10 vmax_linear, 11 vmax_angular, 12 noise_std,
  * 13 step_count, 14 needs_reset, 15 rng_ctr, 16 episode_return */
 int sp_env_read_state(SpEnv* env, int field, double* host_out, void* stream);
+/* overwrite one pose field (ids 0-6 above, 17 start_cos, 18 start_sin) from a
+ * host array (external order) -- the reference tests' place() (test_env.py:37-42) */
+int sp_env_write_state(SpEnv* env, int field, const double* host_in, void* stream);
+/* SimBatch.reset_lane (core.py:114-161) for the lanes with mask[i] != 0 (device,
+ * external order), continuing each lane's stream; writes their rows of states. */
+int sp_env_reset_lanes(SpEnv* env, const uint8_t* mask, float* states, void* stream);
 int sp_env_map_info(SpEnv* env, int64_t* slot_of_env /* host n_envs, may be NULL */,
                     int64_t* smem_bytes, int32_t* threads_per_cta, int32_t* ctas);
 

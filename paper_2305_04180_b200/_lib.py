@@ -83,6 +83,8 @@ SIGNATURES = [
     ("sp_env_stats_reset", ctypes.c_int, [c_vp, ctypes.c_int, c_vp]),
     ("sp_env_stats_totals", ctypes.c_int, [c_vp, c_vp, c_vp]),
     ("sp_env_read_state", ctypes.c_int, [c_vp, ctypes.c_int, c_dp, c_vp]),
+    ("sp_env_write_state", ctypes.c_int, [c_vp, ctypes.c_int, c_dp, c_vp]),
+    ("sp_env_reset_lanes", ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     ("sp_env_map_info", ctypes.c_int, [c_vp, c_i64p, c_i64p, c_i32p, c_i32p]),
     ("sp_env_scan", ctypes.c_int, [c_vp, ctypes.c_int64, c_i64p, c_vp, c_vp, c_vp, c_vp, c_vp,
                                    c_vp]),

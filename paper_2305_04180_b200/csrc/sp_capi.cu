@@ -654,6 +654,8 @@ int sp_env_read_state(SpEnv* env, int field, double* host_out, void* stream) {
     case 11: f64 = d.pva; break;
     case 12: f64 = d.psig; break;
     case 16: f64 = d.ret; break;
+    case 17: f64 = d.c0; break;
+    case 18: f64 = d.s0; break;
     default: break;
   }
   if (f64) {
@@ -679,6 +681,42 @@ int sp_env_read_state(SpEnv* env, int field, double* host_out, void* stream) {
   SP_CUDA(cudaStreamSynchronize(st));
   for (int64_t i = 0; i < env->n; ++i) host_out[i] = tmp[env->slot_of_env[i]];
   return SP_OK;
+}
+
+int sp_env_write_state(SpEnv* env, int field, const double* host_in, void* stream) {
+  if (!env || !host_in) return fail(SP_EINVAL, "null argument");
+  DevDeviceGuard guard(env->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const EnvDev& d = env->d;
+  double* dst = nullptr;
+  switch (field) {
+    case 0: dst = d.x; break;
+    case 1: dst = d.y; break;
+    case 2: dst = d.h; break;
+    case 3: dst = d.vl; break;
+    case 4: dst = d.va; break;
+    case 5: dst = d.sx; break;
+    case 6: dst = d.sy; break;
+    case 17: dst = d.c0; break;
+    case 18: dst = d.s0; break;
+    default: return fail(SP_EINVAL, "field is not writable");
+  }
+  std::vector<double> tmp(env->n);
+  for (int64_t i = 0; i < env->n; ++i) tmp[env->slot_of_env[i]] = host_in[i];
+  SP_CUDA(cudaMemcpyAsync(dst, tmp.data(), 8 * env->n, cudaMemcpyHostToDevice, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  return SP_OK;
+}
+
+int sp_env_reset_lanes(SpEnv* env, const uint8_t* mask, float* states, void* stream) {
+  if (!env || !mask || !states) return fail(SP_EINVAL, "null argument");
+  DevDeviceGuard guard(env->device);
+  std::lock_guard<std::mutex> lk(env->mu);
+  StepArgs a{};
+  a.mode = MODE_RESET_LANES;
+  a.reset_mask = mask;
+  a.states = states;
+  return launch_env(env, a, (cudaStream_t)stream);
 }
 
 int sp_env_map_info(SpEnv* env, int64_t* slot_of_env, int64_t* smem_bytes, int32_t* threads,

@@ -524,17 +524,21 @@ __global__ void __launch_bounds__(768, 1)
     // ---- A: physics, collision, events, reward partial, resets -----------
     bool live = false, ended = false;
     int8_t ev = 0;
+    int32_t step_end = 0;  // episode length before any reset in phase A
     double partial = 0.0;
     if (act) {
       c.xslot[e] = -1;
       c.wmode[e] = W_NONE;
     }
-    if (a.mode == MODE_RESET_ALL) {
-      if (act) {
+    if (a.mode != MODE_STEP) {
+      const bool want = a.mode == MODE_RESET_ALL || (act && a.reset_mask[row] != 0);
+      if (act && want) {
         if (reset_env(d, mv, mc, s, gid, ctr, c, e)) {
           c.wmode[e] = W_STATE;
-          d.ret[s] = 0.0;
-          d.first_event[s] = -1;
+          if (a.mode == MODE_RESET_ALL) {
+            d.ret[s] = 0.0;
+            d.first_event[s] = -1;
+          }
         } else {
           set_error(d, SP_EMAP, row);
         }
@@ -615,6 +619,7 @@ __global__ void __launch_bounds__(768, 1)
         ctr += d.nb;
         d.x[s] = x; d.y[s] = y; d.h[s] = h; d.vl[s] = vl; d.va[s] = va;
         d.step[s] = step;
+        step_end = step;
         c.wmode[e] = W_KEEP;
         if (ended && d.auto_reset) {  // fused auto-reset (vecenv.py:113-114)
           const int k2 = atomicAdd(&c.ctl[2], 1);
@@ -661,7 +666,7 @@ __global__ void __launch_bounds__(768, 1)
         if (d.first_event[s] < 0) {
           d.first_event[s] = ev;
           d.first_ret[s] = ret;
-          d.first_steps[s] = d.step[s];
+          d.first_steps[s] = step_end;
         }
         ret = 0.0;
         if (!d.auto_reset || c.wmode[e] == W_RESET_OV) d.needs_reset[s] = 1;

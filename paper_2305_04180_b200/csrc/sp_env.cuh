@@ -63,12 +63,13 @@ struct EnvDev {
   uint64_t r_magic;       // ceil(2^40 / R) for R < 512 (else 0: plain division)
 };
 
-enum { MODE_STEP = 0, MODE_RESET_ALL = 1 };
+enum { MODE_STEP = 0, MODE_RESET_ALL = 1, MODE_RESET_LANES = 2 };
 
 struct StepArgs {
   int32_t mode;
   uint64_t step_index;
   const int64_t* actions;  // external order
+  const uint8_t* reset_mask;  // MODE_RESET_LANES: external order
   float* states;           // (N, D) post-reset obs
   float* store_states;     // (N, D) pre-reset s'
   double* rewards;

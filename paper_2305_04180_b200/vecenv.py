@@ -103,7 +103,8 @@ class SimView:
     names (``sim/core.py:81-108``).  Each attribute read copies to host."""
 
     _FIELDS = {"x": 0, "y": 1, "heading": 2, "start_x": 5, "start_y": 6, "param_k": 7,
-               "param_dt": 8, "param_noise": 12, "rng_ctr": 15}
+               "param_dt": 8, "param_noise": 12, "rng_ctr": 15, "start_cos": 17,
+               "start_sin": 18}
 
     def __init__(self, env: "VecEnv"):
         self._env = env
@@ -323,6 +324,33 @@ class VecEnv:
                                          out.store_states.data_ptr(), out.rewards.data_ptr(),
                                          out.dones.data_ptr(), out.truncated.data_ptr(),
                                          out.events.data_ptr(), self._stream()), "step")
+
+    def reset_lanes(self, mask):
+        """SimBatch.reset_lane (core.py:114-161) for every lane with mask[i]
+        set, continuing each lane's stream (the manual reset a caller needs
+        with auto_reset=False).  Returns the fresh (N, D) state rows (rows of
+        unmasked lanes are left unspecified)."""
+        torch = self._torch
+        m = torch.as_tensor(np.asarray(mask, dtype=np.uint8) if not isinstance(mask, torch.Tensor)
+                            else mask.to(torch.uint8)).to(self.device).reshape(-1).contiguous()
+        if m.numel() != self.n_copies:
+            raise ValueError("need one mask entry per copy")
+        states = torch.empty((self.n_copies, self.state_dim), dtype=torch.float32,
+                             device=self.device)
+        _lib.check(self._lib.sp_env_reset_lanes(self._h, m.data_ptr(), states.data_ptr(),
+                                                self._stream()), "reset_lanes")
+        self.check()
+        return states
+
+    def place(self, field: str, values) -> None:
+        """Overwrite a pose field for every lane (test hook; the reference tests
+        poke SimBatch arrays the same way, test_env.py:37-42)."""
+        ids = {"x": 0, "y": 1, "heading": 2, "v_linear": 3, "v_angular": 4, "start_x": 5,
+               "start_y": 6, "start_cos": 17, "start_sin": 18}
+        v = np.ascontiguousarray(np.broadcast_to(np.asarray(values, dtype=np.float64),
+                                                 (self.n_copies,)))
+        _lib.check(self._lib.sp_env_write_state(self._h, ids[field], v.ctypes.data_as(_lib.c_dp),
+                                                self._stream()), "place")
 
     # -- reporting -------------------------------------------------------------
     def _per_copy_arrays(self) -> dict:
