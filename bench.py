@@ -64,6 +64,16 @@ def load_maps():
     return lm(N_MAPS)
 
 
+def ncu_traffic():
+    """DRAM bytes per env_step_kernel launch from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_step_traffic.json")
+    if not os.path.exists(p):
+        return None, None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get("traffic_bytes_per_launch"), d.get("source")
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -80,19 +90,24 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, interval_ms: int = 10):
         self.index = index
+        self.interval_ms = interval_ms
         self.proc = None
         self.lines = []
+        self._first = threading.Event()
 
     def __enter__(self):
+        """Start sampling and block until nvidia-smi produced its first sample,
+        so the timed region that follows is covered."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.interval_ms)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
+            self._first.wait(timeout=10.0)
         except OSError:
             self.proc = None
         return self
@@ -100,6 +115,7 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+            self._first.set()
 
     def __exit__(self, *exc):
         if self.proc:
@@ -219,18 +235,19 @@ def run_ours(args, rank, world, local_rank):
                     torch.empty((n, D), dtype=torch.float32, device=dev),
                     torch.empty(n, dtype=torch.int8, device=dev))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    for t in range(W):
-        env.step_device(acts[t].data_ptr(), out)
-    env.check()
-    torch.cuda.synchronize(dev)
-
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     stops = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    wall0 = time.perf_counter()
+    # the clock sampler runs from the warm-up (GPU already loaded) to the end
+    # of the timed region
     with ClockSampler(local_rank) as clocks:
+        for t in range(W):
+            env.step_device(acts[t].data_ptr(), out)
+        env.check()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        wall0 = time.perf_counter()
         for k in range(K):
             flush.fill_(k & 0xFF)  # evict L2 (256 MiB > 126 MB) outside the timed events
             starts[k].record(stream)
@@ -286,6 +303,7 @@ def run_ours(args, rank, world, local_rank):
         mean_launch = t_dev / K
         achieved = BYTES_PER_ENV_STEP * n / mean_launch / 1e9
         info = env.launch_info()
+        traffic, traffic_src = ncu_traffic() if n == N_PER_GPU else (None, None)
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": t_dev_max / K * 1e3, "higher_is_better": True,
@@ -302,7 +320,9 @@ def run_ours(args, rank, world, local_rank):
                     "d2h_bytes_per_step": d2h, "steps": Ke,
                     "path": "VecEnv step with pinned host actions in, every StepBatch field out"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic,
+                         "traffic_unit": "bytes per launch (dram read+write)",
+                         "traffic_source": traffic_src,
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                          "algorithmic_bytes_per_env_step": BYTES_PER_ENV_STEP,
                          "kernel": "env_step_kernel", "mean_launch_ms": mean_launch * 1e3,
