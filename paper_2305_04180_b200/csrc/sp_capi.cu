@@ -53,22 +53,26 @@ struct DevDeviceGuard {
   }
 };
 
-// 2x2-block free-box table: 0 = block holds an occupied (or out-of-grid) cell,
-// else 1 + r with r = (chessboard distance to the nearest such block) - 1.
+// 2x2-block table: a block holding an occupied (or out-of-grid) cell stores
+// 0x80 | mask (bit (dy*2+dx) = cell (2by+dy, 2bx+dx) occupied); a free block
+// stores r = (chessboard distance to the nearest such block) - 1, clamped to
+// 127: the (2r+1)^2 blocks around it are all free.
 void build_block_table(const uint8_t* occ, int H, int W, int Hb, int Wb, uint8_t* out) {
   const int INF = 1 << 29;
   std::vector<int> dist((size_t)Hb * Wb);
+  std::vector<uint8_t> mask((size_t)Hb * Wb, 0);
   for (int by = 0; by < Hb; ++by)
     for (int bx = 0; bx < Wb; ++bx) {
-      bool blocked = false;
-      for (int dy = 0; dy < 2 && !blocked; ++dy)
-        for (int dx = 0; dx < 2 && !blocked; ++dx) {
-          int iy = 2 * by + dy, ix = 2 * bx + dx;
-          if (iy >= H || ix >= W || occ[(size_t)iy * W + ix]) blocked = true;
+      uint8_t mk = 0;
+      for (int dy = 0; dy < 2; ++dy)
+        for (int dx = 0; dx < 2; ++dx) {
+          const int iy = 2 * by + dy, ix = 2 * bx + dx;
+          if (iy >= H || ix >= W || occ[(size_t)iy * W + ix]) mk |= (uint8_t)(1u << (dy * 2 + dx));
         }
+      mask[(size_t)by * Wb + bx] = mk;
       // outside the block grid counts as blocked: distance to the border
-      int border = std::min(std::min(bx + 1, by + 1), std::min(Wb - bx, Hb - by));
-      dist[(size_t)by * Wb + bx] = blocked ? 0 : std::min(border, INF);
+      const int border = std::min(std::min(bx + 1, by + 1), std::min(Wb - bx, Hb - by));
+      dist[(size_t)by * Wb + bx] = mk ? 0 : std::min(border, INF);
     }
   // two-pass chessboard distance transform (exact for the L-inf metric)
   for (int by = 0; by < Hb; ++by)
@@ -91,7 +95,22 @@ void build_block_table(const uint8_t* occ, int H, int W, int Hb, int Wb, uint8_t
         if (bx > 0) d = std::min(d, dist[(size_t)(by + 1) * Wb + bx - 1] + 1);
       }
     }
-  for (size_t i = 0; i < dist.size(); ++i) out[i] = (uint8_t)std::min(dist[i], 255);
+  for (size_t i = 0; i < dist.size(); ++i)
+    out[i] = mask[i] ? (uint8_t)(0x80u | mask[i]) : (uint8_t)std::min(dist[i] - 1, 127);
+}
+
+// every map's border row/column fully occupied (GridMap's invariant,
+// gridmap.py:90-95): no march step can then leave the grid
+bool all_bordered(const SpMapDesc* maps, int n_maps) {
+  for (int m = 0; m < n_maps; ++m) {
+    const int H = maps[m].n_rows, W = maps[m].n_cols;
+    const uint8_t* o = maps[m].occupancy;
+    for (int ix = 0; ix < W; ++ix)
+      if (!o[ix] || !o[(size_t)(H - 1) * W + ix]) return false;
+    for (int iy = 0; iy < H; ++iy)
+      if (!o[(size_t)iy * W] || !o[(size_t)iy * W + W - 1]) return false;
+  }
+  return true;
 }
 
 }  // namespace
@@ -108,6 +127,7 @@ struct SpEnv {
   int grid = 0, threads = 0;
   size_t smem = 0;
   int n_sm = 0, smem_optin = 0;
+  bool bordered = false;
   int32_t* h_err = nullptr;  // pinned
   int64_t* h_scan = nullptr;  // pinned staging for scan offsets (n_maps + 1 + n_sm + 1)
   int64_t* d_scan = nullptr;
@@ -294,6 +314,7 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   env->D = 5 + cfg->n_beams;
   env->n_maps = n_maps;
   env->auto_reset = cfg->auto_reset != 0;
+  env->bordered = all_bordered(maps, n_maps);
   cudaDeviceProp prop;
   if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
     delete env;
@@ -438,7 +459,7 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
     d.nb_shift = (d.nb & (d.nb - 1)) == 0 ? __builtin_ctz((unsigned)d.nb) : -1;
     d.inv_max_range = 1.0 / cfg->max_range_cm;
     const char* rm = std::getenv("SPARROW_REFILL_MIN");
-    d.refill_min = rm ? std::max(1, std::min(32, std::atoi(rm))) : 16;
+    d.refill_min = rm ? std::max(1, std::min(64, std::atoi(rm))) : 32;
   }
   Plan plan = plan_launch(env, env->map_off);
   apply_plan(plan, d);
@@ -452,16 +473,20 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   env->grid = plan.grid;
   env->threads = plan.threads;
   env->smem = plan.smem;
-  cudaError_t e1 = cudaFuncSetAttribute(env_step_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        env->smem_optin);
-  if (e1 == cudaSuccess)
-    e1 = cudaFuncSetAttribute(env_step_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              env->smem_optin);
-  cudaError_t e2 = cudaFuncSetAttribute(env_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        env->smem_optin);
-  if (e2 == cudaSuccess)
-    e2 = cudaFuncSetAttribute(env_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              env->smem_optin);
+  const void* kernels_[] = {(const void*)env_step_kernel<true, true>,
+                            (const void*)env_step_kernel<true, false>,
+                            (const void*)env_step_kernel<false, true>,
+                            (const void*)env_step_kernel<false, false>,
+                            (const void*)env_scan_kernel<true, true>,
+                            (const void*)env_scan_kernel<true, false>,
+                            (const void*)env_scan_kernel<false, true>,
+                            (const void*)env_scan_kernel<false, false>};
+  cudaError_t e1 = cudaSuccess, e2 = cudaSuccess;
+  for (const void* k : kernels_) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         env->smem_optin);
+    if (e != cudaSuccess) e1 = e;
+  }
   cudaError_t e3 = cudaDeviceSynchronize();
   if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
     delete env;
@@ -480,10 +505,15 @@ int sp_env_destroy(SpEnv* env) {
 }
 
 static int launch_env(SpEnv* env, const StepArgs& a, cudaStream_t st) {
-  if (env->d.smem_maps)
-    env_step_kernel<true><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
+  const bool sm = env->d.smem_maps, bd = env->bordered;
+  if (sm && bd)
+    env_step_kernel<true, true><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
+  else if (sm)
+    env_step_kernel<true, false><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
+  else if (bd)
+    env_step_kernel<false, true><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
   else
-    env_step_kernel<false><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
+    env_step_kernel<false, false><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(SP_ECUDA, std::string("env_step_kernel: ") + cudaGetErrorString(e));
   return SP_OK;
@@ -752,10 +782,14 @@ int sp_env_scan(SpEnv* env, int64_t n, const int64_t* query_offsets, const doubl
   SP_CUDA(cudaMemcpyAsync(env->d_scan, env->h_scan, 8 * (nq + nc), cudaMemcpyHostToDevice, st));
   SP_CUDA(cudaEventRecord(env->scan_copied, st));
   ScanArgs q{n, env->d_scan + nq, env->d_scan, x, y, heading, ranges, hit_cell};
-  if (d.smem_maps)
-    env_scan_kernel<true><<<plan.grid, plan.threads, plan.smem, st>>>(d, q);
+  if (d.smem_maps && env->bordered)
+    env_scan_kernel<true, true><<<plan.grid, plan.threads, plan.smem, st>>>(d, q);
+  else if (d.smem_maps)
+    env_scan_kernel<true, false><<<plan.grid, plan.threads, plan.smem, st>>>(d, q);
+  else if (env->bordered)
+    env_scan_kernel<false, true><<<plan.grid, plan.threads, plan.smem, st>>>(d, q);
   else
-    env_scan_kernel<false><<<plan.grid, plan.threads, plan.smem, st>>>(d, q);
+    env_scan_kernel<false, false><<<plan.grid, plan.threads, plan.smem, st>>>(d, q);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(SP_ECUDA, std::string("env_scan_kernel: ") + cudaGetErrorString(e));
   return SP_OK;

@@ -9,10 +9,11 @@
 //   that lies inside one map whenever the map count allows, so a CTA stages
 //   one map once per launch.
 // * Per map, two tables live in shared memory, staged by one TMA bulk copy
-//   (cp.async.bulk + mbarrier): a 1-bit occupancy bitmap (H x ceil(W/32) u32)
-//   and a 2x2-block "free box" table (u8: 0 = block holds an occupied cell,
-//   else 1 + r where the (2r+1)^2 blocks around it are all free).  366 x 366
-//   cells -> 17.6 KB + 33.5 KB.
+//   (cp.async.bulk + mbarrier): a 2x2-block table (u8: 0x80 | occupancy mask
+//   of the block's four cells when any is occupied, else the radius r of the
+//   all-free (2r+1)^2-block box around it) that the march reads once per
+//   step, and a 1-bit occupancy bitmap (H x ceil(W/32) u32) for the exact
+//   disc-collision test.  366 x 366 cells -> 33.5 KB + 17.6 KB.
 // * A CTA walks its range in chunks of up to `chunk_cap` envs with CTA-wide
 //   phases separated by __syncthreads:
 //     A  thread-per-env physics, collision, events, shaped-reward partial,
@@ -87,7 +88,8 @@ __device__ __forceinline__ bool disc_hits(const MapView& mv, const EnvDev& d, do
     return true;  // :124-126
   const int cx = (int)floor(x * d.inv_cell), cy = (int)floor(y * d.inv_cell);
   if (cx >= 0 && cx < d.W && cy >= 0 && cy < d.H) {
-    if (mv.code(cx, cy) > (uint32_t)d.need_r) return false;  // free box covers the bbox
+    const uint32_t code = mv.code(cx, cy);  // free box of radius code covers the bbox?
+    if ((code & 0x80u) == 0u && code >= (uint32_t)d.need_r) return false;
   }
   int ix0 = (int)floor(ddiv(dsub(x, r), cell)); if (ix0 < 0) ix0 = 0;  // :128-135
   int ix1 = (int)floor(ddiv(dadd(x, r), cell)); if (ix1 > d.W - 1) ix1 = d.W - 1;
@@ -119,9 +121,12 @@ __device__ __forceinline__ bool disc_hits(const MapView& mv, const EnvDev& d, do
 }
 
 // ---------------------------------------------------------------- rays ---
+// Ray state in cell units: origin (x0, y0)/cell, direction (dx, dy)/cell and
+// cell/dx, cell/dy (so t = (face - x0) * idx comes out in cm), the step
+// signs and the current cell.
 struct Ray {
   double x0, y0, dx, dy, idx, idy, t;
-  int ix, iy;
+  int ix, iy, sx, sy;
 };
 
 // 1/v to within an ulp: fp32 seed + two fp64 Newton steps (no DDIV).
@@ -136,60 +141,67 @@ __device__ __forceinline__ double recip(double v) {
   return r;
 }
 
-// One free-box step (branch-free up to the finishing tests).  Returns true
-// when the ray is finished; r.t is then the range.
-__device__ __forceinline__ bool ray_step(Ray& r, const MapView& mv, const EnvDev& d, int& hit) {
+// One march step, branch-free: every lane of the warp executes it, and only
+// `live` rays commit.  The block byte is either 0x80 | the occupancy mask of
+// the block's 2x2 cells (then the step is one cell, as _cy.pyx:89-96), or the
+// radius r of the free (2r+1)^2-block box around it (then the ray leaves the
+// whole box).  Either way the ray exits through the face with the smaller
+// parameter (ties to x, as tmx <= tmy does) into the cell containing the
+// exit point.  Returns true when a live ray finished: r.t is then the range
+// and `hit` the occupied cell it entered (or -1).
+// kBordered: every map has an occupied border, so no step can leave the grid.
+template <bool kBordered>
+__device__ __forceinline__ bool ray_step(Ray& r, bool live, const MapView& mv, const EnvDev& d,
+                                         int& hit) {
   const uint32_t code = mv.code(r.ix, r.iy);
-  const uint32_t word = mv.word(r.ix, r.iy);
-  if (code == 0u && ((word >> (r.ix & 31)) & 1u)) {  // entered an occupied cell at r.t
-    hit = r.iy * d.W + r.ix;
-    return true;
+  const bool cellwise = (code & 0x80u) != 0u;
+  const bool occupied = cellwise && ((code >> (((r.iy & 1) << 1) | (r.ix & 1))) & 1u);
+  // forward edge of the free region: the cell itself, or the box's far edge
+  const int fx = (r.sx + 1) >> 1, fy = (r.sy + 1) >> 1;  // 1 when moving +
+  const int two_r = (int)(code << 1);
+  const int ex = cellwise ? r.ix : (r.ix & ~1) + fx + r.sx * two_r;
+  const int ey = cellwise ? r.iy : (r.iy & ~1) + fy + r.sy * two_r;
+  const double tx = ((double)(ex + fx) - r.x0) * r.idx;
+  const double ty = ((double)(ey + fy) - r.y0) * r.idy;
+  const bool xs = tx <= ty;
+  const double t = xs ? tx : ty;
+  // the cell on the other axis at the exit point, between the current cell
+  // and the forward edge (the ray moves monotonically)
+  const int c = (int)floor(xs ? fma(tx, r.dy, r.y0) : fma(ty, r.dx, r.x0));
+  const int cy = r.sy > 0 ? min(max(c, r.iy), ey) : max(min(c, r.iy), ey);
+  const int cx = r.sx > 0 ? min(max(c, r.ix), ex) : max(min(c, r.ix), ex);
+  const int nx = xs ? ex + r.sx : cx;
+  const int ny = xs ? cy : ey + r.sy;
+  const bool over = t > d.max_range;  // :97-99
+  const bool out = !kBordered && ((unsigned)nx >= (unsigned)d.W || (unsigned)ny >= (unsigned)d.H);
+  hit = occupied ? r.iy * d.W + r.ix : -1;
+  const bool finished = occupied || over || out;
+  if (live && !occupied) {
+    r.t = over ? d.max_range : t;
+    if (!finished) {
+      r.ix = nx;
+      r.iy = ny;
+    }
   }
-  const int rr = (int)code - 1;
-  const int bx = r.ix >> 1, by = r.iy >> 1;
-  const bool box = code != 0u;
-  const int lox = box ? (bx - rr) << 1 : r.ix;
-  const int hix = box ? ((bx + rr) << 1) + 1 : r.ix;
-  const int loy = box ? (by - rr) << 1 : r.iy;
-  const int hiy = box ? ((by + rr) << 1) + 1 : r.iy;
-  const bool px = r.dx >= 0.0, py = r.dy >= 0.0;
-  const double tx = ((double)(px ? hix + 1 : lox) * d.cell - r.x0) * r.idx;
-  const double ty = ((double)(py ? hiy + 1 : loy) * d.cell - r.y0) * r.idy;
-  const bool xs = tx <= ty;  // leave through the x face on ties, as _cy.pyx:89
-  r.t = xs ? tx : ty;
-  // the cell on the other axis at the exit point, clamped into the box span
-  const int c = (int)floor((xs ? (r.y0 + tx * r.dy) : (r.x0 + ty * r.dx)) * d.inv_cell);
-  if (xs) {
-    r.ix = px ? hix + 1 : lox - 1;
-    r.iy = min(max(c, loy), hiy);
-  } else {
-    r.iy = py ? hiy + 1 : loy - 1;
-    r.ix = min(max(c, lox), hix);
-  }
-  if (r.t > d.max_range) {  // :97-99
-    r.t = d.max_range;
-    hit = -1;
-    return true;
-  }
-  if ((unsigned)r.ix >= (unsigned)d.W || (unsigned)r.iy >= (unsigned)d.H) {  // :100-102
-    hit = -1;
-    return true;
-  }
-  return false;
+  return live && finished;
 }
 
 // Returns true if finished during setup (origin outside the grid -> 0).
 __device__ __forceinline__ bool ray_setup(Ray& r, double x0, double y0, double ch, double sh,
                                           double2 cs, const EnvDev& d, int& hit) {
-  r.x0 = x0;
-  r.y0 = y0;
-  r.dx = ch * cs.x - sh * cs.y;  // cos(h + o_j)
-  r.dy = sh * cs.x + ch * cs.y;  // sin(h + o_j)
-  r.idx = recip(r.dx);
-  r.idy = recip(r.dy);
+  const double dx = ch * cs.x - sh * cs.y;  // cos(h + o_j)
+  const double dy = sh * cs.x + ch * cs.y;  // sin(h + o_j)
+  r.x0 = x0 * d.inv_cell;
+  r.y0 = y0 * d.inv_cell;
+  r.dx = dx * d.inv_cell;
+  r.dy = dy * d.inv_cell;
+  r.idx = recip(dx) * d.cell;
+  r.idy = recip(dy) * d.cell;
+  r.sx = dx >= 0.0 ? 1 : -1;  // dx == 0: idx = +inf, the x face is never taken
+  r.sy = dy >= 0.0 ? 1 : -1;
   r.t = 0.0;
-  r.ix = (int)floor(x0 * d.inv_cell);
-  r.iy = (int)floor(y0 * d.inv_cell);
+  r.ix = (int)floor(r.x0);
+  r.iy = (int)floor(r.y0);
   if ((unsigned)r.ix >= (unsigned)d.W || (unsigned)r.iy >= (unsigned)d.H) {  // :37-39
     hit = -1;
     return true;
@@ -237,62 +249,79 @@ __device__ __forceinline__ int div_r(int q, const EnvDev& d) {
   return q / d.R;
 }
 
-// CTA-wide ray queue over n_env envs (c.list) x R beams.  fin(e, j, t, hit).
-// Every thread of the CTA must call it.  A warp refills only when at least
-// d.refill_min of its lanes are idle (or the queue is drained), and finished
-// rays are retired in the same branch, so per-ray setup/finish code runs at
-// high SIMT occupancy while the march keeps most lanes busy.
-template <bool kHit, class Fin>
+// CTA-wide ray queue over n_env slots (c.list) x R beams.  fin(slot, j, t, hit).
+// Every thread of the CTA must call it.  Each lane marches two independent
+// rays (slots A and B) so one ray's fp64 dependency chain hides behind the
+// other's.  A warp refills only when at least d.refill_min of its 64 ray
+// slots are idle (or the queue is drained); finished rays are retired in the
+// same branch, so per-ray setup/finish code runs at high SIMT occupancy.
+template <bool kBordered, bool kHit, class Fin>
 __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, const Chunk& c,
                                           const double2* beam, int n_env, const Fin& fin) {
   const int R = d.R;
   const int total = n_env * R;
   const int lane = threadIdx.x & 31;
-  bool active = false, done = false;
+  const unsigned lt = lanemask_lt();
+  bool act_a = false, act_b = false, done_a = false, done_b = false;
   bool drained = total == 0;
-  int e = 0, j = 0, res_hit = -1;
-  double res_t = 0.0;
-  Ray r;
+  int ea = 0, ja = 0, eb = 0, jb = 0, hit_a = -1, hit_b = -1;
+  Ray ra, rb;
+  ra.ix = ra.iy = rb.ix = rb.iy = 0;
+  ra.sx = ra.sy = rb.sx = rb.sy = 1;
+  ra.x0 = ra.y0 = rb.x0 = rb.y0 = 0.5;
+  ra.dx = ra.dy = rb.dx = rb.dy = 1.0;
+  ra.idx = ra.idy = rb.idx = rb.idy = 1.0;
+  ra.t = rb.t = 0.0;
   for (;;) {
-    const unsigned idle = __ballot_sync(SP_FULL, !active);
-    const int n_idle = __popc(idle);
+    const unsigned ia = __ballot_sync(SP_FULL, !act_a);
+    const unsigned ib = __ballot_sync(SP_FULL, !act_b);
+    const int na = __popc(ia), n_idle = na + __popc(ib);
     if (n_idle >= d.refill_min || drained) {
-      if (done) {
-        fin(e, j, res_t, res_hit);
-        done = false;
+      if (done_a) {
+        fin(ea, ja, ra.t, hit_a);
+        done_a = false;
+      }
+      if (done_b) {
+        fin(eb, jb, rb.t, hit_b);
+        done_b = false;
       }
       if (drained) {
-        if (idle == SP_FULL) break;
+        if ((ia & ib) == SP_FULL) break;
       } else {
         int base = 0;
         if (lane == 0) base = atomicAdd(&c.ctl[0], n_idle);
         base = __shfl_sync(SP_FULL, base, 0);
         if (base + n_idle >= total) drained = true;
-        const int my = base + __popc(idle & lanemask_lt());
-        if (!active && my < total) {
-          const int g = div_r(my, d);
-          e = c.list[g];
-          j = my - g * R;
-          int hit;
-          if (ray_setup(r, c.px[e], c.py[e], c.ch[e], c.sh[e], beam[j], d, hit)) {
-            done = true;
-            res_t = 0.0;
-            res_hit = hit;
-          } else {
-            active = true;
-          }
+        const int my_a = base + __popc(ia & lt);
+        const int my_b = base + na + __popc(ib & lt);
+        if (!act_a && my_a < total) {
+          const int g = div_r(my_a, d);
+          ea = c.list[g];
+          ja = my_a - g * R;
+          act_a = !ray_setup(ra, c.px[ea], c.py[ea], c.ch[ea], c.sh[ea], beam[ja], d, hit_a);
+          done_a = !act_a;
         }
-        continue;
+        if (!act_b && my_b < total) {
+          const int g = div_r(my_b, d);
+          eb = c.list[g];
+          jb = my_b - g * R;
+          act_b = !ray_setup(rb, c.px[eb], c.py[eb], c.ch[eb], c.sh[eb], beam[jb], d, hit_b);
+          done_b = !act_b;
+        }
       }
     }
-    if (active) {
-      int hit;
-      if (ray_step(r, mv, d, hit)) {
-        active = false;
-        done = true;
-        res_t = r.t;
-        res_hit = kHit ? hit : -1;
-      }
+    int ha, hb;
+    const bool fa = ray_step<kBordered>(ra, act_a, mv, d, ha);
+    const bool fb = ray_step<kBordered>(rb, act_b, mv, d, hb);
+    if (fa) {
+      act_a = false;
+      done_a = true;
+      hit_a = kHit ? ha : -1;
+    }
+    if (fb) {
+      act_b = false;
+      done_b = true;
+      hit_b = kHit ? hb : -1;
     }
   }
 }
@@ -487,7 +516,7 @@ __device__ __forceinline__ void write_rows(const EnvDev& d, const StepArgs& a, c
 }
 
 // ------------------------------------------------------------ the kernel ---
-template <bool kSmem>
+template <bool kSmem, bool kBordered>
 __global__ void __launch_bounds__(768, 1)
     env_step_kernel(const __grid_constant__ EnvDev d, const __grid_constant__ StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -644,7 +673,7 @@ __global__ void __launch_bounds__(768, 1)
     // ---- N: LiDAR noise; B: LiDAR rays --------------------------------------
     noise_phase(d, c, n_slots);
     __syncthreads();
-    ray_phase<false>(mv, d, c, beam, n_slots, fin);
+    ray_phase<kBordered, false>(mv, d, c, beam, n_slots, fin);
     __syncthreads();
     // ---- C: reward, outputs, statistics ------------------------------------
     if (live) {
@@ -695,7 +724,7 @@ __global__ void __launch_bounds__(768, 1)
       const int n2 = c.ctl[1];
       noise_phase(d, c, n2);
       __syncthreads();
-      ray_phase<false>(mv, d, c, beam, n2, fin);
+      ray_phase<kBordered, false>(mv, d, c, beam, n2, fin);
       __syncthreads();
       write_rows(d, a, c, s0, n);
     }
@@ -716,7 +745,7 @@ struct FinScan {
   }
 };
 
-template <bool kSmem>
+template <bool kSmem, bool kBordered>
 __global__ void __launch_bounds__(768, 1)
     env_scan_kernel(const __grid_constant__ EnvDev d, const __grid_constant__ ScanArgs q) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -750,7 +779,7 @@ __global__ void __launch_bounds__(768, 1)
     }
     __syncthreads();
     const FinScan fin{q.ranges, q.hit_cell, s0, d.R};
-    ray_phase<true>(mv, d, c, beam, n, fin);
+    ray_phase<kBordered, true>(mv, d, c, beam, n, fin);
     s0 += n;
   }
 }
