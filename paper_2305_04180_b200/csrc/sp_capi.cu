@@ -36,7 +36,7 @@ int fail(int code, const std::string& msg) {
       return fail(SP_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));      \
   } while (0)
 
-constexpr int kMaxWarps = 24;  // 768 threads: keeps >= 85 registers per thread
+constexpr int kMaxWarps = SP_CTA_THREADS / 32;
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -126,7 +126,7 @@ struct SpEnv {
   std::vector<void*> allocs;
   int grid = 0, threads = 0;
   size_t smem = 0;
-  int n_sm = 0, smem_optin = 0;
+  int n_sm = 0, smem_optin = 0, smem_per_sm = 0;
   bool bordered = false;
   int32_t* h_err = nullptr;  // pinned
   int64_t* h_scan = nullptr;  // pinned staging for scan offsets (n_maps + 1 + n_sm + 1)
@@ -231,7 +231,11 @@ static Plan plan_launch(SpEnv* env, const std::vector<int64_t>& off, bool stagin
   Plan p;
   const int64_t lanes = off.back() - off.front();
   const size_t fixed = align_up((size_t)d.R * 16, 128) + 128;
-  const size_t budget = (size_t)env->smem_optin - 1024;
+  // per-CTA budget: SP_CTAS_PER_SM CTAs share the SM's shared memory (plus
+  // 1 KB per CTA reserved by the driver)
+  const size_t sm_total = (size_t)env->smem_per_sm;
+  const size_t budget = std::min((size_t)env->smem_optin,
+                                 sm_total / SP_CTAS_PER_SM) - 1024;
   size_t map_bytes = align_up(d.map_bytes, 128);
   p.threads = kMaxWarps * 32;
   if (map_bytes + fixed + chunk_bytes(128, D) + 128 > budget) {
@@ -243,7 +247,8 @@ static Plan plan_launch(SpEnv* env, const std::vector<int64_t>& off, bool stagin
   while (cap > 1 && chunk_bytes(cap, D) > room) cap -= 16;
   p.chunk_cap = std::max(1, cap);
   p.slot_cap = p.chunk_cap + std::max(32, p.chunk_cap / 8);
-  p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(env->n_sm, (lanes + 15) / 16));
+  p.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)env->n_sm * SP_CTAS_PER_SM,
+                                                         (lanes + 15) / 16));
   p.cta_begin = cta_ranges(off, p.grid);
   p.grid = (int)p.cta_begin.size() - 1;
   p.smem = map_bytes + fixed + align_up(chunk_bytes(p.chunk_cap, D), 128);
@@ -322,6 +327,7 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   }
   env->n_sm = prop.multiProcessorCount;
   env->smem_optin = (int)prop.sharedMemPerBlockOptin;
+  env->smem_per_sm = (int)prop.sharedMemPerMultiprocessor;
 
   EnvDev& d = env->d;
   d.n = n_envs;
@@ -432,8 +438,8 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   TRY(env->alloc(&d.err, 4));
 #undef TRY
   if (cudaMallocHost(&env->h_err, 16) != cudaSuccess ||
-      cudaMallocHost(&env->h_scan, 8 * (size_t)(n_maps + env->n_sm + 2)) != cudaSuccess ||
-      env->alloc(&env->d_scan, (size_t)(n_maps + env->n_sm + 2)) != SP_OK ||
+      cudaMallocHost(&env->h_scan, 8 * (size_t)(n_maps + env->n_sm * SP_CTAS_PER_SM + 2)) != cudaSuccess ||
+      env->alloc(&env->d_scan, (size_t)(n_maps + env->n_sm * SP_CTAS_PER_SM + 2)) != SP_OK ||
       cudaEventCreateWithFlags(&env->scan_copied, cudaEventDisableTiming) != cudaSuccess) {
     delete env;
     return fail(SP_ENOMEM, "pinned alloc");
@@ -455,6 +461,7 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
     const int R = env->R;
     d.r_shift = (R & (R - 1)) == 0 ? __builtin_ctz((unsigned)R) : -1;
     d.r_magic = (d.r_shift < 0 && R < 512) ? (((uint64_t)1 << 40) + R - 1) / R : 0;
+    d.d_magic = (((uint64_t)1 << 40) + (uint64_t)env->D - 1) / (uint64_t)env->D;
     d.nb = (R + 3) / 4;
     d.nb_shift = (d.nb & (d.nb - 1)) == 0 ? __builtin_ctz((unsigned)d.nb) : -1;
     d.inv_max_range = 1.0 / cfg->max_range_cm;

@@ -495,29 +495,28 @@ enum : uint8_t {
   W_STATE = 4      // stage[e] -> states only (reset_all, overflow pass)
 };
 
-// Coalesced row writes, one warp per env row.
+// Coalesced row writes: the chunk's rows are walked as one flat array of
+// n x D floats so every lane stores (full SIMT), consecutive lanes hitting
+// consecutive addresses of the same output row.
 __device__ __forceinline__ void write_rows(const EnvDev& d, const StepArgs& a, const Chunk& c,
                                            int64_t s0, int n) {
   const int D = d.D;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int e = warp; e < n; e += nw) {
+  const int total = n * D;
+  for (int f = threadIdx.x; f < total; f += blockDim.x) {
+    const int e = (int)(((uint64_t)(uint32_t)f * d.d_magic) >> 40);  // f / D
+    const int k = f - e * D;
     const uint8_t w = c.wmode[e];
     if (w == W_NONE) continue;
-    const int64_t rr = d.env_of_slot[s0 + e];
-    const float* own = c.stage + e * D;
-    const float* post = w == W_RESET_X ? c.stage + c.xslot[e] * D : own;
-    float* st = a.states + rr * D;
-    float* ss = a.store_states + rr * D;
-    for (int k = lane; k < D; k += 32) {
-      if (w != W_STATE) ss[k] = own[k];
-      if (w != W_RESET_OV) st[k] = post[k];
-    }
+    const int64_t o = d.env_of_slot[s0 + e] * D + k;
+    const float own = c.stage[e * D + k];
+    if (w != W_STATE) a.store_states[o] = own;
+    if (w != W_RESET_OV) a.states[o] = w == W_RESET_X ? c.stage[c.xslot[e] * D + k] : own;
   }
 }
 
 // ------------------------------------------------------------ the kernel ---
 template <bool kSmem, bool kBordered>
-__global__ void __launch_bounds__(768, 1)
+__global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     env_step_kernel(const __grid_constant__ EnvDev d, const __grid_constant__ StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   double2* beam = (double2*)(smem + d.off_beam);
@@ -746,7 +745,7 @@ struct FinScan {
 };
 
 template <bool kSmem, bool kBordered>
-__global__ void __launch_bounds__(768, 1)
+__global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     env_scan_kernel(const __grid_constant__ EnvDev d, const __grid_constant__ ScanArgs q) {
   extern __shared__ __align__(128) uint8_t smem[];
   double2* beam = (double2*)(smem + d.off_beam);

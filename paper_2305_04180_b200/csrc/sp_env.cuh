@@ -2,6 +2,14 @@
 #pragma once
 #include "sp_common.cuh"
 
+// Launch shape: SP_CTAS_PER_SM resident CTAs of SP_CTA_THREADS threads.  Two
+// CTAs per SM let one CTA's ray-queue tail and phase barriers overlap the
+// other's work; each holds its own copy of its map's tables.
+#ifndef SP_CTAS_PER_SM
+#define SP_CTAS_PER_SM 2
+#endif
+#define SP_CTA_THREADS (768 / SP_CTAS_PER_SM)
+
 namespace sp {
 
 // Per-map constants (gridmap.py GridMap fields used by core.py:81-86, 133).
@@ -61,6 +69,7 @@ struct EnvDev {
   int32_t refill_min;     // ray queue: refill a warp once this many lanes idle
   int32_t r_shift;        // q / R: shift when R is a power of two, else -1
   uint64_t r_magic;       // ceil(2^40 / R) for R < 512 (else 0: plain division)
+  uint64_t d_magic;       // ceil(2^40 / D): f / D for f < 2^21 (row writes)
 };
 
 enum { MODE_STEP = 0, MODE_RESET_ALL = 1, MODE_RESET_LANES = 2 };
