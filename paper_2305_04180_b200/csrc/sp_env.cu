@@ -310,18 +310,20 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
         }
       }
     }
-    int ha, hb;
-    const bool fa = ray_step<kBordered>(ra, act_a, mv, d, ha);
-    const bool fb = ray_step<kBordered>(rb, act_b, mv, d, hb);
-    if (fa) {
-      act_a = false;
-      done_a = true;
-      hit_a = kHit ? ha : -1;
-    }
-    if (fb) {
-      act_b = false;
-      done_b = true;
-      hit_b = kHit ? hb : -1;
+    // two march steps per slot between refill checks (halves the loop's
+    // vote/branch overhead per step); a ray that finishes in the first step
+    // sits out the second (live = act)
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      int ha, hb;
+      const bool fa = ray_step<kBordered>(ra, act_a, mv, d, ha);
+      const bool fb = ray_step<kBordered>(rb, act_b, mv, d, hb);
+      if (fa) hit_a = kHit ? ha : -1;
+      if (fb) hit_b = kHit ? hb : -1;
+      act_a = act_a && !fa;
+      act_b = act_b && !fb;
+      done_a = done_a || fa;
+      done_b = done_b || fb;
     }
   }
 }
