@@ -244,7 +244,7 @@ def run_ours(args, rank, world, local_rank):
             env.step_device(acts[t].data_ptr(), out)
         env.check()
         torch.cuda.synchronize(dev)
-        if world > 1:
+        if dist.is_initialized():
             dist.barrier()
         torch.cuda.synchronize(dev)
         wall0 = time.perf_counter()
@@ -254,14 +254,14 @@ def run_ours(args, rank, world, local_rank):
             env.step_device(acts[W + k].data_ptr(), out)
             stops[k].record(stream)
         torch.cuda.synchronize(dev)
-        if world > 1:
+        if dist.is_initialized():
             dist.barrier()
     wall = time.perf_counter() - wall0
     env.check()
     per_step = [s.elapsed_time(e) for s, e in zip(starts, stops)]  # ms
     t_dev = sum(per_step) / 1e3
     t_max = torch.tensor([t_dev], dtype=torch.float64, device=dev)
-    if world > 1:
+    if dist.is_initialized():
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     t_dev_max = float(t_max.item())
     value = world * n * K / t_dev_max
@@ -291,7 +291,7 @@ def run_ours(args, rank, world, local_rank):
         _ = float(h_out[1][0])  # the step's result read on the host
     e2e_t = sum(s.elapsed_time(e) for s, e in zip(e_starts, e_stops)) / 1e3
     et = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
-    if world > 1:
+    if dist.is_initialized():
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
     e2e_value = world * n * Ke / float(et.item())
     h2d = n * 8
@@ -337,7 +337,20 @@ def run_ours(args, rank, world, local_rank):
     return result
 
 
+def _json_out():
+    """Keep stdout for the one JSON line: anything else written to fd 1 (NCCL's
+    version banner, library chatter) goes to stderr."""
+    sys.stdout.flush()
+    fd = os.dup(1)
+    os.dup2(2, 1)
+
+    def emit(obj):
+        os.write(fd, (json.dumps(obj) + "\n").encode())
+    return emit
+
+
 def main():
+    emit = _json_out()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
@@ -368,21 +381,24 @@ def main():
                 "cpu_baseline": base,
                 "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
+        emit(line)
         return
 
-    if world > 1:
+    # under torchrun (any world size) the NCCL plumbing is always exercised
+    launched = "MASTER_ADDR" in os.environ and "RANK" in os.environ
+    if launched:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     result = run_ours(args, rank, world, local_rank)
     if rank == 0:
         if not args.no_cpu_baseline and world == 1:
             result["cpu_baseline"] = cpu_reference(seconds=args.cpu_seconds)
-        print(json.dumps(result), flush=True)
-    if world > 1:
+        emit(result)
+    if launched:
         import torch.distributed as dist
+        dist.barrier()
         dist.destroy_process_group()
 
 

@@ -11,7 +11,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libsparrow.so")
+LIB_PATH = os.environ.get("SPARROW_LIB_PATH") or os.path.join(HERE, "_lib", "libsparrow.so")
 
 SP_OK, SP_EINVAL, SP_EACTION, SP_EEPISODE, SP_EMAP, SP_ENOTREADY, SP_ECUDA, SP_ENOMEM = range(8)
 SP_MAX_ACTIONS = 15

@@ -42,12 +42,15 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in deps if os.path.exists(p))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()) -> str:
+    """Compile libsparrow.so; `defines` (e.g. ["SP_CTAS_PER_SM=1"]) build
+    experimental variants to another `out` path."""
+    if not force and out == OUT and not defines and up_to_date():
         return OUT
-    os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    tmp = OUT + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, os.path.join(CSRC, "sp_capi.cu")]
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    tmp = out + ".tmp"
+    cmd = [nvcc(), *NVCC_FLAGS, *(f"-D{x}" for x in defines), "-o", tmp,
+           os.path.join(CSRC, "sp_capi.cu")]
     if verbose:
         print(" ".join(cmd), flush=True)
     res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
@@ -55,9 +58,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed:\n{res.stdout}\n{res.stderr}")
     if verbose and res.stderr.strip():
         print(res.stderr, file=sys.stderr)
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    args = [a for a in sys.argv[1:] if a != "--force"]
+    if args:  # python -m paper_2305_04180_b200.build OUT.so DEF=1 ...
+        print(build(force=True, verbose=True, out=os.path.abspath(args[0]), defines=args[1:]))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

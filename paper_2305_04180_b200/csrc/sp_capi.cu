@@ -220,9 +220,11 @@ static std::vector<int64_t> cta_ranges(const std::vector<int64_t>& off, int G) {
 }
 
 // shared-memory bytes of a chunk with `cap` envs (layout of chunk_smem)
-static size_t chunk_bytes(int cap, int D) {
-  const size_t slots = (size_t)cap + std::max(32, cap / 8);
-  return slots * (57 + 4 * (size_t)D) + 5 * (size_t)cap + 16;
+static int extra_slots(int cap) { return std::max(32, cap / 8); }
+static size_t chunk_bytes(int cap, int D, int R) {
+  const size_t slots = (size_t)cap + extra_slots(cap);
+  (void)R;
+  return slots * (74 + 4 * (size_t)D) + 5 * (size_t)cap + 96;
 }
 
 static Plan plan_launch(SpEnv* env, const std::vector<int64_t>& off, bool staging = true) {
@@ -238,20 +240,20 @@ static Plan plan_launch(SpEnv* env, const std::vector<int64_t>& off, bool stagin
                                  sm_total / SP_CTAS_PER_SM) - 1024;
   size_t map_bytes = align_up(d.map_bytes, 128);
   p.threads = kMaxWarps * 32;
-  if (map_bytes + fixed + chunk_bytes(128, D) + 128 > budget) {
+  if (map_bytes + fixed + chunk_bytes(128, D, d.R) + 128 > budget) {
     p.smem_maps = 0;  // map does not fit next to a useful chunk: read tables via L1/L2
     map_bytes = 0;
   }
   const size_t room = budget - fixed - map_bytes - 128;
   int cap = p.threads;
-  while (cap > 1 && chunk_bytes(cap, D) > room) cap -= 16;
+  while (cap > 1 && chunk_bytes(cap, D, d.R) > room) cap -= 16;
   p.chunk_cap = std::max(1, cap);
-  p.slot_cap = p.chunk_cap + std::max(32, p.chunk_cap / 8);
+  p.slot_cap = p.chunk_cap + extra_slots(p.chunk_cap);
   p.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)env->n_sm * SP_CTAS_PER_SM,
                                                          (lanes + 15) / 16));
   p.cta_begin = cta_ranges(off, p.grid);
   p.grid = (int)p.cta_begin.size() - 1;
-  p.smem = map_bytes + fixed + align_up(chunk_bytes(p.chunk_cap, D), 128);
+  p.smem = map_bytes + fixed + align_up(chunk_bytes(p.chunk_cap, D, d.R), 128);
   return p;
 }
 
@@ -427,6 +429,8 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   TRY(env->alloc(&d.step, n));
   TRY(env->alloc(&d.delay, n));
   TRY(env->alloc(&d.needs_reset, n, 1));
+  d.R_pad = (env->R + 3) & ~3;
+  TRY(env->alloc(&d.lastq, n * (size_t)d.R_pad, 0x18));  // no history yet: 24 steps
   TRY(env->alloc(&d.episodes, n));
   TRY(env->alloc(&d.arrivals, n));
   TRY(env->alloc(&d.first_event, n, 0xff));

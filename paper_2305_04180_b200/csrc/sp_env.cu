@@ -126,7 +126,7 @@ __device__ __forceinline__ bool disc_hits(const MapView& mv, const EnvDev& d, do
 // signs and the current cell.
 struct Ray {
   double x0, y0, dx, dy, idx, idy, t;
-  int ix, iy, sx, sy;
+  int ix, iy, sx, sy, n;  // n: march steps taken (scheduling history)
 };
 
 // 1/v to within an ulp: fp32 seed + two fp64 Newton steps (no DDIV).
@@ -139,6 +139,15 @@ __device__ __forceinline__ double recip(double v) {
   r = r * (2.0 - v * r);
   r = r * (2.0 - v * r);
   return r;
+}
+
+// Exact int <-> double conversions on the fp64 pipe instead of the slower
+// conversion unit: |v| < 2^31 sits in the low mantissa word of v + 2^52.
+__device__ __forceinline__ double i2d(int n) {  // n >= 0
+  return __hiloint2double(0x43300000, n) - 4503599627370496.0;
+}
+__device__ __forceinline__ int floor_i(double v) {  // floor(v), |v| < 2^31
+  return __double2loint(__dadd_rd(v, 4503599627370496.0));
 }
 
 // One march step, branch-free: every lane of the warp executes it, and only
@@ -161,13 +170,13 @@ __device__ __forceinline__ bool ray_step(Ray& r, bool live, const MapView& mv, c
   const int two_r = (int)(code << 1);
   const int ex = cellwise ? r.ix : (r.ix & ~1) + fx + r.sx * two_r;
   const int ey = cellwise ? r.iy : (r.iy & ~1) + fy + r.sy * two_r;
-  const double tx = ((double)(ex + fx) - r.x0) * r.idx;
-  const double ty = ((double)(ey + fy) - r.y0) * r.idy;
+  const double tx = (i2d(ex + fx) - r.x0) * r.idx;
+  const double ty = (i2d(ey + fy) - r.y0) * r.idy;
   const bool xs = tx <= ty;
   const double t = xs ? tx : ty;
   // the cell on the other axis at the exit point, between the current cell
   // and the forward edge (the ray moves monotonically)
-  const int c = (int)floor(xs ? fma(tx, r.dy, r.y0) : fma(ty, r.dx, r.x0));
+  const int c = floor_i(xs ? fma(tx, r.dy, r.y0) : fma(ty, r.dx, r.x0));
   const int cy = r.sy > 0 ? min(max(c, r.iy), ey) : max(min(c, r.iy), ey);
   const int cx = r.sx > 0 ? min(max(c, r.ix), ex) : max(min(c, r.ix), ex);
   const int nx = xs ? ex + r.sx : cx;
@@ -176,6 +185,7 @@ __device__ __forceinline__ bool ray_step(Ray& r, bool live, const MapView& mv, c
   const bool out = !kBordered && ((unsigned)nx >= (unsigned)d.W || (unsigned)ny >= (unsigned)d.H);
   hit = occupied ? r.iy * d.W + r.ix : -1;
   const bool finished = occupied || over || out;
+  r.n += live ? 1 : 0;
   if (live && !occupied) {
     r.t = over ? d.max_range : t;
     if (!finished) {
@@ -200,6 +210,7 @@ __device__ __forceinline__ bool ray_setup(Ray& r, double x0, double y0, double c
   r.sx = dx >= 0.0 ? 1 : -1;  // dx == 0: idx = +inf, the x face is never taken
   r.sy = dy >= 0.0 ? 1 : -1;
   r.t = 0.0;
+  r.n = 0;
   r.ix = (int)floor(r.x0);
   r.iy = (int)floor(r.y0);
   if ((unsigned)r.ix >= (unsigned)d.W || (unsigned)r.iy >= (unsigned)d.H) {  // :37-39
@@ -216,15 +227,20 @@ struct Chunk {
   double *px, *py, *ch, *sh, *sig;  // per slot: scan origin, heading cos/sin, noise std
   uint64_t* nctr;  // per slot: first Philox block of the slot's LiDAR noise
   uint32_t* gid;   // per slot: the env's stream lane (global env id)
-  int32_t* list;   // queue order: slot of each group of R rays
+  int32_t* list;   // slots in dispatch order (longest predicted scan first)
+  int32_t* reg;    // slots in registration order
+  int32_t* hread;  // per slot: global slot whose step-count history predicts this scan, or -1
+  int32_t* hwrite; // per slot: global slot whose history this scan refreshes, or -1
   int32_t* xslot;  // per env: post-reset slot, -1 if none
   uint8_t* wmode;  // per env: which rows to write (see kernel)
   uint8_t* prox;   // per slot: some ray ended closer than the proximity range
+  uint8_t* sbucket;  // per slot: predicted work bucket (0 = longest)
   int* ctl;        // [0] ray-queue head [1] slots listed [2] extra slots used [3] overflow
+                   // [4..11] bucket counts, [12..19] bucket offsets
   float* stage;    // slots x D staging rows
 };
 
-__device__ __forceinline__ Chunk chunk_smem(uint8_t* base, int cap, int slots, int D) {
+__device__ __forceinline__ Chunk chunk_smem(uint8_t* base, int cap, int slots, int D, int R) {
   Chunk c;
   c.px = (double*)base;
   c.py = c.px + slots;
@@ -235,10 +251,15 @@ __device__ __forceinline__ Chunk chunk_smem(uint8_t* base, int cap, int slots, i
   c.stage = (float*)(c.nctr + slots);
   c.gid = (uint32_t*)(c.stage + (size_t)slots * D);
   c.list = (int32_t*)(c.gid + slots);
-  c.xslot = c.list + slots;
+  c.reg = c.list + slots;
+  c.hread = c.reg + slots;
+  c.hwrite = c.hread + slots;
+  c.xslot = c.hwrite + slots;
   c.ctl = c.xslot + cap;
-  c.wmode = (uint8_t*)(c.ctl + 4);
+  c.wmode = (uint8_t*)(c.ctl + 20);
   c.prox = c.wmode + cap;
+  c.sbucket = c.prox + slots;
+  (void)R;
   return c;
 }
 
@@ -268,6 +289,7 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
   Ray ra, rb;
   ra.ix = ra.iy = rb.ix = rb.iy = 0;
   ra.sx = ra.sy = rb.sx = rb.sy = 1;
+  ra.n = rb.n = 0;
   ra.x0 = ra.y0 = rb.x0 = rb.y0 = 0.5;
   ra.dx = ra.dy = rb.dx = rb.dy = 1.0;
   ra.idx = ra.idy = rb.idx = rb.idy = 1.0;
@@ -278,11 +300,11 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
     const int na = __popc(ia), n_idle = na + __popc(ib);
     if (n_idle >= d.refill_min || drained) {
       if (done_a) {
-        fin(ea, ja, ra.t, hit_a);
+        fin(ea, ja, ra.t, hit_a, ra.n);
         done_a = false;
       }
       if (done_b) {
-        fin(eb, jb, rb.t, hit_b);
+        fin(eb, jb, rb.t, hit_b, rb.n);
         done_b = false;
       }
       if (drained) {
@@ -326,6 +348,51 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
       done_b = done_b || fb;
     }
   }
+}
+
+// Longest-first order (LPT) of the chunk's scans: a scan's predicted work is
+// the mean number of march steps its env's beams took last step (the robot
+// moves <= 1.8 cm and turns <= 0.1 rad per step); unknown history (fresh
+// spawns) counts as long.  Slots are counting-sorted into 8 work buckets and
+// c.list is rewritten longest first; rays are then dispatched slot-major, so
+// the queue tail holds the cheapest scans.
+__device__ __forceinline__ int work_bucket(uint32_t steps) {
+  return steps >= 24 ? 0 : steps >= 16 ? 1 : steps >= 12 ? 2 : steps >= 9 ? 3
+       : steps >= 7 ? 4 : steps >= 5 ? 5 : steps >= 3 ? 6 : 7;
+}
+
+// predicted bucket of one scan (called by the thread that registers it)
+__device__ __forceinline__ uint8_t scan_bucket(const EnvDev& d, int32_t hread) {
+  if (hread < 0) return 0;
+  const uint32_t* q = (const uint32_t*)(d.lastq + (int64_t)hread * d.R_pad);
+  uint32_t sum = 0;
+  for (int w = 0; w < (d.R + 3) >> 2; ++w) {
+    const uint32_t v = q[w];
+    sum += (v & 0xff) + ((v >> 8) & 0xff) + ((v >> 16) & 0xff) + (v >> 24);
+  }
+  return (uint8_t)work_bucket(sum / (uint32_t)d.R_pad);
+}
+
+__device__ __forceinline__ void order_slots(const Chunk& c, int n_slots) {
+  int* cnt = c.ctl + 4;
+  int* off = c.ctl + 12;
+  if (threadIdx.x < 8) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  for (int k = threadIdx.x; k < n_slots; k += blockDim.x) atomicAdd(&cnt[c.sbucket[c.reg[k]]], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 0; b < 8; ++b) {
+      off[b] = acc;
+      acc += cnt[b];
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < n_slots; k += blockDim.x) {
+    const int slot = c.reg[k];
+    c.list[atomicAdd(&off[c.sbucket[slot]], 1)] = slot;
+  }
+  __syncthreads();  // c.list complete before anyone dispatches from it
 }
 
 __device__ __forceinline__ void set_error(const EnvDev& d, int code, int64_t row) {
@@ -395,14 +462,17 @@ __device__ __forceinline__ double div_by(double v, double m, double inv_m) {
 // is "some ray < 30", core.py:205).
 struct FinObs {
   Chunk c;
-  int D;
+  int D, R_pad;
   double max_range, inv_max_range, proximity;
-  __device__ __forceinline__ void operator()(int slot, int j, double t, int) const {
+  uint8_t* lastq;
+  __device__ __forceinline__ void operator()(int slot, int j, double t, int, int steps) const {
     float* rowp = c.stage + slot * D;
     const double z = (double)rowp[5 + j];
     const double v = dclip(dadd(t, dadd(0.0, dmul(c.sig[slot], z))), 0.0, max_range);
     rowp[5 + j] = (float)div_by(v, max_range, inv_max_range);
     if (t < proximity) c.prox[slot] = 1;
+    const int hw = c.hwrite[slot];
+    if (hw >= 0) lastq[(int64_t)hw * R_pad + j] = (uint8_t)min(steps, 254);
   }
 };
 
@@ -435,13 +505,17 @@ __device__ __forceinline__ MapView bind_map(const EnvDev& d, int m, uint8_t* sme
 }
 
 // Register a scan slot: origin, heading, noise stream position; queue it.
-__device__ __forceinline__ void add_slot(const Chunk& c, int slot, double x, double y, double ch,
-                                         double sh, double sig, uint32_t gid, uint64_t nctr) {
+__device__ __forceinline__ void add_slot(const EnvDev& d, const Chunk& c, int slot, double x,
+                                         double y, double ch, double sh, double sig, uint32_t gid,
+                                         uint64_t nctr, int32_t hread, int32_t hwrite) {
+  c.sbucket[slot] = scan_bucket(d, hread);
+  c.hread[slot] = hread;
+  c.hwrite[slot] = hwrite;
   c.px[slot] = x; c.py[slot] = y; c.ch[slot] = ch; c.sh[slot] = sh; c.sig[slot] = sig;
   c.gid[slot] = gid;
   c.nctr[slot] = nctr;
   c.prox[slot] = 0;
-  c.list[atomicAdd(&c.ctl[1], 1)] = slot;
+  c.reg[atomicAdd(&c.ctl[1], 1)] = slot;
 }
 
 // core.py:114-156 for one lane (stream bound to gid): resample, spawn, write
@@ -483,7 +557,7 @@ __device__ __forceinline__ bool reset_env(const EnvDev& d, const MapView& mv, co
   for (int wi = 0; wi < ((delay + 15) >> 4); ++wi) d.hist[(int64_t)wi * d.n + s] = ~0ull;
   header_row(mc, x, y, bearing_error(x, y, th, mc.goal_x, mc.goal_y), c0, s0, 0.0, 0.0, vml, vma,
              c.stage + slot * d.D);
-  add_slot(c, slot, x, y, c0, s0, sig, gid, ctr);
+  add_slot(d, c, slot, x, y, c0, s0, sig, gid, ctr, -1, (int32_t)s);
   ctr += d.nb;
   return true;
 }
@@ -523,14 +597,14 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
   extern __shared__ __align__(128) uint8_t smem[];
   double2* beam = (double2*)(smem + d.off_beam);
   uint64_t* bar = (uint64_t*)(smem + d.off_bar);
-  const Chunk c = chunk_smem(smem + d.off_chunk, d.chunk_cap, d.slot_cap, d.D);
+  const Chunk c = chunk_smem(smem + d.off_chunk, d.chunk_cap, d.slot_cap, d.D, d.R);
   for (int j = threadIdx.x; j < d.R; j += blockDim.x) beam[j] = d.beam_cs[j];
   if (threadIdx.x == 0 && kSmem) mbar_init(bar, 1);
   __syncthreads();
   uint32_t phase = 0;
   const int64_t sb = d.cta_begin[blockIdx.x], se = d.cta_begin[blockIdx.x + 1];
   const int D = d.D;
-  const FinObs fin{c, D, d.max_range, d.inv_max_range, d.proximity};
+  const FinObs fin{c, D, d.R_pad, d.max_range, d.inv_max_range, d.proximity, d.lastq};
   int m = 0, cur_map = -1;
   MapView mv{};
   for (int64_t s0 = sb; s0 < se;) {
@@ -645,7 +719,8 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
         }
         header_row(mc, x, y, alpha, d.c0[s], d.s0[s], vl, va, vml, vma, c.stage + e * D);
         // the post-step scan (core.py:203-206); cos/sin of h1 == of wrap(h1)
-        add_slot(c, e, x, y, cos1, sin1, d.psig[s], gid, ctr);
+        add_slot(d, c, e, x, y, cos1, sin1, d.psig[s], gid, ctr, (int32_t)s,
+                 ended && d.auto_reset ? -1 : (int32_t)s);
         ctr += d.nb;
         d.x[s] = x; d.y[s] = y; d.h[s] = h; d.vl[s] = vl; d.va[s] = va;
         d.step[s] = step;
@@ -671,7 +746,8 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     }
     __syncthreads();
     const int n_slots = c.ctl[1];
-    // ---- N: LiDAR noise; B: LiDAR rays --------------------------------------
+    // ---- N: LiDAR noise + longest-first ray order; B: LiDAR rays ------------
+    order_slots(c, n_slots);
     noise_phase(d, c, n_slots);
     __syncthreads();
     ray_phase<kBordered, false>(mv, d, c, beam, n_slots, fin);
@@ -723,6 +799,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       }
       __syncthreads();
       const int n2 = c.ctl[1];
+      order_slots(c, n2);
       noise_phase(d, c, n2);
       __syncthreads();
       ray_phase<kBordered, false>(mv, d, c, beam, n2, fin);
@@ -739,7 +816,7 @@ struct FinScan {
   int32_t* hit_cell;
   int64_t s0;
   int R;
-  __device__ __forceinline__ void operator()(int e, int j, double t, int hit) const {
+  __device__ __forceinline__ void operator()(int e, int j, double t, int hit, int) const {
     const int64_t o = (s0 + e) * R + j;
     ranges[o] = t;
     if (hit_cell) hit_cell[o] = hit;
@@ -752,7 +829,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
   extern __shared__ __align__(128) uint8_t smem[];
   double2* beam = (double2*)(smem + d.off_beam);
   uint64_t* bar = (uint64_t*)(smem + d.off_bar);
-  const Chunk c = chunk_smem(smem + d.off_chunk, d.chunk_cap, d.slot_cap, d.D);
+  const Chunk c = chunk_smem(smem + d.off_chunk, d.chunk_cap, d.slot_cap, d.D, d.R);
   for (int j = threadIdx.x; j < d.R; j += blockDim.x) beam[j] = d.beam_cs[j];
   if (threadIdx.x == 0 && kSmem) mbar_init(bar, 1);
   __syncthreads();

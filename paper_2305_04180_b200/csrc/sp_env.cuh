@@ -6,7 +6,7 @@
 // CTAs per SM let one CTA's ray-queue tail and phase barriers overlap the
 // other's work; each holds its own copy of its map's tables.
 #ifndef SP_CTAS_PER_SM
-#define SP_CTAS_PER_SM 2
+#define SP_CTAS_PER_SM 1
 #endif
 #define SP_CTA_THREADS (768 / SP_CTAS_PER_SM)
 
@@ -42,6 +42,8 @@ struct EnvDev {
   uint64_t* ctr;          // Philox block counter per lane
   int32_t *step, *delay;
   uint8_t* needs_reset;
+  uint8_t* lastq;         // n x R_pad: march steps each beam took last scan (254 cap)
+  int32_t R_pad;          // R rounded up to a multiple of 4 (lastq row stride)
   const double* ranges;   // 12 doubles per lane (or shared when ranges_shared)
   int32_t ranges_shared;
   const int64_t* env_of_slot;
