@@ -64,14 +64,14 @@ def load_maps():
     return lm(N_MAPS)
 
 
-def ncu_traffic():
-    """DRAM bytes per env_step_kernel launch from the committed ncu capture."""
+def ncu_metrics():
+    """Per-launch metrics of env_step_kernel from the committed ncu capture
+    (DRAM traffic, issue-slot utilization): profiles/ncu_step_traffic.json."""
     p = os.path.join(ROOT, "profiles", "ncu_step_traffic.json")
     if not os.path.exists(p):
-        return None, None
+        return {}
     with open(p) as f:
-        d = json.load(f)
-    return d.get("traffic_bytes_per_launch"), d.get("source")
+        return json.load(f)
 
 
 def measured_peaks():
@@ -303,7 +303,8 @@ def run_ours(args, rank, world, local_rank):
         mean_launch = t_dev / K
         achieved = BYTES_PER_ENV_STEP * n / mean_launch / 1e9
         info = env.launch_info()
-        traffic, traffic_src = ncu_traffic() if n == N_PER_GPU else (None, None)
+        nm = ncu_metrics() if n == N_PER_GPU else {}
+        traffic, traffic_src = nm.get("traffic_bytes_per_launch"), nm.get("source")
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": t_dev_max / K * 1e3, "higher_is_better": True,
@@ -327,6 +328,10 @@ def run_ours(args, rank, world, local_rank):
                          "algorithmic_bytes_per_env_step": BYTES_PER_ENV_STEP,
                          "kernel": "env_step_kernel", "mean_launch_ms": mean_launch * 1e3,
                          "note": "issue/latency-bound (fp64 LiDAR march); see DESIGN.md 4"},
+            "compute_roofline": {"bound": "issue", "unit": "% of issue slots (4/clk/SM)",
+                                 "achieved": nm.get("issue_active_pct"),
+                                 "simt_threads_per_inst": nm.get("simt_threads_per_inst"),
+                                 "source": nm.get("source")},
             "clocks": clocks.summary(),
             "gpu_launches": K,
             "per_step_ms": {"min": min(per_step), "median": statistics.median(per_step),
