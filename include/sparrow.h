@@ -26,6 +26,7 @@
  *   sp_rb_size          replay.py:45-46 (__len__)
  *   sp_rb_gather        replay.py:81-87 (snapshot: rows in storage order)
  *   sp_random_actions   bench.py:97-105 (random policy actions), on device
+ *   sp_philox_fill      asl/vem.py:57-66 draws (rng.random / rng.integers), on device
  */
 #ifndef SPARROW_H_
 #define SPARROW_H_
@@ -163,6 +164,11 @@ int sp_rb_gather(SpReplay* rb, float* states, int64_t* actions, float* rewards,
                  float* next_states, uint8_t* dones, void* stream);
 
 /* ---- benchmark helpers ----------------------------------------------------- */
+/* Philox stream draws on device (DESIGN.md RNG contract), blocks ctr0 .. ctr0+n-1 of
+ * (seed, lane, tag): kind 0 -> double out[i] = uniform(lo, hi); kind 1 -> int64
+ * out[i] = integers(lo, hi).  The VEM epsilon-greedy draws (asl/vem.py:57-66). */
+int sp_philox_fill(int64_t n, uint64_t seed, uint32_t lane, uint32_t tag, uint64_t ctr0,
+                   int kind, double lo, double hi, void* out, void* stream);
 /* actions[i] = integers(0, n_actions) from block `step` of (seed, env_id0 + i, tag 1) */
 int sp_random_actions(int64_t n, uint64_t seed, int64_t env_id0, int64_t step, int32_t n_actions,
                       int64_t* actions, void* stream);

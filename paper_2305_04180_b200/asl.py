@@ -1,0 +1,595 @@
+"""Actor-Sharer-Learner on the GPU (BASELINE cfg5).
+
+Restates the reference's learner side in torch on the same device as the
+environment, so the whole ASL loop runs without host round-trips:
+
+* ``QNet``: the [5+R, 256, 128, 5] ReLU MLP of ``net.py``.
+  - He-uniform fan-in init from a numpy Generator, so a given rng yields the
+    reference's exact initial weights (``net.py:52-60``).
+  - Explicit backprop of the mean Huber(delta=1) loss on the chosen-action
+    outputs (``net.py:88-115``).
+  - Bias-corrected Adam in the reference's operation order
+    (``net.py:141-161``).
+  - The ``COLORNET`` checkpoint format (``net.py:178-228``), byte-compatible.
+* ``compute_targets`` / ``DdqnLearner``: double-DQN (``ddqn.py:38-77``).
+* ``VemSchedule`` / ``select_actions``: per-copy epsilon-greedy
+  (``asl/vem.py``).  Draws come from a device-side Philox stream
+  (``sp_philox_fill``) with the reference's call order: ``random(n)``, then
+  ``integers(0, A, n)``.
+* ``TfmConfig`` / ``TfmState``: time-feedback pacing (``asl/tfm.py``).
+* ``Sharer``, ``actor_loop``, ``learner_loop``, ``start_session``,
+  ``Session``: the two-thread ASL session (``asl/sharer.py``,
+  ``asl/loops.py``).  Each thread runs on its own CUDA stream; the GPU
+  replay ring orders appends and samples with CUDA events.
+
+Matmuls are plain cuBLAS through torch (library GEMM). TF32 is disabled, so
+the fp32 numerics follow the numpy reference to ~1e-6.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import io
+import math
+import struct
+import threading
+import time
+import zlib
+from dataclasses import dataclass, field
+from typing import NamedTuple
+
+import numpy as np
+
+from paper_2305_04180_b200 import _lib
+from paper_2305_04180_b200.replay import BufferNotReady, PhiloxGenerator, ReplayBuffer
+
+CHECKPOINT_MAGIC = b"COLORNET"  # net.py:19-20
+CHECKPOINT_FORMAT_VERSION = 1
+HIDDEN = (256, 128)
+
+
+class CheckpointError(ValueError):
+    """Malformed, truncated, or shape-incompatible checkpoint data."""
+
+
+class TrainingDiverged(RuntimeError):
+    """A non-finite loss appeared during optimization (ddqn.py:68-71)."""
+
+
+def _torch():
+    import torch
+    torch.backends.cuda.matmul.allow_tf32 = False
+    return torch
+
+
+# -- Q-network (net.py) -----------------------------------------------------------
+
+class QNet:
+    """Weights (fan_in, fan_out) and biases as float32 CUDA tensors + version."""
+
+    def __init__(self, weights, biases, version: int = 0):
+        self.weights = list(weights)
+        self.biases = list(biases)
+        self.version = int(version)
+
+    @property
+    def sizes(self) -> tuple:
+        return (int(self.weights[0].shape[0]),) + tuple(int(w.shape[1]) for w in self.weights)
+
+    @classmethod
+    def init(cls, rng: np.random.Generator, sizes, device=None) -> "QNet":
+        """He-style uniform fan-in init, zero biases (net.py:52-60)."""
+        torch = _torch()
+        dev = _lib.require_cuda(device)
+        ws, bs = [], []
+        for fan_in, fan_out in zip(sizes[:-1], sizes[1:]):
+            bound = np.sqrt(6.0 / fan_in)
+            w = rng.uniform(-bound, bound, (fan_in, fan_out)).astype(np.float32)
+            ws.append(torch.from_numpy(w).to(dev))
+            bs.append(torch.zeros(fan_out, dtype=torch.float32, device=dev))
+        return cls(ws, bs)
+
+    @classmethod
+    def from_numpy(cls, weights, biases, version=0, device=None) -> "QNet":
+        torch = _torch()
+        dev = _lib.require_cuda(device)
+        return cls([torch.as_tensor(np.asarray(w, np.float32)).to(dev) for w in weights],
+                   [torch.as_tensor(np.asarray(b, np.float32)).to(dev) for b in biases], version)
+
+    def copy(self) -> "QNet":
+        return QNet([w.clone() for w in self.weights], [b.clone() for b in self.biases],
+                    self.version)
+
+    def copy_from(self, other: "QNet") -> None:
+        for a, b in zip(self.weights, other.weights):
+            a.copy_(b)
+        for a, b in zip(self.biases, other.biases):
+            a.copy_(b)
+        self.version = other.version
+
+    def forward_cached(self, states):
+        """Forward pass keeping pre-activations for backprop (net.py:63-74)."""
+        torch = _torch()
+        h = states.to(torch.float32)
+        acts, pre = [h], []
+        last = len(self.weights) - 1
+        for li, (w, b) in enumerate(zip(self.weights, self.biases)):
+            z = torch.addmm(b, h, w)
+            pre.append(z)
+            h = z if li == last else torch.relu(z)
+            acts.append(h)
+        return acts, pre
+
+    def forward(self, states):
+        """Batched Q-values (B, n_actions) (net.py:77-80)."""
+        return self.forward_cached(states)[0][-1]
+
+    # -- checkpoints (net.py:178-228) ----------------------------------------
+    def to_bytes(self) -> bytes:
+        buf = io.BytesIO()
+        buf.write(CHECKPOINT_MAGIC)
+        sizes = self.sizes
+        buf.write(struct.pack("<II", CHECKPOINT_FORMAT_VERSION, len(sizes)))
+        buf.write(struct.pack(f"<{len(sizes)}I", *sizes))
+        for w, b in zip(self.weights, self.biases):
+            buf.write(np.ascontiguousarray(w.cpu().numpy(), dtype="<f4").tobytes())
+            buf.write(np.ascontiguousarray(b.cpu().numpy(), dtype="<f4").tobytes())
+        buf.write(struct.pack("<Q", self.version))
+        return buf.getvalue()
+
+    @classmethod
+    def from_bytes(cls, data: bytes, expect_sizes=None, device=None) -> "QNet":
+        buf = io.BytesIO(data)
+
+        def read(n, what):
+            chunk = buf.read(n)
+            if len(chunk) != n:
+                raise CheckpointError(f"truncated checkpoint while reading {what}")
+            return chunk
+
+        if read(len(CHECKPOINT_MAGIC), "magic") != CHECKPOINT_MAGIC:
+            raise CheckpointError("bad magic bytes; not a COLORNET checkpoint")
+        fmt, n_sizes = struct.unpack("<II", read(8, "header"))
+        if fmt != CHECKPOINT_FORMAT_VERSION:
+            raise CheckpointError(f"unsupported checkpoint format version {fmt}")
+        if not 2 <= n_sizes <= 64:
+            raise CheckpointError(f"implausible layer count {n_sizes}")
+        sizes = struct.unpack(f"<{n_sizes}I", read(4 * n_sizes, "layer sizes"))
+        if expect_sizes is not None and tuple(sizes) != tuple(expect_sizes):
+            raise CheckpointError(f"layer sizes {tuple(sizes)} do not match {tuple(expect_sizes)}")
+        ws, bs = [], []
+        for fan_in, fan_out in zip(sizes[:-1], sizes[1:]):
+            ws.append(np.frombuffer(read(4 * fan_in * fan_out, "weights"), "<f4")
+                      .reshape(fan_in, fan_out).copy())
+            bs.append(np.frombuffer(read(4 * fan_out, "biases"), "<f4").copy())
+        (version,) = struct.unpack("<Q", read(8, "version"))
+        if buf.read(1):
+            raise CheckpointError("trailing bytes after checkpoint payload")
+        return cls.from_numpy(ws, bs, version, device)
+
+
+def huber_residual_grad(residual):
+    """d mean-Huber(delta=1) / d residual, before the 1/B (net.py:83-105)."""
+    return residual.clamp(-1.0, 1.0)
+
+
+def backward(net: QNet, states, actions, targets):
+    """Gradients of the mean Huber loss on q[i, a_i] (net.py:88-115).
+    Returns (grad_w, grad_b, loss tensor, mean |td| tensor)."""
+    torch = _torch()
+    acts, pre = net.forward_cached(states)
+    q = acts[-1]
+    batch = q.shape[0]
+    rows = torch.arange(batch, device=q.device)
+    residual = q[rows, actions] - targets.to(q.dtype)
+    a = residual.abs()
+    loss = torch.where(a <= 1.0, 0.5 * residual * residual, a - 0.5).mean()
+    mean_abs_td = a.mean()
+    dq = torch.zeros_like(q)
+    dq[rows, actions] = huber_residual_grad(residual) / batch
+    gw = [None] * len(net.weights)
+    gb = [None] * len(net.biases)
+    delta = dq
+    for li in range(len(net.weights) - 1, -1, -1):
+        gw[li] = acts[li].t() @ delta
+        gb[li] = delta.sum(dim=0)
+        if li > 0:
+            delta = (delta @ net.weights[li].t()) * (pre[li - 1] > 0)
+    return gw, gb, loss, mean_abs_td
+
+
+@dataclass
+class AdamState:  # net.py:118-139
+    lr: float = 1e-4
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    step: int = 0
+    m_weights: list = field(default_factory=list)
+    v_weights: list = field(default_factory=list)
+    m_biases: list = field(default_factory=list)
+    v_biases: list = field(default_factory=list)
+
+    @classmethod
+    def for_params(cls, net: QNet, lr: float = 1e-4) -> "AdamState":
+        torch = _torch()
+        z = torch.zeros_like
+        return cls(lr=lr, m_weights=[z(w) for w in net.weights], v_weights=[z(w) for w in net.weights],
+                   m_biases=[z(b) for b in net.biases], v_biases=[z(b) for b in net.biases])
+
+
+def _adam_update(p, g, m, v, st: AdamState, t: int) -> None:  # net.py:141-148
+    torch = _torch()
+    m.mul_(st.beta1).add_((1.0 - st.beta1) * g)
+    v.mul_(st.beta2).add_((1.0 - st.beta2) * torch.square(g))
+    m_hat = m / (1.0 - st.beta1 ** t)
+    v_hat = v / (1.0 - st.beta2 ** t)
+    p.sub_(st.lr * m_hat / (torch.sqrt(v_hat) + st.eps))
+
+
+def adam_step(net: QNet, gw, gb, st: AdamState) -> QNet:  # net.py:151-161
+    st.step += 1
+    t = st.step
+    for li in range(len(net.weights)):
+        _adam_update(net.weights[li], gw[li], st.m_weights[li], st.v_weights[li], st, t)
+        _adam_update(net.biases[li], gb[li], st.m_biases[li], st.v_biases[li], st, t)
+    net.version += 1
+    return net
+
+
+# -- DDQN (ddqn.py) ---------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class DdqnConfig:
+    gamma: float = 0.98
+    target_sync_period: int = 200
+    batch_size: int = 256
+    lr: float = 1e-4
+
+    def __post_init__(self):
+        if not 0.0 <= self.gamma < 1.0:
+            raise ValueError(f"gamma must lie in [0, 1), got {self.gamma}")
+        if self.target_sync_period < 1 or self.batch_size < 1:
+            raise ValueError("target_sync_period and batch_size must be positive")
+
+
+class UpdateStats(NamedTuple):
+    loss: float
+    mean_abs_td: float
+    version: int
+    target_synced: bool
+
+
+def compute_targets(batch, online: QNet, target: QNet, gamma: float):
+    """y = r + gamma (1 - done) Q_target(s', argmax_a Q_online(s', a)) (ddqn.py:38-51);
+    argmax ties break toward the lowest index."""
+    torch = _torch()
+    best = torch.argmax(online.forward(batch.next_states), dim=1)
+    q_target = target.forward(batch.next_states)
+    bootstrap = q_target[torch.arange(best.shape[0], device=best.device), best]
+    not_done = (~batch.dones.bool()).to(q_target.dtype)
+    return batch.rewards.to(q_target.dtype) + gamma * not_done * bootstrap
+
+
+class DdqnLearner:
+    """Online/target pair and one update per batch (ddqn.py:54-77)."""
+
+    def __init__(self, params: QNet, config: DdqnConfig | None = None, check_finite: bool = True):
+        self.config = config or DdqnConfig()
+        self.online = params
+        self.target = params.copy()
+        self.adam = AdamState.for_params(params, lr=self.config.lr)
+        self.update_count = 0
+        self.check_finite = check_finite
+
+    def update(self, batch) -> UpdateStats:
+        targets = compute_targets(batch, self.online, self.target, self.config.gamma)
+        gw, gb, loss, mad = backward(self.online, batch.states, batch.actions, targets)
+        loss_v = float(loss) if self.check_finite else float("nan")
+        if self.check_finite and not math.isfinite(loss_v):
+            raise TrainingDiverged(f"non-finite loss {loss_v!r} at update {self.update_count + 1} "
+                                   f"(parameter version {self.online.version})")
+        adam_step(self.online, gw, gb, self.adam)
+        self.update_count += 1
+        synced = self.update_count % self.config.target_sync_period == 0
+        if synced:
+            self.target.copy_from(self.online)
+        return UpdateStats(loss_v, float(mad) if self.check_finite else float("nan"),
+                           self.online.version, synced)
+
+
+# -- VEM (asl/vem.py) ------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class VemSchedule:
+    n_envs: int
+    or_init: int = 16
+    or_final: int = 3
+    decay_steps: int = 500_000
+    e_min: float = 0.01
+    e_max: float = 0.8
+
+    def __post_init__(self):
+        if not 1 <= self.or_final <= self.or_init <= self.n_envs:
+            raise ValueError(f"need 1 <= or_final <= or_init <= n_envs, got "
+                             f"{self.or_final}, {self.or_init}, {self.n_envs}")
+        if not 0.0 <= self.e_min <= self.e_max <= 1.0:
+            raise ValueError("need 0 <= e_min <= e_max <= 1")
+        if self.decay_steps < 1:
+            raise ValueError("decay_steps must be positive")
+
+    def exploring_interval(self, t_step: int) -> int:  # vem.py:38-40
+        frac = min(t_step / self.decay_steps, 1.0)
+        return int(math.floor(self.or_init + (self.or_final - self.or_init) * frac + 0.5))
+
+    def epsilons(self, t_step: int) -> np.ndarray:  # vem.py:42-54, vectorized
+        size = self.exploring_interval(t_step)
+        first = self.n_envs - size
+        i = np.arange(self.n_envs)
+        ramp = self.e_min + (self.e_max - self.e_min) * (i - first) / max(size - 1, 1)
+        eps = np.where(i < first, self.e_min, ramp)
+        eps[-1] = self.e_max if size >= 1 else eps[-1]
+        return eps.astype(np.float64)
+
+    def epsilon(self, i: int, t_step: int) -> float:
+        if not 0 <= i < self.n_envs:
+            raise ValueError(f"copy index {i} out of range [0, {self.n_envs})")
+        return float(self.epsilons(t_step)[i])
+
+
+def philox_fill(n: int, stream, kind: int, lo: float, hi: float, device=None):
+    """Device draws from a PhiloxGenerator-like stream (seed, lane, ctr, tag);
+    advances its counter by n blocks.  kind 0: uniform f64, kind 1: integers."""
+    torch = _torch()
+    dev = _lib.require_cuda(device)
+    out = torch.empty(n, dtype=torch.float64 if kind == 0 else torch.int64, device=dev)
+    tag = int(getattr(stream, "tag", 3))
+    _lib.check(_lib.load().sp_philox_fill(n, stream.seed, stream.lane, tag, stream.ctr, kind,
+                                          float(lo), float(hi), out.data_ptr(),
+                                          _lib.stream_ptr(dev)), "philox_fill")
+    stream.ctr += n
+    return out
+
+
+def select_actions(q, epsilons, rng):
+    """Row-wise epsilon-greedy on device (vem.py:57-66): random action with
+    probability eps (draws: random(n), then integers(0, A, n)), else argmax
+    (ties to the lowest index)."""
+    torch = _torch()
+    n, n_actions = q.shape
+    eps = torch.as_tensor(epsilons, dtype=torch.float64, device=q.device)
+    explore = philox_fill(n, rng, 0, 0.0, 1.0, q.device) < eps
+    randoms = philox_fill(n, rng, 1, 0, n_actions, q.device)
+    greedy = torch.argmax(q, dim=1)
+    return torch.where(explore, randoms, greedy)
+
+
+# -- TFM (asl/tfm.py) -------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class TfmConfig:
+    n_envs: int
+    tps: float
+    batch_size: int
+    warmup_samples: int = 10
+    max_sleep_s: float = 1.0
+
+    def __post_init__(self):
+        if self.n_envs < 1 or self.batch_size < 1 or self.tps <= 0:
+            raise ValueError("n_envs, batch_size must be >= 1 and tps > 0")
+
+    @property
+    def rho(self) -> float:  # tfm.py:27-29
+        return self.n_envs * self.tps / self.batch_size
+
+
+@dataclass
+class TfmState:  # tfm.py:32-77
+    ema_factor: float = 0.1
+    v_period_s: float | None = None
+    b_period_s: float | None = None
+    v_count: int = 0
+    b_count: int = 0
+
+    def record_interaction(self, seconds: float) -> None:
+        self.v_period_s = self._ema(self.v_period_s, seconds)
+        self.v_count += 1
+
+    def record_optimization(self, seconds: float) -> None:
+        self.b_period_s = self._ema(self.b_period_s, seconds)
+        self.b_count += 1
+
+    def _ema(self, prev, sample):
+        return sample if prev is None else (1.0 - self.ema_factor) * prev + self.ema_factor * sample
+
+    def ready(self, cfg: TfmConfig) -> bool:
+        return self.v_count >= cfg.warmup_samples and self.b_count >= cfg.warmup_samples
+
+    def compute_xi(self, cfg: TfmConfig) -> float:
+        if self.v_period_s is None or self.b_period_s is None:
+            raise ValueError("both loop periods must be recorded before computing xi")
+        return cfg.rho * self.b_period_s - self.v_period_s
+
+    def actor_sleep(self, cfg: TfmConfig) -> float:
+        if not self.ready(cfg):
+            return 0.0
+        xi = self.compute_xi(cfg)
+        return min(xi, cfg.max_sleep_s) if xi > 0 else 0.0
+
+    def learner_sleep(self, cfg: TfmConfig) -> float:
+        if not self.ready(cfg):
+            return 0.0
+        xi = self.compute_xi(cfg)
+        return min(-xi / cfg.rho, cfg.max_sleep_s) if xi <= 0 else 0.0
+
+
+# -- Sharer + loops (asl/sharer.py, asl/loops.py) ------------------------------------------
+
+class PublishedModel(NamedTuple):
+    version: int
+    params: QNet
+    checksum: int
+
+
+def _checksum(params: QNet) -> int:
+    return zlib.crc32(params.to_bytes())
+
+
+def verify_snapshot(snapshot: PublishedModel) -> bool:
+    return _checksum(snapshot.params) == snapshot.checksum
+
+
+class Sharer:
+    """Replay ring + counters + versioned parameter exchange (sharer.py:34-86)."""
+
+    def __init__(self, buffer: ReplayBuffer, tfm: TfmState | None = None):
+        self.buffer = buffer
+        self.tfm = tfm or TfmState()
+        self.t_step = 0
+        self.b_step = 0
+        self.publish_count = 0
+        self.stop = threading.Event()
+        self._published: PublishedModel | None = None
+        self._error: BaseException | None = None
+
+    def publish_params(self, params: QNet) -> PublishedModel:
+        snap_params = params.copy()
+        snap = PublishedModel(params.version, snap_params, _checksum(snap_params))
+        self._published = snap  # atomic reference swap
+        self.publish_count += 1
+        return snap
+
+    def fetch_params(self, newer_than: int) -> PublishedModel | None:
+        snap = self._published
+        return snap if snap is not None and snap.version > newer_than else None
+
+    @property
+    def published_version(self):
+        snap = self._published
+        return snap.version if snap is not None else None
+
+    def measured_tps(self, batch_size: int):
+        return None if self.t_step == 0 else batch_size * self.b_step / self.t_step
+
+    def record_error(self, exc: BaseException) -> None:
+        if self._error is None:
+            self._error = exc
+        self.stop.set()
+
+    def raise_if_failed(self) -> None:
+        if self._error is not None:
+            raise self._error
+
+    @property
+    def failed(self) -> bool:
+        return self._error is not None
+
+
+_IDLE_POLL_S = 0.002
+
+
+def actor_loop(sharer: Sharer, vec_env, initial_states, params: QNet, vem: VemSchedule,
+               tfm_cfg: TfmConfig, max_steps: int, rng) -> None:
+    """loops.py:43-71 on device: forward -> VEM -> step -> append, no host data."""
+    torch = _torch()
+    dev = vec_env.device
+    with torch.cuda.stream(torch.cuda.Stream(dev)):
+        states = initial_states
+        params = params.copy()
+        version = params.version
+        n = vec_env.n_copies
+        try:
+            while sharer.t_step < max_steps and not sharer.stop.is_set():
+                started = time.perf_counter()
+                snap = sharer.fetch_params(version)
+                if snap is not None:
+                    params, version = snap.params, snap.version
+                q = params.forward(states)
+                actions = select_actions(q, vem.epsilons(sharer.t_step), rng)
+                batch = vec_env.step_batch(actions)
+                sharer.buffer.append_batch(states, actions, batch.rewards, batch.store_states,
+                                           batch.dones)
+                states = batch.states
+                torch.cuda.current_stream(dev).synchronize()  # the period TFM measures
+                sharer.tfm.record_interaction(time.perf_counter() - started)
+                sharer.t_step += n
+                nap = sharer.tfm.actor_sleep(tfm_cfg)
+                if nap > 0:
+                    time.sleep(nap)
+        finally:
+            sharer.stop.set()
+
+
+def learner_loop(sharer: Sharer, algo: DdqnLearner, tfm_cfg: TfmConfig, learn_start: int,
+                 upload_period: int, rng) -> None:
+    """loops.py:74-99 on device."""
+    torch = _torch()
+    dev = algo.online.weights[0].device
+    batch_size = tfm_cfg.batch_size
+    with torch.cuda.stream(torch.cuda.Stream(dev)):
+        while not sharer.stop.is_set():
+            if len(sharer.buffer) <= learn_start:
+                time.sleep(_IDLE_POLL_S)
+                continue
+            started = time.perf_counter()
+            try:
+                batch = sharer.buffer.sample(batch_size, rng)
+            except BufferNotReady:
+                time.sleep(_IDLE_POLL_S)
+                continue
+            algo.update(batch)
+            sharer.b_step += 1
+            if sharer.b_step % upload_period == 0:
+                sharer.publish_params(algo.online)
+            torch.cuda.current_stream(dev).synchronize()
+            sharer.tfm.record_optimization(time.perf_counter() - started)
+            nap = sharer.tfm.learner_sleep(tfm_cfg)
+            if nap > 0:
+                time.sleep(nap)
+
+
+@dataclass
+class Session:
+    sharer: Sharer
+    actor: threading.Thread
+    learner: threading.Thread
+    max_steps: int
+
+    @property
+    def running(self) -> bool:
+        return self.actor.is_alive() or self.learner.is_alive()
+
+    def wait(self, timeout: float | None = None) -> None:
+        self.actor.join(timeout)
+        self.learner.join(timeout)
+        self.sharer.raise_if_failed()
+
+    def abort(self) -> None:
+        self.sharer.stop.set()
+
+
+def _guarded(fn, sharer: Sharer, *args) -> None:
+    try:
+        fn(sharer, *args)
+    except BaseException as exc:  # noqa: BLE001 (re-raised by Session.wait)
+        sharer.record_error(exc)
+
+
+def start_session(sharer: Sharer, vec_env, initial_states, params: QNet, vem: VemSchedule,
+                  tfm_cfg: TfmConfig, max_steps: int, algo: DdqnLearner, learn_start: int,
+                  upload_period: int, seed: int) -> Session:
+    """Publish the initial model and start the actor and learner threads
+    (loops.py:130-149); their streams are (seed, 0xAC) / (seed, 0x1E)."""
+    sharer.publish_params(params)
+    actor_rng = PhiloxGenerator(seed, 0xAC)
+    actor_rng.tag = 3
+    learner_rng = PhiloxGenerator(seed, 0x1E)
+    actor = threading.Thread(target=_guarded, name="color-actor", daemon=True,
+                             args=(actor_loop, sharer, vec_env, initial_states, params, vem,
+                                   tfm_cfg, max_steps, actor_rng))
+    learner = threading.Thread(target=_guarded, name="color-learner", daemon=True,
+                               args=(learner_loop, sharer, algo, tfm_cfg, learn_start,
+                                     upload_period, learner_rng))
+    actor.start()
+    learner.start()
+    return Session(sharer, actor, learner, max_steps)

@@ -932,6 +932,17 @@ int sp_rb_gather(SpReplay* rb, float* states, int64_t* actions, float* rewards, 
   return SP_OK;
 }
 
+int sp_philox_fill(int64_t n, uint64_t seed, uint32_t lane, uint32_t tag, uint64_t ctr0,
+                   int kind, double lo, double hi, void* out, void* stream) {
+  if (n < 1) return SP_OK;
+  if (!out || (kind != 0 && kind != 1)) return fail(SP_EINVAL, "bad arguments");
+  if (kind == 1 && !(hi > lo)) return fail(SP_EINVAL, "integers: high <= low");
+  philox_fill_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(n, seed, lane, tag, ctr0,
+                                                                        kind, lo, hi, out);
+  SP_CUDA(cudaGetLastError());
+  return SP_OK;
+}
+
 int sp_random_actions(int64_t n, uint64_t seed, int64_t env_id0, int64_t step, int32_t n_actions,
                       int64_t* actions, void* stream) {
   if (n < 1) return SP_OK;

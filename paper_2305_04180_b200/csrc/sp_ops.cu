@@ -199,6 +199,18 @@ __global__ void random_actions_kernel(int64_t n, uint64_t seed, int64_t env_id0,
   }
 }
 
+__global__ void philox_fill_kernel(int64_t n, uint64_t seed, uint32_t lane, uint32_t tag,
+                                   uint64_t ctr0, int kind, double lo, double hi, void* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const Block4 b = stream_block(seed, lane, tag, ctr0 + (uint64_t)i);
+    if (kind == 0)
+      ((double*)out)[i] = draw_uniform(b, lo, hi);
+    else
+      ((int64_t*)out)[i] = draw_integer(b, (int64_t)lo, (int64_t)hi);
+  }
+}
+
 // Deterministic single-CTA totals {episodes, arrivals, return_sum}.
 __global__ void stats_totals_kernel(const int64_t* __restrict__ eps,
                                     const int64_t* __restrict__ arr,

@@ -1,0 +1,159 @@
+"""ASL learner side on the GPU vs the reference's
+numpy implementation (oracle/_ref): Q-net init/forward/backward/Adam, DDQN
+targets and updates, VEM epsilons and epsilon-greedy draws, TFM pacing,
+COLORNET checkpoints; plus a cfg5-shaped session on the CUDA env + replay."""
+
+import numpy as np
+import pytest
+
+from helpers import config, load_maps, ranges
+from oracle import oracle as O
+from oracle.philox_shim import PhiloxStream
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not O.reference_available(), reason="oracle/_ref not built")]
+
+SIZES = (37, 256, 128, 5)
+
+
+def ref():
+    O.import_reference(37)
+    import color_rl
+    return color_rl
+
+
+def _batch(rng, n, dim=37, torch_dev=None):
+    s = rng.standard_normal((n, dim)).astype(np.float32)
+    a = rng.integers(0, 5, n)
+    r = rng.standard_normal(n).astype(np.float32)
+    s2 = rng.standard_normal((n, dim)).astype(np.float32)
+    d = rng.random(n) < 0.1
+    return s, a, r, s2, d
+
+
+def _tb(arrs):
+    import torch
+    from paper_2305_04180_b200 import TransitionBatch
+    s, a, r, s2, d = arrs
+    return TransitionBatch(*(torch.from_numpy(np.ascontiguousarray(x)).cuda()
+                             for x in (s, a, r, s2, d)))
+
+
+def test_init_and_forward_match_reference():
+    ref()
+    from color_rl import net
+    from paper_2305_04180_b200.asl import QNet
+    p_ref = net.init_params(np.random.default_rng(7), SIZES)
+    p = QNet.init(np.random.default_rng(7), SIZES)
+    for w, wr in zip(p.weights, p_ref.weights):
+        assert np.array_equal(w.cpu().numpy(), wr)
+    x = np.random.default_rng(1).standard_normal((512, 37)).astype(np.float32)
+    import torch
+    np.testing.assert_allclose(p.forward(torch.from_numpy(x).cuda()).cpu().numpy(),
+                               net.forward(p_ref, x), rtol=1e-5, atol=1e-5)
+
+
+def test_ddqn_updates_match_reference():
+    ref()
+    from color_rl import net
+    from color_rl.ddqn import DdqnConfig as RC, DdqnLearner as RL
+    from color_rl.replay import TransitionBatch as RTB
+    from paper_2305_04180_b200.asl import DdqnConfig, DdqnLearner, QNet, compute_targets
+    from color_rl.ddqn import compute_targets as ref_targets
+    rl = RL(net.init_params(np.random.default_rng(3), SIZES), RC(target_sync_period=5))
+    gl = DdqnLearner(QNet.init(np.random.default_rng(3), SIZES), DdqnConfig(target_sync_period=5))
+    rng = np.random.default_rng(11)
+    for k in range(12):
+        arrs = _batch(rng, 256)
+        tb = _tb(arrs)
+        y_ref = ref_targets(RTB(*arrs), rl.online, rl.target, 0.98)
+        y = compute_targets(tb, gl.online, gl.target, 0.98).cpu().numpy()
+        np.testing.assert_allclose(y, y_ref, rtol=1e-4, atol=1e-5)
+        sr = rl.update(RTB(*arrs))
+        sg = gl.update(tb)
+        assert sg.version == sr.version and sg.target_synced == sr.target_synced
+        np.testing.assert_allclose(sg.loss, sr.loss, rtol=1e-4)
+        np.testing.assert_allclose(sg.mean_abs_td, sr.mean_abs_td, rtol=1e-4)
+    for w, wr in zip(gl.online.weights, rl.online.weights):
+        np.testing.assert_allclose(w.cpu().numpy(), wr, rtol=1e-4, atol=1e-6)
+    for w, wr in zip(gl.target.weights, rl.target.weights):
+        np.testing.assert_allclose(w.cpu().numpy(), wr, rtol=1e-4, atol=1e-6)
+
+
+def test_vem_epsilons_and_selection_match_reference():
+    ref()
+    from color_rl.asl.vem import VemSchedule as RV, select_actions as ref_select
+    from paper_2305_04180_b200.asl import VemSchedule, select_actions
+    import torch
+    for n, t in ((16, 0), (16, 250_000), (4096, 10), (4096, 999_999), (3, 5)):
+        kw = dict(or_init=min(16, n), or_final=min(3, n))
+        assert np.array_equal(VemSchedule(n, **kw).epsilons(t), RV(n, **kw).epsilons(t))
+    q = np.random.default_rng(2).standard_normal((4096, 5)).astype(np.float32)
+    q[:8] = 0.0  # ties -> lowest index
+    eps = RV(4096).epsilons(100)
+    want = ref_select(q, eps, PhiloxStream(5, 0xAC, tag=3))
+    g = PhiloxStream(5, 0xAC, tag=3)
+    got = select_actions(torch.from_numpy(q).cuda(), eps, g).cpu().numpy()
+    assert np.array_equal(got, want)
+    assert g.ctr == 2 * 4096
+
+
+def test_tfm_matches_reference():
+    ref()
+    from color_rl.asl import tfm as rt
+    from paper_2305_04180_b200 import asl
+    cfg, rcfg = asl.TfmConfig(4096, 256, 256, warmup_samples=3), rt.TfmConfig(4096, 256, 256, warmup_samples=3)
+    a, b = asl.TfmState(), rt.TfmState()
+    rng = np.random.default_rng(0)
+    for _ in range(20):
+        v, w = rng.uniform(1e-3, 5e-3), rng.uniform(1e-4, 1e-3)
+        a.record_interaction(v); b.record_interaction(v)
+        a.record_optimization(w); b.record_optimization(w)
+        assert a.actor_sleep(cfg) == b.actor_sleep(rcfg)
+        assert a.learner_sleep(cfg) == b.learner_sleep(rcfg)
+    assert cfg.rho == rcfg.rho == 4096
+
+
+def test_checkpoint_bytes_compatible():
+    ref()
+    from color_rl import net
+    from paper_2305_04180_b200.asl import CheckpointError, QNet
+    p_ref = net.init_params(np.random.default_rng(9), SIZES)
+    p_ref.version = 42
+    p = QNet.from_numpy(p_ref.weights, p_ref.biases, 42)
+    assert p.to_bytes() == net.to_bytes(p_ref)
+    back = QNet.from_bytes(net.to_bytes(p_ref), expect_sizes=SIZES)
+    assert back.version == 42 and back.to_bytes() == p.to_bytes()
+    with pytest.raises(CheckpointError):
+        QNet.from_bytes(b"NOTCOLOR" + p.to_bytes()[8:])
+    with pytest.raises(CheckpointError):
+        QNet.from_bytes(p.to_bytes()[:-3])
+
+
+def test_asl_session_cfg5_shape():
+    """cfg5 shape: 4096 CUDA envs -> 1M GPU replay -> batch-256 DDQN with TFM
+    pacing; runs a few seconds, both loops make progress, no failures."""
+    import time
+    from paper_2305_04180_b200 import ReplayBuffer, VecEnv
+    from paper_2305_04180_b200.asl import (DdqnConfig, DdqnLearner, QNet, Sharer, TfmConfig,
+                                           VemSchedule, start_session)
+    n = 4096
+    env = VecEnv(load_maps(16), n, ranges(0.3), config(32), check_actions=False)
+    states = env.reset_all(0)
+    algo = DdqnLearner(QNet.init(np.random.default_rng(0), SIZES), DdqnConfig())
+    sharer = Sharer(ReplayBuffer(1_000_000, 37))
+    tfm = TfmConfig(n, 256.0, 256)
+    session = start_session(sharer, env, states, algo.online, VemSchedule(n), tfm,
+                            max_steps=n * 400, algo=algo, learn_start=20_000, upload_period=50,
+                            seed=0)
+    t0 = time.time()
+    while session.running and time.time() - t0 < 6.0:
+        time.sleep(0.1)
+    session.abort()
+    session.wait(timeout=30)
+    assert sharer.t_step > 20_000
+    assert sharer.b_step > 10
+    assert len(sharer.buffer) == min(sharer.t_step, 1_000_000)
+    assert sharer.publish_count >= 1 + sharer.b_step // 50
+    snap = env.snapshot_stats()
+    assert snap.episodes > 0
