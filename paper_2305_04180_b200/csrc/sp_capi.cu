@@ -231,6 +231,11 @@ static Plan plan_launch(SpEnv* env, const std::vector<int64_t>& off, bool stagin
   const EnvDev& d = env->d;
   const int D = staging ? d.D : 0;  // the scan kernel stages nothing
   Plan p;
+#ifdef SP_SCAN_THREADS
+  const int max_threads = staging ? kMaxWarps * 32 : SP_SCAN_THREADS;
+#else
+  const int max_threads = kMaxWarps * 32;
+#endif
   const int64_t lanes = off.back() - off.front();
   const size_t fixed = align_up((size_t)d.R * 16, 128) + 128;
   // per-CTA budget: SP_CTAS_PER_SM CTAs share the SM's shared memory (plus
@@ -239,7 +244,7 @@ static Plan plan_launch(SpEnv* env, const std::vector<int64_t>& off, bool stagin
   const size_t budget = std::min((size_t)env->smem_optin,
                                  sm_total / SP_CTAS_PER_SM) - 1024;
   size_t map_bytes = align_up(d.map_bytes, 128);
-  p.threads = kMaxWarps * 32;
+  p.threads = max_threads;
   if (map_bytes + fixed + chunk_bytes(128, D, d.R) + 128 > budget) {
     p.smem_maps = 0;  // map does not fit next to a useful chunk: read tables via L1/L2
     map_bytes = 0;

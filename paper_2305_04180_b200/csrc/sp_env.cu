@@ -823,8 +823,11 @@ struct FinScan {
   }
 };
 
+#ifndef SP_SCAN_THREADS
+#define SP_SCAN_THREADS SP_CTA_THREADS
+#endif
 template <bool kSmem, bool kBordered>
-__global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
+__global__ void __launch_bounds__(SP_SCAN_THREADS, SP_CTAS_PER_SM)
     env_scan_kernel(const __grid_constant__ EnvDev d, const __grid_constant__ ScanArgs q) {
   extern __shared__ __align__(128) uint8_t smem[];
   double2* beam = (double2*)(smem + d.off_beam);
