@@ -27,6 +27,7 @@
  *   sp_rb_gather        replay.py:81-87 (snapshot: rows in storage order)
  *   sp_random_actions   bench.py:97-105 (random policy actions), on device
  *   sp_philox_fill      asl/vem.py:57-66 draws (rng.random / rng.integers), on device
+ *   sp_adam_step        net.py:141-161 adam_step, fused over all tensors, on device
  */
 #ifndef SPARROW_H_
 #define SPARROW_H_
@@ -172,6 +173,19 @@ int sp_philox_fill(int64_t n, uint64_t seed, uint32_t lane, uint32_t tag, uint64
 /* actions[i] = integers(0, n_actions) from block `step` of (seed, env_id0 + i, tag 1) */
 int sp_random_actions(int64_t n, uint64_t seed, int64_t env_id0, int64_t step, int32_t n_actions,
                       int64_t* actions, void* stream);
+
+/* ---- learner side ------------------------------------- */
+#define SP_ADAM_MAX 16
+/* Bias-corrected Adam over n_tensors fp32 device tensors in one launch; replaces
+ * net.py:141-161 (_adam_update / adam_step), same op order and fp32 roundings.
+ * params/grads/m/v: host arrays of device pointers; numels: host array.
+ * t = step_dev ? *step_dev + 1 (then *step_dev += 1 on device) : step_host.
+ * gate (nullable device scalar, e.g. the loss): the step applies only if it is
+ * finite, so a diverged update leaves every tensor untouched (ddqn.py:66-71). */
+int sp_adam_step(int n_tensors, float* const* params, const float* const* grads, float* const* m,
+                 float* const* v, const int64_t* numels, double* step_dev, int64_t step_host,
+                 const float* gate, double lr, double beta1, double beta2, double eps,
+                 void* stream);
 
 #ifdef __cplusplus
 }

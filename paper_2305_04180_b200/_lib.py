@@ -108,6 +108,9 @@ SIGNATURES = [
                                       ctypes.c_double, ctypes.c_double, c_vp, c_vp]),
     ("sp_random_actions", ctypes.c_int, [ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64,
                                          ctypes.c_int64, ctypes.c_int32, c_vp, c_vp]),
+    ("sp_adam_step", ctypes.c_int, [ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_i64p, c_vp,
+                                    ctypes.c_int64, c_vp, ctypes.c_double, ctypes.c_double,
+                                    ctypes.c_double, ctypes.c_double, c_vp]),
 ]
 
 _lib = None

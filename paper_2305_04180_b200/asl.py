@@ -218,21 +218,34 @@ class AdamState:  # net.py:118-139
                    m_biases=[z(b) for b in net.biases], v_biases=[z(b) for b in net.biases])
 
 
-def _adam_update(p, g, m, v, st: AdamState, t: int) -> None:  # net.py:141-148
+def _adam_launch(net: QNet, gw, gb, st: AdamState, step_dev=None, step_host: int = 0,
+                 gate=None) -> None:
+    """One ``sp_adam_step`` launch over every weight and bias tensor
+    (net.py:141-161 ``_adam_update`` per tensor, fused)."""
     torch = _torch()
-    m.mul_(st.beta1).add_((1.0 - st.beta1) * g)
-    v.mul_(st.beta2).add_((1.0 - st.beta2) * torch.square(g))
-    m_hat = m / (1.0 - st.beta1 ** t)
-    v_hat = v / (1.0 - st.beta2 ** t)
-    p.sub_(st.lr * m_hat / (torch.sqrt(v_hat) + st.eps))
+    ps = list(net.weights) + list(net.biases)
+    gs = [g.contiguous() for g in list(gw) + list(gb)]
+    ms = list(st.m_weights) + list(st.m_biases)
+    vs = list(st.v_weights) + list(st.v_biases)
+    for t in ps + ms + vs:
+        if not t.is_contiguous() or t.dtype != torch.float32:
+            raise ValueError("adam: parameters and moments must be contiguous float32")
+    n = len(ps)
+    arr = ctypes.c_void_p * n
+    numels = (ctypes.c_int64 * n)(*[t.numel() for t in ps])
+    lib = _lib.load()
+    dev = ps[0].device
+    _lib.check(lib.sp_adam_step(
+        n, arr(*[t.data_ptr() for t in ps]), arr(*[t.data_ptr() for t in gs]),
+        arr(*[t.data_ptr() for t in ms]), arr(*[t.data_ptr() for t in vs]), numels,
+        None if step_dev is None else step_dev.data_ptr(), int(step_host),
+        None if gate is None else gate.data_ptr(), float(st.lr), float(st.beta1),
+        float(st.beta2), float(st.eps), _lib.stream_ptr(dev)), "adam_step")
 
 
 def adam_step(net: QNet, gw, gb, st: AdamState) -> QNet:  # net.py:151-161
     st.step += 1
-    t = st.step
-    for li in range(len(net.weights)):
-        _adam_update(net.weights[li], gw[li], st.m_weights[li], st.v_weights[li], st, t)
-        _adam_update(net.biases[li], gb[li], st.m_biases[li], st.v_biases[li], st, t)
+    _adam_launch(net, gw, gb, st, step_host=st.step)
     net.version += 1
     return net
 
@@ -271,18 +284,122 @@ def compute_targets(batch, online: QNet, target: QNet, gamma: float):
     return batch.rewards.to(q_target.dtype) + gamma * not_done * bootstrap
 
 
-class DdqnLearner:
-    """Online/target pair and one update per batch (ddqn.py:54-77)."""
+class _GraphedUpdate:
+    """One DDQN update captured as a CUDA graph: the targets, the backward and
+    Adam (about 90 small kernels, launch-bound when eager) replay as one
+    ``cudaGraphLaunch``.
 
-    def __init__(self, params: QNet, config: DdqnConfig | None = None, check_finite: bool = True):
+    The batch lives in static tensors that the replay sampler fills in place
+    (``ReplayBuffer.sample(out=...)``). The Adam step count is a device scalar,
+    so the bias corrections need no host constants. The fused Adam kernel
+    (``sp_adam_step``) is gated on ``isfinite(loss)``: a diverged update
+    leaves the parameters and moments untouched, exactly as the reference
+    raises before stepping (``ddqn.py:66-71``). The graph holds the tensor addresses of ``online``, ``target`` and
+    the moments, so those tensors are only ever updated in place."""
+
+    def __init__(self, learner: "DdqnLearner", batch_size: int, state_dim: int):
+        from paper_2305_04180_b200.replay import TransitionBatch
+        torch = _torch()
+        self.learner = learner
+        on = learner.online
+        dev = on.weights[0].device
+        b, d = int(batch_size), int(state_dim)
+        self.batch_size, self.state_dim = b, d
+        self.batch = TransitionBatch(torch.zeros((b, d), dtype=torch.float32, device=dev),
+                                     torch.zeros(b, dtype=torch.int64, device=dev),
+                                     torch.zeros(b, dtype=torch.float32, device=dev),
+                                     torch.zeros((b, d), dtype=torch.float32, device=dev),
+                                     torch.zeros(b, dtype=torch.bool, device=dev))
+        self.t = torch.full((), float(learner.adam.step), dtype=torch.float64, device=dev)
+        self.loss = torch.zeros((), dtype=torch.float32, device=dev)
+        self.mad = torch.zeros((), dtype=torch.float32, device=dev)
+        ad = learner.adam
+        state = on.weights + on.biases + ad.m_weights + ad.v_weights + ad.m_biases + ad.v_biases
+        saved = [x.clone() for x in state]
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):  # warm-up: cuBLAS handles/workspaces, allocator
+            for _ in range(2):
+                self._body()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        for x, y in zip(state, saved):
+            x.copy_(y)
+        self.t.fill_(float(ad.step))
+        self.graph = torch.cuda.CUDAGraph()
+        # thread_local: the actor thread keeps syncing its own stream meanwhile
+        with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
+            self._body()
+
+    def _body(self) -> None:
+        torch = _torch()
+        lr = self.learner
+        on, ad = lr.online, lr.adam
+        bt = self.batch
+        targets = compute_targets(bt, on, lr.target, lr.config.gamma)
+        gw, gb, loss, mad = backward(on, bt.states, bt.actions, targets)
+        self.loss.copy_(loss)
+        self.mad.copy_(mad)
+        # gated on isfinite(loss); advances the device step count itself
+        _adam_launch(on, gw, gb, ad, step_dev=self.t, gate=self.loss)
+
+    def run(self, batch) -> None:
+        if batch is not self.batch:
+            for dst, src in zip(self.batch, batch):
+                dst.copy_(src.reshape(dst.shape), non_blocking=True)
+        self.graph.replay()
+
+
+class DdqnLearner:
+    """Online/target pair and one update per batch (ddqn.py:54-77).
+
+    ``graph=True`` replays each update as one CUDA graph (``_GraphedUpdate``);
+    numerics are unchanged. ``graph_batch(B, D)`` returns the static batch a
+    sampler should fill to skip the copy-in."""
+
+    def __init__(self, params: QNet, config: DdqnConfig | None = None, check_finite: bool = True,
+                 graph: bool = False):
         self.config = config or DdqnConfig()
         self.online = params
         self.target = params.copy()
         self.adam = AdamState.for_params(params, lr=self.config.lr)
         self.update_count = 0
         self.check_finite = check_finite
+        self.graph = bool(graph)
+        self._graphed = None
+
+    def graph_batch(self, batch_size: int, state_dim: int):
+        if not self.graph:
+            return None
+        g = self._graphed
+        if g is None or g.batch_size != batch_size or g.state_dim != state_dim:
+            g = self._graphed = _GraphedUpdate(self, batch_size, state_dim)
+        return g.batch
+
+    def _update_graphed(self, batch) -> UpdateStats:
+        b, d = int(batch.states.shape[0]), int(batch.states.shape[1])
+        self.graph_batch(b, d)
+        g = self._graphed
+        g.run(batch)
+        if self.check_finite:
+            loss_v = float(g.loss)
+            if not math.isfinite(loss_v):
+                raise TrainingDiverged(f"non-finite loss {loss_v!r} at update "
+                                       f"{self.update_count + 1} (parameter version "
+                                       f"{self.online.version})")
+            mad_v = float(g.mad)
+        else:
+            loss_v = mad_v = float("nan")
+        self.adam.step += 1
+        self.online.version += 1
+        self.update_count += 1
+        synced = self.update_count % self.config.target_sync_period == 0
+        if synced:
+            self.target.copy_from(self.online)
+        return UpdateStats(loss_v, mad_v, self.online.version, synced)
 
     def update(self, batch) -> UpdateStats:
+        if self.graph:
+            return self._update_graphed(batch)
         targets = compute_targets(batch, self.online, self.target, self.config.gamma)
         gw, gb, loss, mad = backward(self.online, batch.states, batch.actions, targets)
         loss_v = float(loss) if self.check_finite else float("nan")
@@ -533,7 +650,9 @@ def learner_loop(sharer: Sharer, algo: DdqnLearner, tfm_cfg: TfmConfig, learn_st
                 continue
             started = time.perf_counter()
             try:
-                batch = sharer.buffer.sample(batch_size, rng)
+                batch = sharer.buffer.sample(batch_size, rng,
+                                             out=algo.graph_batch(batch_size,
+                                                                  sharer.buffer.state_dim))
             except BufferNotReady:
                 time.sleep(_IDLE_POLL_S)
                 continue
@@ -581,6 +700,7 @@ def start_session(sharer: Sharer, vec_env, initial_states, params: QNet, vem: Ve
     """Publish the initial model and start the actor and learner threads
     (loops.py:130-149); their streams are (seed, 0xAC) / (seed, 0x1E)."""
     sharer.publish_params(params)
+    algo.graph_batch(tfm_cfg.batch_size, sharer.buffer.state_dim)  # capture before threads run
     actor_rng = PhiloxGenerator(seed, 0xAC)
     actor_rng.tag = 3
     learner_rng = PhiloxGenerator(seed, 0x1E)

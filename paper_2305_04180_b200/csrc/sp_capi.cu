@@ -958,4 +958,35 @@ int sp_random_actions(int64_t n, uint64_t seed, int64_t env_id0, int64_t step, i
   return SP_OK;
 }
 
+int sp_adam_step(int n_tensors, float* const* params, const float* const* grads, float* const* m,
+                 float* const* v, const int64_t* numels, double* step_dev, int64_t step_host,
+                 const float* gate, double lr, double beta1, double beta2, double eps,
+                 void* stream) {
+  if (n_tensors < 1 || n_tensors > SP_ADAM_MAX || !params || !grads || !m || !v || !numels)
+    return fail(SP_EINVAL, "adam: bad tensor list");
+  if (!step_dev && step_host < 1) return fail(SP_EINVAL, "adam: step must be >= 1");
+  AdamTensors T;
+  int64_t acc = 0;
+  for (int k = 0; k < n_tensors; ++k) {
+    if (numels[k] < 1 || !params[k] || !grads[k] || !m[k] || !v[k])
+      return fail(SP_EINVAL, "adam: empty or null tensor");
+    T.p[k] = params[k];
+    T.g[k] = grads[k];
+    T.m[k] = m[k];
+    T.v[k] = v[k];
+    acc += numels[k];
+    T.end[k] = acc;
+  }
+  T.n = n_tensors;
+  cudaStream_t s = (cudaStream_t)stream;
+  adam_kernel<<<grid_for(acc, 256), 256, 0, s>>>(T, step_dev, step_host, gate, lr, beta1, beta2,
+                                                  eps);
+  SP_CUDA(cudaGetLastError());
+  if (step_dev) {
+    adam_tick_kernel<<<1, 1, 0, s>>>(step_dev, gate);
+    SP_CUDA(cudaGetLastError());
+  }
+  return SP_OK;
+}
+
 }  // extern "C"

@@ -242,4 +242,51 @@ __global__ void stats_totals_kernel(const int64_t* __restrict__ eps,
   }
 }
 
+// Bias-corrected Adam over up to SP_ADAM_MAX tensors in one launch
+// (net.py:141-161), with the reference's operation order and fp32 roundings:
+//   m = m*b1 + (1-b1)*g;  v = v*b2 + (1-b2)*g^2;
+//   p -= (lr * (m / c1)) / (sqrt(v / c2) + eps),  c_k = f32(1 - beta_k^t) in f64.
+// Python-double scalars are rounded to f32 as numpy's weak-scalar rule does.
+// gate (nullable): apply only if *gate is finite (ddqn.py:66-71 abort leaves
+// the state untouched). t = step_dev ? *step_dev + 1 : step_host.
+struct AdamTensors {
+  float* p[SP_ADAM_MAX];
+  const float* g[SP_ADAM_MAX];
+  float* m[SP_ADAM_MAX];
+  float* v[SP_ADAM_MAX];
+  int64_t end[SP_ADAM_MAX];  // inclusive prefix sums of numels
+  int n;
+};
+
+__global__ void adam_kernel(const __grid_constant__ AdamTensors T, const double* step_dev,
+                            int64_t step_host, const float* gate, double lr, double b1,
+                            double b2, double eps) {
+  if (gate && !isfinite(*gate)) return;
+  const double t = step_dev ? *step_dev + 1.0 : (double)step_host;
+  const float c1 = (float)(1.0 - pow(b1, t));
+  const float c2 = (float)(1.0 - pow(b2, t));
+  const float fb1 = (float)b1, fb2 = (float)b2, f1b1 = (float)(1.0 - b1),
+              f1b2 = (float)(1.0 - b2), flr = (float)lr, feps = (float)eps;
+  const int64_t total = T.end[T.n - 1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int k = 0;
+    while (i >= T.end[k]) ++k;
+    const int64_t j = i - (k ? T.end[k - 1] : 0);
+    const float g = T.g[k][j];
+    const float m = __fadd_rn(__fmul_rn(T.m[k][j], fb1), __fmul_rn(f1b1, g));
+    const float v = __fadd_rn(__fmul_rn(T.v[k][j], fb2), __fmul_rn(f1b2, __fmul_rn(g, g)));
+    T.m[k][j] = m;
+    T.v[k][j] = v;
+    const float m_hat = __fdiv_rn(m, c1);
+    const float v_hat = __fdiv_rn(v, c2);
+    const float upd = __fdiv_rn(__fmul_rn(flr, m_hat), __fadd_rn(__fsqrt_rn(v_hat), feps));
+    T.p[k][j] = __fsub_rn(T.p[k][j], upd);
+  }
+}
+
+__global__ void adam_tick_kernel(double* step_dev, const float* gate) {
+  if (!gate || isfinite(*gate)) *step_dev += 1.0;
+}
+
 }  // namespace sp

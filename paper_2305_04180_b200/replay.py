@@ -75,6 +75,16 @@ def _stream_of(rng) -> tuple:
     raise TypeError(f"unsupported rng {type(rng).__name__}")
 
 
+def _check_out(out: TransitionBatch, b: int, dim: int, dev, torch) -> None:
+    want = (((b, dim), torch.float32), ((b,), torch.int64), ((b,), torch.float32),
+            ((b, dim), torch.float32), ((b,), torch.bool))
+    for t, (shape, dtype) in zip(out, want):
+        if (tuple(t.shape) != shape or t.dtype != dtype or t.device != dev
+                or not t.is_contiguous()):
+            raise ValueError(f"out batch tensor {tuple(t.shape)} {t.dtype} on {t.device}: "
+                             f"need contiguous {shape} {dtype} on {dev}")
+
+
 class ReplayBuffer:
     def __init__(self, capacity: int = 1_000_000, state_dim: int = 32, device=None):
         if capacity < 1:
@@ -152,16 +162,22 @@ class ReplayBuffer:
 
     add = append_batch  # the paper's Sharer.buffer.add
 
-    def sample(self, batch_size: int, rng, return_indices: bool = False):
-        """Uniform with replacement over the filled slots; returns fresh tensors."""
+    def sample(self, batch_size: int, rng, return_indices: bool = False,
+               out: TransitionBatch | None = None):
+        """Uniform with replacement over the filled slots. Returns fresh tensors,
+        or fills ``out`` (contiguous device tensors of the batch shape, e.g. a
+        CUDA-graphed learner's static batch) in place."""
         torch = self._torch
         g = _stream_of(rng)
         b, dim, dev = int(batch_size), self.state_dim, self.device
-        out = TransitionBatch(torch.empty((b, dim), dtype=torch.float32, device=dev),
-                              torch.empty(b, dtype=torch.int64, device=dev),
-                              torch.empty(b, dtype=torch.float32, device=dev),
-                              torch.empty((b, dim), dtype=torch.float32, device=dev),
-                              torch.empty(b, dtype=torch.bool, device=dev))
+        if out is not None:
+            _check_out(out, b, dim, dev, torch)
+        else:
+            out = TransitionBatch(torch.empty((b, dim), dtype=torch.float32, device=dev),
+                                  torch.empty(b, dtype=torch.int64, device=dev),
+                                  torch.empty(b, dtype=torch.float32, device=dev),
+                                  torch.empty((b, dim), dtype=torch.float32, device=dev),
+                                  torch.empty(b, dtype=torch.bool, device=dev))
         idx = torch.empty(b, dtype=torch.int64, device=dev)
         with self._lock:
             self._order_after(self._last_append)

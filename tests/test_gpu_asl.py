@@ -53,7 +53,8 @@ def test_init_and_forward_match_reference():
                                net.forward(p_ref, x), rtol=1e-5, atol=1e-5)
 
 
-def test_ddqn_updates_match_reference():
+@pytest.mark.parametrize("graph", [False, True])
+def test_ddqn_updates_match_reference(graph):
     ref()
     from color_rl import net
     from color_rl.ddqn import DdqnConfig as RC, DdqnLearner as RL
@@ -61,7 +62,8 @@ def test_ddqn_updates_match_reference():
     from paper_2305_04180_b200.asl import DdqnConfig, DdqnLearner, QNet, compute_targets
     from color_rl.ddqn import compute_targets as ref_targets
     rl = RL(net.init_params(np.random.default_rng(3), SIZES), RC(target_sync_period=5))
-    gl = DdqnLearner(QNet.init(np.random.default_rng(3), SIZES), DdqnConfig(target_sync_period=5))
+    gl = DdqnLearner(QNet.init(np.random.default_rng(3), SIZES), DdqnConfig(target_sync_period=5),
+                     graph=graph)
     rng = np.random.default_rng(11)
     for k in range(12):
         arrs = _batch(rng, 256)
@@ -78,6 +80,83 @@ def test_ddqn_updates_match_reference():
         np.testing.assert_allclose(w.cpu().numpy(), wr, rtol=1e-4, atol=1e-6)
     for w, wr in zip(gl.target.weights, rl.target.weights):
         np.testing.assert_allclose(w.cpu().numpy(), wr, rtol=1e-4, atol=1e-6)
+
+
+def test_fused_adam_bit_exact_vs_reference():
+    """sp_adam_step over all six tensors == net.py:151-161 adam_step (numpy
+    fp32, weak Python-float scalars) bit for bit, over several steps."""
+    ref()
+    from color_rl import net
+    from paper_2305_04180_b200.asl import AdamState, QNet, adam_step
+    import torch
+    p_ref = net.init_params(np.random.default_rng(12), SIZES)
+    st_ref = net.AdamState.for_params(p_ref, lr=3e-4)
+    p = QNet.from_numpy(p_ref.weights, p_ref.biases)
+    st = AdamState.for_params(p, lr=3e-4)
+    rng = np.random.default_rng(13)
+    for _ in range(7):
+        gw = [rng.standard_normal(w.shape).astype(np.float32) * 1e-2 for w in p_ref.weights]
+        gb = [rng.standard_normal(b.shape).astype(np.float32) * 1e-2 for b in p_ref.biases]
+        net.adam_step(p_ref, net.Gradients(gw, gb), st_ref)
+        adam_step(p, [torch.from_numpy(g).cuda() for g in gw],
+                  [torch.from_numpy(g).cuda() for g in gb], st)
+    assert p.version == p_ref.version == 7
+    for a, b in zip(p.weights + p.biases + st.m_weights + st.v_weights,
+                    p_ref.weights + p_ref.biases + st_ref.m_weights + st_ref.v_weights):
+        assert np.array_equal(a.cpu().numpy(), b)
+
+
+def test_graphed_update_nonfinite_aborts_and_keeps_params():
+    """ddqn.py:66-71 / test_ddqn.py:113-119: a non-finite loss raises
+    TrainingDiverged; the gated graph leaves parameters, moments and the
+    Adam step count untouched, and the next finite update proceeds."""
+    from paper_2305_04180_b200.asl import DdqnLearner, QNet, TrainingDiverged
+    import torch
+    gl = DdqnLearner(QNet.init(np.random.default_rng(4), SIZES), graph=True)
+    rng = np.random.default_rng(5)
+    gl.update(_tb(_batch(rng, 64)))
+    before = [w.clone() for w in gl.online.weights + gl.adam.m_weights]
+    bad = _batch(rng, 64)
+    bad[0][3, 7] = np.inf
+    with pytest.raises(TrainingDiverged):
+        gl.update(_tb(bad))
+    for x, y in zip(gl.online.weights + gl.adam.m_weights, before):
+        assert torch.equal(x, y)
+    assert gl.adam.step == 1 and gl.online.version == 1
+    eager = DdqnLearner(QNet.init(np.random.default_rng(4), SIZES))
+    rng = np.random.default_rng(5)
+    eager.update(_tb(_batch(rng, 64)))
+    _batch(rng, 64)
+    nxt = _batch(rng, 64)
+    s1, s2 = gl.update(_tb(nxt)), eager.update(_tb(nxt))
+    assert s1.version == s2.version == 2
+    np.testing.assert_allclose(s1.loss, s2.loss, rtol=1e-5)
+    for w, we in zip(gl.online.weights, eager.online.weights):
+        np.testing.assert_allclose(w.cpu().numpy(), we.cpu().numpy(), rtol=1e-5, atol=1e-7)
+
+
+def test_graphed_update_samples_into_static_batch():
+    """ReplayBuffer.sample(out=learner.graph_batch(...)) fills the graph's
+    static batch in place; the update equals the eager one on the same rows."""
+    from paper_2305_04180_b200 import PhiloxGenerator, ReplayBuffer
+    from paper_2305_04180_b200.asl import DdqnLearner, QNet
+    import torch
+    buf = ReplayBuffer(4096, 37)
+    s, a, r, s2, d = _tb(_batch(np.random.default_rng(6), 3000))
+    buf.append_batch(s, a, r, s2, d)
+    gl = DdqnLearner(QNet.init(np.random.default_rng(8), SIZES), graph=True)
+    el = DdqnLearner(QNet.init(np.random.default_rng(8), SIZES))
+    for k in range(6):
+        out = gl.graph_batch(256, 37)
+        got = buf.sample(256, PhiloxGenerator(9, 0, ctr=256 * k), out=out)
+        assert got is out
+        want = buf.sample(256, PhiloxGenerator(9, 0, ctr=256 * k))
+        for x, y in zip(out, want):
+            assert torch.equal(x, y)
+        sg, se = gl.update(out), el.update(want)
+        np.testing.assert_allclose(sg.loss, se.loss, rtol=1e-5)
+    with pytest.raises(ValueError):
+        buf.sample(128, PhiloxGenerator(9), out=gl.graph_batch(256, 37))
 
 
 def test_vem_epsilons_and_selection_match_reference():
@@ -140,7 +219,7 @@ def test_asl_session_cfg5_shape():
     n = 4096
     env = VecEnv(load_maps(16), n, ranges(0.3), config(32), check_actions=False)
     states = env.reset_all(0)
-    algo = DdqnLearner(QNet.init(np.random.default_rng(0), SIZES), DdqnConfig())
+    algo = DdqnLearner(QNet.init(np.random.default_rng(0), SIZES), DdqnConfig(), graph=True)
     sharer = Sharer(ReplayBuffer(1_000_000, 37))
     tfm = TfmConfig(n, 256.0, 256)
     session = start_session(sharer, env, states, algo.online, VemSchedule(n), tfm,

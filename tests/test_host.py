@@ -124,3 +124,23 @@ def test_shard_partitions_global_ids():
         assert ids == list(range(total))
     with pytest.raises(ValueError):
         dist.shard(10, 3, 3)
+
+
+def test_eval_report_matches_reference_formatting():
+    """EvalReport/MapEval/summarize_rates host logic (evaluate.py:22-133):
+    same dicts and rendered table as the reference for the same counts."""
+    from oracle import oracle as O
+    from paper_2305_04180_b200 import evaluate as E
+    rows = [("a", 10, 7, 2, 1, 3.25, 41.5), ("bb", 4, 0, 4, 0, -10.0, 12.0)]
+    got = E.EvalReport(seed=3, results=[E.MapEval(*r) for r in rows])
+    assert got.episodes == 14 and got.arrival_rate == 0.5
+    assert got.to_dict()["maps"][1]["arrival_rate"] == 0.0
+    assert E.summarize_rates([]) == {"per_seed": [], "mean": 0.0, "std": 0.0}
+    if not O.reference_available():
+        return
+    O.import_reference()
+    from color_rl import evaluate as R
+    want = R.EvalReport(seed=3, results=[R.MapEval(*r) for r in rows])
+    assert got.to_dict() == want.to_dict()
+    assert got.render() == want.render()
+    assert E.summarize_rates([got, got]) == R.summarize_rates([want, want])
