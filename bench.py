@@ -275,20 +275,17 @@ def run_ours(args, rank, world, local_rank):
     # ---- e2e through the public API with host buffers -----------------------
     Ke = max(3, min(K, args.e2e_steps))
     h_act = [torch.from_numpy(acts[W + k % K].cpu().numpy()).pin_memory() for k in range(Ke)]
-    h_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in out]
-    d_act = torch.empty(n, dtype=torch.int64, device=dev)
+    hb = env.host_buffers()
     e_starts = [torch.cuda.Event(enable_timing=True) for _ in range(Ke)]
     e_stops = [torch.cuda.Event(enable_timing=True) for _ in range(Ke)]
     for k in range(Ke):
         flush.fill_(k & 0xFF)
+        hb.actions.copy_(h_act[k])  # the step's inputs, already in pinned host memory
         e_starts[k].record(stream)
-        d_act.copy_(h_act[k], non_blocking=True)
-        env.step_device(d_act.data_ptr(), out)
-        for h, d in zip(h_out, out):
-            h.copy_(d, non_blocking=True)
+        res = env.step_host(hb.actions, hb)  # H2D actions, step, D2H of every field, sync
         e_stops[k].record(stream)
         e_stops[k].synchronize()
-        _ = float(h_out[1][0])  # the step's result read on the host
+        _ = float(res.rewards[0])  # the step's result read on the host
     e2e_t = sum(s.elapsed_time(e) for s, e in zip(e_starts, e_stops)) / 1e3
     et = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
     if dist.is_initialized():
@@ -319,7 +316,7 @@ def run_ours(args, rank, world, local_rank):
                        "launch": info},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": Ke,
-                    "path": "VecEnv step with pinned host actions in, every StepBatch field out"},
+                    "path": "VecEnv.step_host: pinned host actions in, every StepBatch field out as numpy"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_unit": "bytes per launch (dram read+write)",

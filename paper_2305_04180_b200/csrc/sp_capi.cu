@@ -251,6 +251,7 @@ static Plan plan_launch(SpEnv* env, const std::vector<int64_t>& off, bool stagin
   }
   const size_t room = budget - fixed - map_bytes - 128;
   int cap = p.threads;
+  if (const char* mc = getenv("SPARROW_MAX_CHUNK")) cap = std::max(16, std::min(cap, atoi(mc)));
   while (cap > 1 && chunk_bytes(cap, D, d.R) > room) cap -= 16;
   p.chunk_cap = std::max(1, cap);
   p.slot_cap = p.chunk_cap + extra_slots(p.chunk_cap);

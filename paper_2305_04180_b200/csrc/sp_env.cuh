@@ -8,7 +8,9 @@
 #ifndef SP_CTAS_PER_SM
 #define SP_CTAS_PER_SM 1
 #endif
+#ifndef SP_CTA_THREADS
 #define SP_CTA_THREADS (768 / SP_CTAS_PER_SM)
+#endif
 
 namespace sp {
 

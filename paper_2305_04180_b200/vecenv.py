@@ -44,6 +44,16 @@ class StepBatch(NamedTuple):  # vecenv.py:24-30
     events: "torch.Tensor"        # (N,) int8 Event codes
 
 
+class HostStep(NamedTuple):
+    """Buffers of ``VecEnv.step_host``: page-locked host side + device twins."""
+    actions: "torch.Tensor"    # (N,) int64, pinned
+    out: StepBatch             # pinned host tensors, StepBatch dtypes
+    d_actions: "torch.Tensor"  # device staging
+    d_out: StepBatch
+    h_flat: "torch.Tensor"     # the storage behind ``out`` / ``d_out``
+    d_flat: "torch.Tensor"
+
+
 @dataclass
 class CopyStats:  # vecenv.py:33-41
     episodes: int = 0
@@ -317,6 +327,65 @@ class VecEnv:
                                    out.events.data_ptr(), self._stream())
         _lib.check(rc, "step")
         return out
+
+    def host_buffers(self) -> "HostStep":
+        """Page-locked host buffers (and their device twins) for ``step_host``.
+        Every output field is a view into one flat buffer per side, so the
+        results come back in a single D2H copy."""
+        torch = self._torch
+        n, d = self.n_copies, self.state_dim
+        fields = ((n, torch.float64, 8), ((n, d), torch.float32, 4), ((n, d), torch.float32, 4),
+                  (n, torch.bool, 1), (n, torch.bool, 1), (n, torch.int8, 1))
+        total = sum(int(np.prod(sh)) * sz for sh, _, sz in fields)
+
+        def views(flat):
+            out, off = [], 0
+            for sh, dt, sz in fields:
+                nb = int(np.prod(sh)) * sz
+                out.append(flat[off:off + nb].view(dt).view(sh))
+                off += nb
+            r, st, ss, dn, tr, ev = out
+            return StepBatch(st, r, dn, tr, ss, ev)
+        h_flat = torch.empty(total, dtype=torch.uint8).pin_memory()
+        d_flat = torch.empty(total, dtype=torch.uint8, device=self.device)
+        return HostStep(torch.empty(n, dtype=torch.int64).pin_memory(), views(h_flat),
+                        torch.empty(n, dtype=torch.int64, device=self.device), views(d_flat),
+                        h_flat, d_flat)
+
+    def step_host(self, actions, bufs: "HostStep | None" = None) -> StepBatch:
+        """The reference's numpy ``step_batch`` (vecenv.py:94-116): host actions
+        in, a StepBatch of numpy arrays out. One H2D copy of the actions, the
+        fused step, and one D2H copy per field from/to page-locked buffers, all
+        on the current stream; returns once it has synchronized. The arrays are
+        views of ``bufs`` (default: buffers owned by this env), so the next call
+        overwrites them. ``actions`` may already be ``bufs.actions``."""
+        if not self._seeded:
+            raise EpisodeTerminated("reset_all(seed) must be called before stepping")
+        torch = self._torch
+        if bufs is None:
+            if getattr(self, "_host_bufs", None) is None:
+                self._host_bufs = self.host_buffers()
+            bufs = self._host_bufs
+        if not (isinstance(actions, torch.Tensor) and actions.data_ptr() == bufs.actions.data_ptr()):
+            a = np.asarray(actions.cpu() if isinstance(actions, torch.Tensor) else actions)
+            if a.shape != (self.n_copies,):
+                raise ValueError(f"expected {self.n_copies} actions, got shape {a.shape}")
+            np.copyto(bufs.actions.numpy(), a, casting="same_kind")
+        if self.check_actions:
+            av = bufs.actions.numpy()
+            if av.min() < 0 or av.max() >= self.n_actions:  # core.py:169-170
+                raise ValueError("action index out of range")
+        if not self.auto_reset:
+            flag = ctypes.c_int32(0)
+            _lib.check(self._lib.sp_env_any_needs_reset(self._h, self._stream(),
+                                                        ctypes.byref(flag)), "step")
+            if flag.value:
+                raise EpisodeTerminated("some lanes finished their episode; reset before stepping")
+        bufs.d_actions.copy_(bufs.actions, non_blocking=True)
+        self.step_device(bufs.d_actions.data_ptr(), bufs.d_out)
+        bufs.h_flat.copy_(bufs.d_flat, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return StepBatch(*(t.numpy() for t in bufs.out))
 
     def step_device(self, actions_ptr: int, out: StepBatch) -> None:
         """Raw launch on pre-validated device actions (benchmarks, CUDA graphs)."""

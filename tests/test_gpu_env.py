@@ -390,3 +390,24 @@ def test_many_resets_in_one_step_use_the_overflow_pass():
         assert np.array_equal(g.events.cpu().numpy(), c.events)
         assert_close(g.states.cpu().numpy(), c.states, atol=ATOL_OBS, what=f"states {t}")
         assert_close(g.store_states.cpu().numpy(), c.store_states, atol=ATOL_OBS, what="store")
+
+
+def test_step_host_matches_device_step():
+    """VecEnv.step_host (numpy in, numpy StepBatch out through page-locked
+    buffers) gives the same StepBatch as the device path."""
+    from paper_2305_04180_b200 import VecEnv
+    maps = load_maps(4)
+    n = 1000
+    a_env = VecEnv(maps, n, ranges(0.3), config(32))
+    b_env = VecEnv(maps, n, ranges(0.3), config(32))
+    a_env.reset_all(3)
+    b_env.reset_all(3)
+    for t in range(60):
+        acts = random_actions(3, np.arange(n), t)
+        x = a_env.step_batch(acts)
+        y = b_env.step_host(acts)
+        assert isinstance(y.states, np.ndarray) and y.states.dtype == np.float32
+        for f in ("states", "store_states", "rewards", "dones", "truncated", "events"):
+            assert np.array_equal(getattr(x, f).cpu().numpy(), getattr(y, f)), (t, f)
+    with pytest.raises(ValueError):
+        b_env.step_host(np.full(n, 7))

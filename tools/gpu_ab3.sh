@@ -1,0 +1,15 @@
+# A/B of launch-shape variants: scan kernel (cfg4, R=32/256) and full step (bench.py)
+for lib in default variants/lib_t896.so variants/lib_t640.so; do
+  if [ "$lib" = default ]; then unset SPARROW_LIB_PATH; else export SPARROW_LIB_PATH=$PWD/$lib; fi
+  n=$(basename $lib)
+  for b in 32 256; do timeout 120 python tools/bench_scan.py --beams $b > gpurun_out/ab3_${n}_$b.json 2>&1; done
+  timeout 300 python bench.py --steps 50 --warmup 5 --no-cpu-baseline > gpurun_out/ab3_${n}_bench.json 2>/dev/null
+done
+python - <<'PY'
+import json,glob
+for f in sorted(glob.glob("gpurun_out/ab3_*.json")):
+    try:
+        d=json.loads(open(f).read().strip().splitlines()[-1])
+        print(f, "%.4f ms"%d.get("ms", d.get("ms_per_step", 0)), d.get("launch", d.get("config",{}).get("launch")))
+    except Exception as e: print(f, open(f).read()[-300:])
+PY
