@@ -156,38 +156,39 @@ __device__ __forceinline__ int floor_i(double v) {  // floor(v), |v| < 2^31
 // radius r of the free (2r+1)^2-block box around it (then the ray leaves the
 // whole box).  Either way the ray exits through the face with the smaller
 // parameter (ties to x, as tmx <= tmy does) into the cell containing the
-// exit point.  Returns true when a live ray finished: r.t is then the range
-// and `hit` the occupied cell it entered (or -1).
+// exit point.  Returns true when a live ray finished.  r.t then holds the
+// exit parameter of its last free cell: the range once clipped to max_range
+// (ray_range), and ray_hit() recovers the occupied cell it stopped in.
 // kBordered: every map has an occupied border, so no step can leave the grid.
 template <bool kBordered>
-__device__ __forceinline__ bool ray_step(Ray& r, bool live, const MapView& mv, const EnvDev& d,
-                                         int& hit) {
+__device__ __forceinline__ bool ray_step(Ray& r, bool live, const MapView& mv, const EnvDev& d) {
   const uint32_t code = mv.code(r.ix, r.iy);
-  const bool cellwise = (code & 0x80u) != 0u;
+  const bool cellwise = code >= 0x80u;
   const bool occupied = cellwise && ((code >> (((r.iy & 1) << 1) | (r.ix & 1))) & 1u);
-  // forward edge of the free region: the cell itself, or the box's far edge
+  // last cell of the free region on each axis: the cell itself, or the box's
+  // far cell (ix | 1) + sx * (2r + 1) - fx, written as a face index below
+  const int k = (int)(code << 1) + 1;  // 2r + 1 (unused when cellwise)
   const int fx = (r.sx + 1) >> 1, fy = (r.sy + 1) >> 1;  // 1 when moving +
-  const int two_r = (int)(code << 1);
-  const int ex = cellwise ? r.ix : (r.ix & ~1) + fx + r.sx * two_r;
-  const int ey = cellwise ? r.iy : (r.iy & ~1) + fy + r.sy * two_r;
-  const double tx = (i2d(ex + fx) - r.x0) * r.idx;
-  const double ty = (i2d(ey + fy) - r.y0) * r.idy;
+  const int face_x = cellwise ? r.ix + fx : (r.ix | 1) + r.sx * k;
+  const int face_y = cellwise ? r.iy + fy : (r.iy | 1) + r.sy * k;
+  const double tx = (i2d(face_x) - r.x0) * r.idx;
+  const double ty = (i2d(face_y) - r.y0) * r.idy;
   const bool xs = tx <= ty;
   const double t = xs ? tx : ty;
-  // the cell on the other axis at the exit point, between the current cell
-  // and the forward edge (the ray moves monotonically)
-  const int c = floor_i(xs ? fma(tx, r.dy, r.y0) : fma(ty, r.dx, r.x0));
-  const int cy = r.sy > 0 ? min(max(c, r.iy), ey) : max(min(c, r.iy), ey);
-  const int cx = r.sx > 0 ? min(max(c, r.ix), ex) : max(min(c, r.ix), ex);
-  const int nx = xs ? ex + r.sx : cx;
-  const int ny = xs ? cy : ey + r.sy;
+  // the cell on the other axis at the exit point, clamped between the current
+  // cell and the region's far cell (the ray moves monotonically)
+  const int c = floor_i(fma(t, xs ? r.dy : r.dx, xs ? r.y0 : r.x0));
+  const int lo = xs ? r.iy : r.ix;
+  const int hi = xs ? face_y - fy : face_x - fx;
+  const int cc = min(max(c, min(lo, hi)), max(lo, hi));
+  const int nx = xs ? face_x - fx + r.sx : cc;  // far cell + sx
+  const int ny = xs ? cc : face_y - fy + r.sy;
   const bool over = t > d.max_range;  // :97-99
   const bool out = !kBordered && ((unsigned)nx >= (unsigned)d.W || (unsigned)ny >= (unsigned)d.H);
-  hit = occupied ? r.iy * d.W + r.ix : -1;
   const bool finished = occupied || over || out;
   r.n += live ? 1 : 0;
   if (live && !occupied) {
-    r.t = over ? d.max_range : t;
+    r.t = t;
     if (!finished) {
       r.ix = nx;
       r.iy = ny;
@@ -196,9 +197,23 @@ __device__ __forceinline__ bool ray_step(Ray& r, bool live, const MapView& mv, c
   return live && finished;
 }
 
+// range of a finished ray (the over-range exit clips to max_range)
+__device__ __forceinline__ double ray_range(const Ray& r, const EnvDev& d) {
+  return r.t > d.max_range ? d.max_range : r.t;
+}
+
+// occupied cell a finished ray stopped in, or -1 (range / grid exit, origin
+// outside the grid): a ray that hits stays in the occupied cell.
+__device__ __forceinline__ int ray_hit(const Ray& r, const MapView& mv, const EnvDev& d) {
+  if ((unsigned)r.ix >= (unsigned)d.W || (unsigned)r.iy >= (unsigned)d.H) return -1;
+  const uint32_t code = mv.code(r.ix, r.iy);
+  const bool occ = code >= 0x80u && ((code >> (((r.iy & 1) << 1) | (r.ix & 1))) & 1u);
+  return occ ? r.iy * d.W + r.ix : -1;
+}
+
 // Returns true if finished during setup (origin outside the grid -> 0).
 __device__ __forceinline__ bool ray_setup(Ray& r, double x0, double y0, double ch, double sh,
-                                          double2 cs, const EnvDev& d, int& hit) {
+                                          double2 cs, const EnvDev& d) {
   const double dx = ch * cs.x - sh * cs.y;  // cos(h + o_j)
   const double dy = sh * cs.x + ch * cs.y;  // sin(h + o_j)
   r.x0 = x0 * d.inv_cell;
@@ -213,11 +228,7 @@ __device__ __forceinline__ bool ray_setup(Ray& r, double x0, double y0, double c
   r.n = 0;
   r.ix = (int)floor(r.x0);
   r.iy = (int)floor(r.y0);
-  if ((unsigned)r.ix >= (unsigned)d.W || (unsigned)r.iy >= (unsigned)d.H) {  // :37-39
-    hit = -1;
-    return true;
-  }
-  return false;
+  return (unsigned)r.ix >= (unsigned)d.W || (unsigned)r.iy >= (unsigned)d.H;  // :37-39
 }
 
 // Per-CTA chunk scratch (shared memory).  A chunk holds up to `cap` envs;
@@ -285,7 +296,7 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
   const unsigned lt = lanemask_lt();
   bool act_a = false, act_b = false, done_a = false, done_b = false;
   bool drained = total == 0;
-  int ea = 0, ja = 0, eb = 0, jb = 0, hit_a = -1, hit_b = -1;
+  int ea = 0, ja = 0, eb = 0, jb = 0;
   Ray ra, rb;
   ra.ix = ra.iy = rb.ix = rb.iy = 0;
   ra.sx = ra.sy = rb.sx = rb.sy = 1;
@@ -300,11 +311,11 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
     const int na = __popc(ia), n_idle = na + __popc(ib);
     if (n_idle >= d.refill_min || drained) {
       if (done_a) {
-        fin(ea, ja, ra.t, hit_a, ra.n);
+        fin(ea, ja, ray_range(ra, d), kHit ? ray_hit(ra, mv, d) : -1, ra.n);
         done_a = false;
       }
       if (done_b) {
-        fin(eb, jb, rb.t, hit_b, rb.n);
+        fin(eb, jb, ray_range(rb, d), kHit ? ray_hit(rb, mv, d) : -1, rb.n);
         done_b = false;
       }
       if (drained) {
@@ -320,14 +331,14 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
           const int g = div_r(my_a, d);
           ea = c.list[g];
           ja = my_a - g * R;
-          act_a = !ray_setup(ra, c.px[ea], c.py[ea], c.ch[ea], c.sh[ea], beam[ja], d, hit_a);
+          act_a = !ray_setup(ra, c.px[ea], c.py[ea], c.ch[ea], c.sh[ea], beam[ja], d);
           done_a = !act_a;
         }
         if (!act_b && my_b < total) {
           const int g = div_r(my_b, d);
           eb = c.list[g];
           jb = my_b - g * R;
-          act_b = !ray_setup(rb, c.px[eb], c.py[eb], c.ch[eb], c.sh[eb], beam[jb], d, hit_b);
+          act_b = !ray_setup(rb, c.px[eb], c.py[eb], c.ch[eb], c.sh[eb], beam[jb], d);
           done_b = !act_b;
         }
       }
@@ -337,11 +348,8 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
     // sits out the second (live = act)
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-      int ha, hb;
-      const bool fa = ray_step<kBordered>(ra, act_a, mv, d, ha);
-      const bool fb = ray_step<kBordered>(rb, act_b, mv, d, hb);
-      if (fa) hit_a = kHit ? ha : -1;
-      if (fb) hit_b = kHit ? hb : -1;
+      const bool fa = ray_step<kBordered>(ra, act_a, mv, d);
+      const bool fb = ray_step<kBordered>(rb, act_b, mv, d);
       act_a = act_a && !fa;
       act_b = act_b && !fb;
       done_a = done_a || fa;
