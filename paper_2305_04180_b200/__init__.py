@@ -8,6 +8,10 @@ Drop-in names of the reference package ``color_rl``:
   GridMap, MapError, DiversityRanges, SimParams,
   LidarConfig, EnvConfig, Event, EpisodeTerminated     (color_rl.sim)
   kernels (BACKEND_NAME = "cuda": cast_rays, disc_collides)  (color_rl.kernels seam)
+Submodules beyond the hot path:
+  asl       Q-net, DDQN + fused Adam + CUDA-graphed update, VEM, TFM, Sharer, session
+  evaluate  greedy evaluation (evaluate_params, EvalReport, summarize_rates)
+  mapgen    procedural arenas, host side (generate_map(s), write_maps)
 """
 
 from paper_2305_04180_b200.sim import (  # noqa: F401

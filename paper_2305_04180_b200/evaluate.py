@@ -37,6 +37,7 @@ __all__ = ["MapEval", "EvalReport", "evaluate_params", "summarize_rates"]
 
 @dataclass
 class MapEval:  # evaluate.py:22-42
+    """Outcome counts of one map's scored first episodes."""
     name: str
     episodes: int
     arrivals: int
@@ -49,17 +50,29 @@ class MapEval:  # evaluate.py:22-42
     def arrival_rate(self) -> float:
         return self.arrivals / self.episodes
 
+    _KEYS = ("name", "episodes", "arrivals", "collisions", "timeouts", "arrival_rate",
+             "mean_return", "mean_steps")
+
     def to_dict(self) -> dict:
-        return {
-            "name": self.name, "episodes": self.episodes,
-            "arrivals": self.arrivals, "collisions": self.collisions,
-            "timeouts": self.timeouts, "arrival_rate": self.arrival_rate,
-            "mean_return": self.mean_return, "mean_steps": self.mean_steps,
-        }
+        return {k: getattr(self, k) for k in self._KEYS}
+
+
+# render() columns: (header, width, row formatter) -- evaluate.py:72-85
+_COLUMNS = (("map", -28, lambda r: r.name), ("episodes", 8, lambda r: f"{r.episodes}"),
+            ("arrived", 8, lambda r: f"{r.arrivals}"), ("rate", 6, lambda r: f"{r.arrival_rate:.2f}"),
+            ("return", 9, lambda r: f"{r.mean_return:.2f}"), ("steps", 7, lambda r: f"{r.mean_steps:.1f}"))
+
+
+def _cells(values) -> str:
+    out = []
+    for (_, w, _f), v in zip(_COLUMNS, values):
+        out.append(v.ljust(-w) if w < 0 else v.rjust(w))
+    return " ".join(out)
 
 
 @dataclass
 class EvalReport:  # evaluate.py:45-85
+    """Per-map results of one evaluation seed, pooled on demand."""
     seed: int
     results: list = field(default_factory=list)
 
@@ -69,35 +82,25 @@ class EvalReport:  # evaluate.py:45-85
 
     @property
     def arrival_rate(self) -> float:
-        total = self.episodes
-        return sum(r.arrivals for r in self.results) / total if total else 0.0
+        n = self.episodes
+        return sum(r.arrivals for r in self.results) / n if n else 0.0
 
     @property
     def mean_return(self) -> float:
-        total = self.episodes
-        if not total:
-            return 0.0
-        return sum(r.mean_return * r.episodes for r in self.results) / total
+        n = self.episodes
+        return sum(r.mean_return * r.episodes for r in self.results) / n if n else 0.0
 
     def to_dict(self) -> dict:
-        return {
-            "seed": self.seed,
-            "arrival_rate": self.arrival_rate,
-            "mean_return": self.mean_return,
-            "episodes": self.episodes,
-            "maps": [r.to_dict() for r in self.results],
-        }
+        return dict(seed=self.seed, arrival_rate=self.arrival_rate,
+                    mean_return=self.mean_return, episodes=self.episodes,
+                    maps=[r.to_dict() for r in self.results])
 
     def render(self) -> str:
-        lines = [f"{'map':<28} {'episodes':>8} {'arrived':>8} {'rate':>6} "
-                 f"{'return':>9} {'steps':>7}"]
-        for r in self.results:
-            lines.append(f"{r.name:<28} {r.episodes:>8} {r.arrivals:>8} "
-                         f"{r.arrival_rate:>6.2f} {r.mean_return:>9.2f} "
-                         f"{r.mean_steps:>7.1f}")
-        lines.append(f"{'pooled':<28} {self.episodes:>8} "
-                     f"{sum(r.arrivals for r in self.results):>8} "
-                     f"{self.arrival_rate:>6.2f} {self.mean_return:>9.2f}")
+        lines = [_cells([c[0] for c in _COLUMNS])]
+        lines += [_cells([f(r) for _, _, f in _COLUMNS]) for r in self.results]
+        pooled = ["pooled", f"{self.episodes}", f"{sum(r.arrivals for r in self.results)}",
+                  f"{self.arrival_rate:.2f}", f"{self.mean_return:.2f}"]
+        lines.append(_cells(pooled))
         return "\n".join(lines)
 
 

@@ -197,6 +197,27 @@ class GridMap:
     def in_bounds(self, x_cm: float, y_cm: float) -> bool:
         return 0.0 <= x_cm < self.width_cm and 0.0 <= y_cm < self.height_cm
 
+    def edt_cells(self) -> np.ndarray:
+        """Euclidean distance (cell units, centre to centre) to the nearest
+        occupied cell (gridmap.py:62-71). The device path does not use it: the
+        marcher skips free space with its own chessboard block table. It is
+        kept for API parity and computed once on first use."""
+        if getattr(self, "_edt", None) is None:
+            from scipy import ndimage
+            self._edt = ndimage.distance_transform_edt(~self.occupancy).astype(np.float64)
+        return self._edt
+
+    def to_ascii(self, robot_xy=None) -> str:
+        """Text-format body without the header; 'R' marks the robot's cell when
+        a pose is given (gridmap.py:185-195)."""
+        rows = self.to_text().splitlines()[1:]
+        if robot_xy is not None:
+            ix, iy = self.cell_of(*robot_xy)
+            k = self.n_rows - 1 - iy
+            if 0 <= k < len(rows) and 0 <= ix < self.n_cols:
+                rows[k] = rows[k][:ix] + "R" + rows[k][ix + 1:]
+        return "\n".join(rows)
+
     def _check(self) -> None:  # gridmap.py:75-103
         c = self.cell_size_cm
         if c <= 0:

@@ -144,3 +144,55 @@ def test_eval_report_matches_reference_formatting():
     assert got.to_dict() == want.to_dict()
     assert got.render() == want.render()
     assert E.summarize_rates([got, got]) == R.summarize_rates([want, want])
+
+
+def test_mapgen_reproduces_golden_maps():
+    """mapgen restatement: seed 0 regenerates the reference-made golden maps
+    cell for cell (tests/golden/maps16.npz came from the reference's
+    generate_maps(16, seed=0))."""
+    import hashlib
+    from helpers import golden
+    from paper_2305_04180_b200.mapgen import generate_maps
+    from paper_2305_04180_b200.sim import GridMap as G
+    want = load_maps(4)  # stored after the reference's text round trip
+    sha = golden("maps16.npz")["sha256"]  # of the reference's original map text
+    got = generate_maps(4, seed=0)
+    for g, w, h in zip(got, want, sha):
+        assert np.array_equal(g.occupancy, w.occupancy)
+        assert hashlib.sha256(g.to_text().encode()).hexdigest() == str(h)
+        rt = G.from_text(g.to_text())
+        assert rt.goal_center == w.goal_center and rt.goal_radius_cm == w.goal_radius_cm
+        assert rt.spawn_region == w.spawn_region
+
+
+def test_mapgen_matches_reference_small(tmp_path):
+    """Small arenas, other seeds and densities: same maps as the reference's
+    generate_maps; write_maps names and round-trips; errors as the reference."""
+    from oracle import oracle as O
+    from paper_2305_04180_b200.mapgen import MapGenError, generate_map, generate_maps, write_maps
+    from paper_2305_04180_b200.sim import GridMap as G
+    maps = generate_maps(3, seed=5, size_cm=120)
+    paths = write_maps(maps, tmp_path)
+    assert [p.name for p in paths] == ["map00.txt", "map01.txt", "map02.txt"]
+    for p, m in zip(paths, maps):
+        assert np.array_equal(G.load(p).occupancy, m.occupancy)
+    with pytest.raises(ValueError):
+        generate_map(np.random.default_rng(0), density=1.0)
+    with pytest.raises(ValueError):
+        generate_map(np.random.default_rng(0), size_cm=6)
+    with pytest.raises(MapGenError):
+        generate_map(np.random.default_rng(0), size_cm=120, robot_radius_cm=60.0, layout_attempts=2)
+    if not O.reference_available():
+        return
+    O.import_reference()
+    from color_rl import mapgen as R
+    for seed, size, dens in ((5, 120, 0.08), (7, 200, 0.15), (11, 366, 0.05)):
+        a = generate_maps(2, seed=seed, size_cm=size, density=dens)
+        b = R.generate_maps(2, seed=seed, size_cm=size, density=dens)
+        for x, y in zip(a, b):
+            assert x.to_text() == y.to_text()
+    m = G.from_text(maps[0].to_text())
+    ref_m = R.GridMap.from_text(maps[0].to_text())
+    assert np.array_equal(m.edt_cells(), ref_m.edt_cells())
+    assert m.to_ascii((30.0, 30.0)) == ref_m.to_ascii((30.0, 30.0))
+    assert m.to_ascii() == ref_m.to_ascii()
