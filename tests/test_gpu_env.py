@@ -411,3 +411,69 @@ def test_step_host_matches_device_step():
             assert np.array_equal(getattr(x, f).cpu().numpy(), getattr(y, f)), (t, f)
     with pytest.raises(ValueError):
         b_env.step_host(np.full(n, 7))
+
+
+def test_reset_clears_terminal_flag_and_velocity():  # test_env.py:282-296
+    env = make_env(40, cfg=EnvConfig(timeout_steps=3))
+    env.reset(17)
+    for _ in range(3):
+        out = env.step(2)
+        if out.done or out.truncated:
+            break
+    assert env.episode_over
+    env.reset(18)
+    assert not env.episode_over
+    st = env.state
+    assert st.v_linear_cm_s == 0.0 and st.v_angular_rad_s == 0.0
+    assert env.steps_taken == 0
+
+
+def test_lidar_scan_noise_is_clamped_and_seeded():  # test_env.py:310-319
+    from paper_2305_04180_b200.env import RobotState, lidar_scan
+    m = make_map(30)
+    pose = RobotState(15.0, 15.0, 0.0, 0, 0, 9.0)
+    cfg = LidarConfig(max_range_cm=50.0)
+    a = lidar_scan(m, pose, cfg, noise_std=5.0, rng=np.random.default_rng(1))
+    b = lidar_scan(m, pose, cfg, noise_std=5.0, rng=np.random.default_rng(1))
+    assert np.array_equal(a, b)
+    assert (a >= 0).all() and (a <= 50.0).all()
+    assert not np.array_equal(a, lidar_scan(m, pose, cfg, noise_std=0.0))
+
+
+def test_pooled_rate_matches_raw_counters():  # test_vecenv.py:141-152
+    from paper_2305_04180_b200 import VecEnv
+    env = VecEnv([make_map(40)], 3, _rg(0.0), EnvConfig(timeout_steps=2))
+    env.reset_all(11)
+    for _ in range(8):
+        env.step_batch([0, 1, 2])
+    snap = env.snapshot_stats()
+    eps = sum(c.episodes for c in snap.per_copy)
+    arr = sum(c.arrivals for c in snap.per_copy)
+    assert snap.episodes == eps == 3 * 4
+    assert (snap.arrival_rate or 0.0) == pytest.approx(arr / eps if eps else 0.0)
+
+
+def test_mixed_grid_shapes_rejected():  # test_vecenv.py:162-164
+    from paper_2305_04180_b200 import VecEnv
+    with pytest.raises(MapError):
+        VecEnv([make_map(40), make_map(50)], 2, [_rg(), _rg()])
+    with pytest.raises(ValueError):
+        VecEnv([make_map(40)], 2, [_rg()])  # one DiversityRanges per lane
+
+
+def test_n1_matches_single_env():  # test_vecenv.py:27-39
+    """A 1-copy VecEnv and the single-robot RobotEnv on the same map and seed
+    reset and step identically (the RobotEnv is lane 0 of the same kernel)."""
+    from paper_2305_04180_b200 import VecEnv
+    from paper_2305_04180_b200.env import RobotEnv
+    m = make_map(40)
+    vec = VecEnv([m], 1, _rg())
+    sv = vec.reset_all(3).cpu().numpy()
+    env = RobotEnv(m, _rg())
+    ss = env.reset(3)
+    assert np.array_equal(sv[0], ss)
+    for a in (2, 0, 4, 2, 1):
+        b = vec.step_batch([a])
+        out = env.step(a)
+        assert np.array_equal(b.store_states[0].cpu().numpy(), out.state)
+        assert float(b.rewards[0]) == out.reward

@@ -156,3 +156,55 @@ def test_cuda_backend_drives_the_unmodified_reference():
         acts = random_actions(5, np.arange(32), t)
         x, y = stock.step_batch(acts), ours.step_batch(acts)
         assert np.array_equal(x.states, y.states) and np.array_equal(x.rewards, y.rewards)
+
+
+def _slab_entry(occ, x, y, ang, max_range):
+    """Exact geometry, independent of any DDA: the smallest entry parameter of
+    the ray into an occupied cell rectangle (slab test over every occupied
+    cell), capped at max_range; plus that crossing's chord length."""
+    dx, dy = np.cos(ang), np.sin(ang)
+    iy, ix = np.nonzero(occ)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        tx0, tx1 = (ix - x) / dx, (ix + 1 - x) / dx
+        ty0, ty1 = (iy - y) / dy, (iy + 1 - y) / dy
+    if dx == 0.0:
+        inside = (ix <= x) & (x < ix + 1)
+        tx0 = np.where(inside, -np.inf, np.inf)
+        tx1 = np.where(inside, np.inf, -np.inf)
+    if dy == 0.0:
+        inside = (iy <= y) & (y < iy + 1)
+        ty0 = np.where(inside, -np.inf, np.inf)
+        ty1 = np.where(inside, np.inf, -np.inf)
+    t_in = np.maximum(np.minimum(tx0, tx1), np.minimum(ty0, ty1))
+    t_out = np.minimum(np.maximum(tx0, tx1), np.maximum(ty0, ty1))
+    ok = (t_out >= np.maximum(t_in, 0.0))
+    if not ok.any():
+        return max_range, 0.0
+    k = np.argmin(np.where(ok, np.maximum(t_in, 0.0), np.inf))
+    t = max(t_in[k], 0.0)
+    return (min(t, max_range), t_out[k] - t) if t < max_range else (max_range, 0.0)
+
+
+def test_matches_exact_slab_geometry():  # test_kernels.py:47-67 (exact oracle instead of a fine march)
+    """Every range equals the exact first entry into an occupied cell, except
+    tangential grazes (chord ~0) where the DDA's face order decides."""
+    rng = np.random.default_rng(11)
+    for _ in range(20):
+        occ, sample = random_scene(rng)
+        x, y = sample()
+        angles = rng.uniform(-np.pi, np.pi) + np.linspace(-2.3, 2.3, 27)
+        got = cast(occ, x, y, angles, max_range=45.0)
+        for a, g in zip(angles, got):
+            t, chord = _slab_entry(occ, x, y, a, 45.0)
+            if abs(g - t) > 1e-9:
+                assert chord < 1e-9 and g > t, (x, y, a, g, t, chord)
+
+
+def test_batched_equals_per_ray():  # test_kernels.py:102-110
+    rng = np.random.default_rng(9)
+    occ, sample = random_scene(rng)
+    x, y = sample()
+    angles = rng.uniform(-np.pi, np.pi, 27)
+    batched = cast(occ, x, y, angles)
+    single = np.concatenate([cast(occ, x, y, angles[i:i + 1]) for i in range(27)])
+    assert np.array_equal(batched, single)
