@@ -76,7 +76,7 @@ def main():
                               np.repeat(qy[sub], args.beams), np.cos(ang).ravel(),
                               np.sin(ang).ravel(), 1.0, args.max_range)
     out = {"poses": n, "beams": args.beams, "max_range": args.max_range,
-           "refill_min": os.environ.get("SPARROW_REFILL_MIN", "16"),
+           "refill_min": os.environ.get("SPARROW_REFILL_MIN", "32 (default)"),
            "ms": t * 1e3, "rays_per_s": rays / t, "mean_dda_cells_per_ray": float(cells.mean()),
            "ray_cells_per_s": rays * float(cells.mean()) / t, "launch": env.launch_info()}
     print(json.dumps(out))
