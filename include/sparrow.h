@@ -28,6 +28,7 @@
  *   sp_random_actions   bench.py:97-105 (random policy actions), on device
  *   sp_philox_fill      asl/vem.py:57-66 draws (rng.random / rng.integers), on device
  *   sp_adam_step        net.py:141-161 adam_step, fused over all tensors, on device
+ *   sp_ddqn_update      ddqn.py:54-77 DdqnLearner.update (targets, backprop, Adam), on device
  */
 #ifndef SPARROW_H_
 #define SPARROW_H_
@@ -186,6 +187,31 @@ int sp_adam_step(int n_tensors, float* const* params, const float* const* grads,
                  float* const* v, const int64_t* numels, double* step_dev, int64_t step_host,
                  const float* gate, double lr, double beta1, double beta2, double eps,
                  void* stream);
+
+/* The Q-net of net.py: sizes {D0, H1, H2, A}; W[l] row-major (fan_in, fan_out)
+ * fp32 device arrays, b[l] (fan_out). */
+typedef struct SpMlp {
+  int32_t sizes[4];
+  float* W[3];
+  float* b[3];
+} SpMlp;
+
+/* scratch (floats) sp_ddqn_update needs for a batch of `batch` rows */
+int64_t sp_ddqn_scratch_floats(const int32_t* sizes, int64_t batch);
+/* One double-DQN update in three launches (row-parallel forward/deltas,
+ * parameter-parallel gradient + gated Adam, step tick); replaces ddqn.py:54-77 (DdqnLearner.
+ * update: compute_targets :38-51, net.backward :88-115, adam_step net.py:151-161).
+ * Batch columns are device arrays (s, s2: (batch, D0) f32; a i64; r f32; d u8).
+ * m/v: the six Adam moment tensors in W1 W2 W3 b1 b2 b3 order; *step_dev is the
+ * Adam step count (incremented on device when the update applies).  The update
+ * applies only if the loss is finite (ddqn.py:66-71); stats_out (device, 2 f32)
+ * receives {mean Huber loss, mean |td|}.  Requires D0 <= 128, H1, H2 <= 256,
+ * A <= 16 and 16-byte aligned weights.  The target net is read only. */
+int sp_ddqn_update(const SpMlp* online, const SpMlp* target, const float* s, const int64_t* a,
+                   const float* r, const float* s2, const uint8_t* d, int64_t batch, float gamma,
+                   float* const* m, float* const* v, double* step_dev, double lr, double beta1,
+                   double beta2, double eps, float* scratch, int64_t scratch_floats,
+                   float* stats_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -111,9 +111,22 @@ SIGNATURES = [
     ("sp_adam_step", ctypes.c_int, [ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_i64p, c_vp,
                                     ctypes.c_int64, c_vp, ctypes.c_double, ctypes.c_double,
                                     ctypes.c_double, ctypes.c_double, c_vp]),
+    ("sp_ddqn_scratch_floats", ctypes.c_int64, [c_i32p, ctypes.c_int64]),
+    ("sp_ddqn_update", ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_int64,
+                                      ctypes.c_float, c_vp, c_vp, c_vp, ctypes.c_double,
+                                      ctypes.c_double, ctypes.c_double, ctypes.c_double, c_vp,
+                                      ctypes.c_int64, c_vp, c_vp]),
 ]
 
 _lib = None
+
+
+class SpMlp(ctypes.Structure):
+    _fields_ = [
+        ("sizes", ctypes.c_int32 * 4),
+        ("W", ctypes.c_void_p * 3),
+        ("b", ctypes.c_void_p * 3),
+    ]
 
 
 class SparrowError(RuntimeError):

@@ -349,15 +349,117 @@ class _GraphedUpdate:
         self.graph.replay()
 
 
+class _FusedUpdate:
+    """One DDQN update as ``sp_ddqn_update``: two hand-written kernels plus a
+    one-thread step tick (csrc/sp_learn.cu), instead of ~100 small torch ones.
+    - ``ddqn_rows_kernel``: one CTA per 4-row tile, weights TMA-staged per layer.
+      It computes the targets, the cached forward, the Huber gradient and the
+      layer deltas.
+    - ``ddqn_grad_adam_kernel``: the weight gradients as 16x32 tiles over the
+      batch (fixed row order), with the finite-gated Adam step in the epilogue.
+    Optionally the three launches replay as one CUDA graph. Same static-batch
+    and device-step contract as ``_GraphedUpdate``."""
+
+    def __init__(self, learner: "DdqnLearner", batch_size: int, state_dim: int, graph: bool):
+        from paper_2305_04180_b200.replay import TransitionBatch
+        torch = _torch()
+        self.learner = learner
+        on, tg, ad = learner.online, learner.target, learner.adam
+        if len(on.weights) != 3:
+            raise ValueError("the fused learner kernel supports the 3-layer Q-net only")
+        if batch_size * (16 + 32) * 4 > 200 * 1024:
+            raise ValueError("fused learner: batch > 1066 rows exceeds the gradient-tile staging; "
+                             "use graph=True without fused")
+        dev = on.weights[0].device
+        b, d = int(batch_size), int(state_dim)
+        self.batch_size, self.state_dim = b, d
+        self.batch = TransitionBatch(torch.zeros((b, d), dtype=torch.float32, device=dev),
+                                     torch.zeros(b, dtype=torch.int64, device=dev),
+                                     torch.zeros(b, dtype=torch.float32, device=dev),
+                                     torch.zeros((b, d), dtype=torch.float32, device=dev),
+                                     torch.zeros(b, dtype=torch.bool, device=dev))
+        self.t = torch.full((), float(ad.step), dtype=torch.float64, device=dev)
+        self.stats = torch.zeros(2, dtype=torch.float32, device=dev)
+        self._lib = _lib.load()
+        sizes = (ctypes.c_int32 * 4)(*on.sizes)
+        n = int(self._lib.sp_ddqn_scratch_floats(sizes, b))
+        if n < 0:
+            raise ValueError("bad learner shapes")
+        self.scratch = torch.empty(n, dtype=torch.float32, device=dev)
+        for t in on.weights + on.biases + tg.weights + tg.biases:
+            if not t.is_contiguous() or t.dtype != torch.float32:
+                raise ValueError("Q-net tensors must be contiguous float32")
+
+        def mlp(net):
+            m = _lib.SpMlp()
+            for i, v in enumerate(net.sizes):
+                m.sizes[i] = v
+            for i in range(3):
+                m.W[i] = net.weights[i].data_ptr()
+                m.b[i] = net.biases[i].data_ptr()
+            return m
+        self._on, self._tg = mlp(on), mlp(tg)
+        arr = ctypes.c_void_p * 6
+        self._m = arr(*[t.data_ptr() for t in ad.m_weights + ad.m_biases])
+        self._v = arr(*[t.data_ptr() for t in ad.v_weights + ad.v_biases])
+        self.graph = None
+        if graph:
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            state = on.weights + on.biases + ad.m_weights + ad.v_weights + ad.m_biases + ad.v_biases
+            saved = [x.clone() for x in state]
+            with torch.cuda.stream(side):
+                self._launch()  # warm-up (attribute setup) before capture
+            torch.cuda.current_stream(dev).wait_stream(side)
+            for x, y in zip(state, saved):
+                x.copy_(y)
+            self.t.fill_(float(ad.step))
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
+                self._launch()
+
+    @property
+    def loss(self):
+        return self.stats[0]
+
+    @property
+    def mad(self):
+        return self.stats[1]
+
+    def _launch(self) -> None:
+        lr, ad, bt = self.learner, self.learner.adam, self.batch
+        dev = lr.online.weights[0].device
+        _lib.check(self._lib.sp_ddqn_update(
+            ctypes.byref(self._on), ctypes.byref(self._tg), bt.states.data_ptr(),
+            bt.actions.data_ptr(), bt.rewards.data_ptr(), bt.next_states.data_ptr(),
+            bt.dones.data_ptr(), self.batch_size, float(lr.config.gamma), self._m, self._v,
+            self.t.data_ptr(), float(ad.lr), float(ad.beta1), float(ad.beta2), float(ad.eps),
+            self.scratch.data_ptr(), self.scratch.numel(), self.stats.data_ptr(),
+            _lib.stream_ptr(dev)), "ddqn_update")
+
+    def run(self, batch) -> None:
+        if batch is not self.batch:
+            for dst, src in zip(self.batch, batch):
+                dst.copy_(src.reshape(dst.shape), non_blocking=True)
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._launch()
+
+
 class DdqnLearner:
     """Online/target pair and one update per batch (ddqn.py:54-77).
 
-    ``graph=True`` replays each update as one CUDA graph (``_GraphedUpdate``);
-    numerics are unchanged. ``graph_batch(B, D)`` returns the static batch a
-    sampler should fill to skip the copy-in."""
+    Update paths, same numerics contract (fp32, tests at 1e-4 vs the reference):
+    - eager torch (default);
+    - ``graph=True``: the torch update replayed as one CUDA graph (``_GraphedUpdate``);
+    - ``fused=True``: the hand-written ``sp_ddqn_update`` kernels (``_FusedUpdate``),
+      optionally graph-replayed too.
+    ``graph_batch(B, D)`` returns the static batch a sampler should fill to
+    skip the copy-in (None on the eager path)."""
 
     def __init__(self, params: QNet, config: DdqnConfig | None = None, check_finite: bool = True,
-                 graph: bool = False):
+                 graph: bool = False, fused: bool = False):
         self.config = config or DdqnConfig()
         self.online = params
         self.target = params.copy()
@@ -365,14 +467,16 @@ class DdqnLearner:
         self.update_count = 0
         self.check_finite = check_finite
         self.graph = bool(graph)
+        self.fused = bool(fused)
         self._graphed = None
 
     def graph_batch(self, batch_size: int, state_dim: int):
-        if not self.graph:
+        if not (self.graph or self.fused):
             return None
         g = self._graphed
         if g is None or g.batch_size != batch_size or g.state_dim != state_dim:
-            g = self._graphed = _GraphedUpdate(self, batch_size, state_dim)
+            g = self._graphed = (_FusedUpdate(self, batch_size, state_dim, self.graph)
+                                 if self.fused else _GraphedUpdate(self, batch_size, state_dim))
         return g.batch
 
     def _update_graphed(self, batch) -> UpdateStats:
@@ -398,7 +502,7 @@ class DdqnLearner:
         return UpdateStats(loss_v, mad_v, self.online.version, synced)
 
     def update(self, batch) -> UpdateStats:
-        if self.graph:
+        if self.graph or self.fused:
             return self._update_graphed(batch)
         targets = compute_targets(batch, self.online, self.target, self.config.gamma)
         gw, gb, loss, mad = backward(self.online, batch.states, batch.actions, targets)

@@ -17,6 +17,7 @@
 
 #include "sp_env.cu"
 #include "sp_ops.cu"
+#include "sp_learn.cu"
 
 using namespace sp;
 
@@ -908,7 +909,7 @@ int sp_rb_sample(SpReplay* rb, int64_t batch, uint64_t seed, uint32_t stream_id,
                                   std::to_string(batch));
   if (batch < 1) return SP_OK;
   if (!states || !actions || !rewards || !next_states || !dones) return fail(SP_EINVAL, "null argument");
-  const int blocks = (int)((batch + 255) / 256);
+  const int blocks = (int)((batch + 7) / 8);  // one warp per row
   rb_sample_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
       rb->s, rb->a, rb->r, rb->s2, rb->dn, rb->dim, rb->size, batch, seed, stream_id, ctr, states,
       actions, rewards, next_states, dones, idx_out);
@@ -987,6 +988,104 @@ int sp_adam_step(int n_tensors, float* const* params, const float* const* grads,
     adam_tick_kernel<<<1, 1, 0, s>>>(step_dev, gate);
     SP_CUDA(cudaGetLastError());
   }
+  return SP_OK;
+}
+
+static int learn_tr(int64_t batch) { return batch % 4 == 0 ? 4 : 1; }
+
+int64_t sp_ddqn_scratch_floats(const int32_t* sz, int64_t batch) {
+  if (!sz || batch < 1) return -1;
+  const int64_t tiles = batch / learn_tr(batch);
+  // a1, d1 (B x H1), a2, d2 (B x H2), dq (B x A), loss partials (tiles x 2)
+  return batch * (2 * (int64_t)sz[1] + 2 * (int64_t)sz[2] + sz[3]) + 2 * tiles;
+}
+
+int sp_ddqn_update(const SpMlp* on, const SpMlp* tg, const float* s, const int64_t* a,
+                   const float* r, const float* s2, const uint8_t* d, int64_t batch, float gamma,
+                   float* const* m, float* const* v, double* step_dev, double lr, double beta1,
+                   double beta2, double eps, float* scratch, int64_t scratch_floats,
+                   float* stats_out, void* stream) {
+  if (!on || !tg || !s || !a || !r || !s2 || !d || !m || !v || !step_dev || !scratch || !stats_out)
+    return fail(SP_EINVAL, "ddqn_update: null argument");
+  const int D0 = on->sizes[0], H1 = on->sizes[1], H2 = on->sizes[2], A = on->sizes[3];
+  for (int k = 0; k < 4; ++k)
+    if (tg->sizes[k] != on->sizes[k]) return fail(SP_EINVAL, "ddqn_update: online/target shapes differ");
+  if (D0 < 1 || D0 > kLearnMaxD0 || H1 < 1 || H1 > kLearnMaxH || H2 < 1 || H2 > kLearnMaxH ||
+      A < 1 || A > kLearnMaxA)
+    return fail(SP_EINVAL, "ddqn_update: unsupported layer sizes");
+  for (int l = 0; l < 3; ++l)
+    if (((uintptr_t)on->W[l] | (uintptr_t)tg->W[l]) & 15)
+      return fail(SP_EINVAL, "ddqn_update: weights must be 16-byte aligned");
+  if (((int64_t)D0 * H1) % 4 || ((int64_t)H1 * H2) % 4 || ((int64_t)H2 * A) % 4)
+    return fail(SP_EINVAL, "ddqn_update: each weight matrix must hold a multiple of 4 floats");
+  if (batch < 1 || batch > (1 << 24)) return fail(SP_EINVAL, "ddqn_update: bad batch size");
+  const int64_t need = sp_ddqn_scratch_floats(on->sizes, batch);
+  if (scratch_floats < need) return fail(SP_EINVAL, "ddqn_update: scratch too small");
+  const int TR = learn_tr(batch);
+  const int tiles = (int)(batch / TR);
+  LearnArgs la{};
+  for (int l = 0; l < 3; ++l) {
+    la.on.W[l] = on->W[l];
+    la.on.b[l] = on->b[l];
+    la.tgt.W[l] = tg->W[l];
+    la.tgt.b[l] = tg->b[l];
+  }
+  la.s = s; la.a = a; la.r = r; la.s2 = s2; la.d = d;
+  la.B = (int)batch; la.D0 = D0; la.H1 = H1; la.H2 = H2; la.A = A;
+  la.a1 = scratch;
+  la.d1 = la.a1 + batch * H1;
+  la.a2 = la.d1 + batch * H1;
+  la.d2 = la.a2 + batch * H2;
+  la.dq = la.d2 + batch * H2;
+  la.lpart = la.dq + batch * A;
+  la.gamma = gamma;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (TR == 4) {
+    const size_t sm = learn_smem_bytes<4>(D0, H1, H2, A);
+    SP_CUDA(cudaFuncSetAttribute(ddqn_rows_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sm));
+    ddqn_rows_kernel<4><<<tiles, kLearnThreads, sm, st>>>(la);
+  } else {
+    const size_t sm = learn_smem_bytes<1>(D0, H1, H2, A);
+    SP_CUDA(cudaFuncSetAttribute(ddqn_rows_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sm));
+    ddqn_rows_kernel<1><<<tiles, kLearnThreads, sm, st>>>(la);
+  }
+  SP_CUDA(cudaGetLastError());
+  AdamTensors T;
+  const float* ps[6] = {on->W[0], on->W[1], on->W[2], on->b[0], on->b[1], on->b[2]};
+  const int64_t n[6] = {(int64_t)D0 * H1, (int64_t)H1 * H2, (int64_t)H2 * A, H1, H2, A};
+  int64_t acc = 0;
+  for (int k = 0; k < 6; ++k) {
+    if (!m[k] || !v[k]) return fail(SP_EINVAL, "ddqn_update: null moment tensor");
+    T.p[k] = const_cast<float*>(ps[k]);
+    T.g[k] = nullptr;
+    T.m[k] = m[k];
+    T.v[k] = v[k];
+    acc += n[k];
+    T.end[k] = acc;
+  }
+  T.n = 6;
+  GradTiles gt{};
+  const int dims[3][2] = {{D0, H1}, {H1, H2}, {H2, A}};
+  for (int tk = 0; tk < 3; ++tk)
+    for (int k0 = 0; k0 < dims[tk][0]; k0 += kGradTK)
+      for (int j0 = 0; j0 < dims[tk][1]; j0 += kGradTJ) {
+        if (gt.n >= kMaxGradTiles) return fail(SP_EINVAL, "ddqn_update: too many gradient tiles");
+        gt.tensor[gt.n] = (uint8_t)tk;
+        gt.k0[gt.n] = (int16_t)k0;
+        gt.j0[gt.n] = (int16_t)j0;
+        ++gt.n;
+      }
+  const size_t gsm = sizeof(float) * (size_t)batch * (kGradTK + kGradTJ);
+  if (gsm > 200 * 1024) return fail(SP_EINVAL, "ddqn_update: batch too large for the gradient tiles");
+  SP_CUDA(cudaFuncSetAttribute(ddqn_grad_adam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)gsm));
+  ddqn_grad_adam_kernel<<<gt.n, 256, gsm, st>>>(la, T, gt, tiles, step_dev, lr, beta1, beta2, eps,
+                                                stats_out);
+  SP_CUDA(cudaGetLastError());
+  adam_tick_stats_kernel<<<1, 1, 0, st>>>(step_dev, stats_out);
+  SP_CUDA(cudaGetLastError());
   return SP_OK;
 }
 

@@ -1,0 +1,391 @@
+// sp_learn.cu -- one double-DQN update of the [D0, H1, H2, A] ReLU MLP in three
+// launches (the reference's ddqn.py:38-77 + net.py:63-161).
+//
+//   ddqn_rows_kernel   row-parallel, one CTA per TR-row tile of the batch.  Each
+//                      layer's weight matrix is staged whole into shared memory
+//                      with coalesced 16-byte loads (<= 133 KB), then:
+//                        targets  y = r + gamma (1-d) Q_tgt(s', argmax Q_on(s'))
+//                        forward  Q_on(s) keeping activations
+//                        Huber(1) gradient dq on q[i, a_i] (mean over B)
+//                        deltas   d2 = (dq W3^T)[z2>0], d1 = (d2 W2^T)[z1>0]
+//                      a1, a2, dq, d2, d1 go to a global scratch (B rows each).
+//   ddqn_grad_adam_kernel  the weight gradients as 32x64 GEMM tiles over the
+//                      batch (rows in order: deterministic), Adam fused into the
+//                      epilogue (adam_kernel's gated update).
+//   adam_tick_stats_kernel   advances the device Adam step when the loss is finite.
+//
+// Everything is fp32, the reference's numpy dtype, with its elementwise
+// operation order.  ReLU propagates NaN as np.maximum does, so a diverged
+// batch reaches the finite-loss gate (ddqn.py:66-71).  Matmul sums run in a
+// fixed order (k ascending), which differs from BLAS blocking in the last bits
+// only.  The tests hold this path to the torch path's bar: 1e-4 after 12
+// updates.  Parameters are the Adam tensor order of asl._adam_launch:
+// W1 W2 W3 b1 b2 b3.
+#pragma once
+#include "sp_common.cuh"
+
+namespace sp {
+
+constexpr int kLearnThreads = 256;
+constexpr int kLearnMaxD0 = 128, kLearnMaxH = 256, kLearnMaxA = 16;
+
+struct MlpDev {
+  const float* W[3];  // (D0,H1) (H1,H2) (H2,A) row-major, as net.py stores them
+  const float* b[3];
+};
+
+struct LearnArgs {
+  MlpDev on, tgt;
+  const float* s;       // (B, D0)
+  const int64_t* a;     // (B,)
+  const float* r;       // (B,)
+  const float* s2;      // (B, D0)
+  const uint8_t* d;     // (B,)
+  float *a1, *a2, *dq, *d1, *d2;  // (B,H1) (B,H2) (B,A) (B,H1) (B,H2) scratch
+  float* lpart;         // (n_tiles, 2): sum of Huber terms, sum of |td|
+  int B, D0, H1, H2, A;
+  float gamma;
+};
+
+__device__ __forceinline__ float relu_nan(float v) { return v < 0.0f ? 0.0f : v; }
+
+__host__ __device__ __forceinline__ int pad4(int n) { return (n + 3) & ~3; }
+
+// Stage a (rows x cols) row-major weight matrix global -> shared with one TMA
+// bulk copy (cp.async.bulk + mbarrier, issued by thread 0), zero-filling rows
+// rows .. pad4(rows)-1 so a k-loop unrolled by 4 needs no tail.  Every thread
+// must call it (after a barrier that retired the buffer's previous readers);
+// on return the data is visible to the whole CTA.  rows * cols % 4 == 0 and a
+// 16-byte aligned source, checked by the host.
+__device__ __forceinline__ void stage(float* dst, const float* __restrict__ src, int rows, int cols,
+                                      uint64_t* bar, uint32_t& phase) {
+  const int n = rows * cols, np = pad4(rows) * cols;
+  for (int i = n + threadIdx.x; i < np; i += blockDim.x) dst[i] = 0.0f;
+  if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic writes
+    mbar_expect_tx(bar, (uint32_t)n * 4u);
+    tma_bulk_g2s(dst, src, (uint32_t)n * 4u, bar);
+  }
+  mbar_wait(bar, phase);
+  phase ^= 1u;
+  __syncthreads();  // the zero-filled pad rows
+}
+
+template <int TR>
+__host__ __device__ __forceinline__ int learn_part_floats(int L0, int H1, int H2) {
+  // split-K partials of a dense layer: splits * TR * n_out <= 4 * threads * TR
+  (void)L0; (void)H1; (void)H2;
+  return 4 * kLearnThreads * TR;
+}
+
+// y[r][j] = b[j] + sum_k x[r][k] Ws[k][j] (Ws staged in SMEM) for the TR rows.
+// n_out % 4 == 0: thread = (4-column quad, k-split).  Each thread reads each of
+// its weights once (float4) and applies it to all TR rows (x rows read as
+// float4, broadcast across the warp), so shared-memory traffic is one weight
+// word per TR FMAs.  The k-split partials meet in `part` and are summed in
+// split order (deterministic).  n_in is the padded row stride of x (% 4 == 0).
+// Otherwise (the A-wide output layer) one thread per (row, column).
+template <int TR>
+__device__ __forceinline__ void dense_smem(const float* Ws, const float* __restrict__ bias,
+                                           const float* x, int n_in, int n_out, float* y, float* z,
+                                           bool relu, float* part) {
+  if ((n_out & 3) == 0) {
+    const int quads = n_out >> 2;
+    const int splits = max(1, min((int)blockDim.x / quads, n_in >> 2));
+    const int kq = ((n_in >> 2) + splits - 1) / splits;  // k-quads per split
+    for (int t = threadIdx.x; t < quads * splits; t += blockDim.x) {
+      const int jq = t % quads, sp = t / quads;
+      const int kb = 4 * sp * kq, ke = min(n_in, kb + 4 * kq);
+      float acc[TR][4];
+#pragma unroll
+      for (int q = 0; q < TR; ++q)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[q][c] = 0.0f;
+      for (int k = kb; k < ke; k += 4) {
+        float4 w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) w[u] = *(const float4*)(Ws + (k + u) * n_out + 4 * jq);
+#pragma unroll
+        for (int q = 0; q < TR; ++q) {
+          const float4 xv = *(const float4*)(x + q * n_in + k);
+          const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            acc[q][0] = fmaf(xs[u], w[u].x, acc[q][0]);
+            acc[q][1] = fmaf(xs[u], w[u].y, acc[q][1]);
+            acc[q][2] = fmaf(xs[u], w[u].z, acc[q][2]);
+            acc[q][3] = fmaf(xs[u], w[u].w, acc[q][3]);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < TR; ++q)
+        *(float4*)(part + (sp * TR + q) * n_out + 4 * jq) =
+            make_float4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
+    }
+    __syncthreads();
+    const int stride = TR * n_out;
+    for (int e = threadIdx.x; e < stride; e += blockDim.x) {
+      const int j = (n_out & (n_out - 1)) == 0 ? (e & (n_out - 1)) : e % n_out;
+      float v = part[e];
+      for (int sp = 1; sp < splits; ++sp) v += part[sp * stride + e];
+      v += bias[j];  // x @ W + b (net.py:63-74)
+      if (z) z[e] = v;
+      y[e] = relu ? relu_nan(v) : v;
+    }
+    return;
+  }
+  for (int t = threadIdx.x; t < TR * n_out; t += blockDim.x) {
+    const int r = t / n_out, jj = t - r * n_out;
+    float acc = 0.0f;
+    for (int k = 0; k < n_in; ++k) acc = fmaf(x[r * n_in + k], Ws[k * n_out + jj], acc);
+    const float v = acc + bias[jj];
+    if (z) z[r * n_out + jj] = v;
+    y[r * n_out + jj] = relu ? relu_nan(v) : v;
+  }
+}
+
+template <int TR>
+__device__ __forceinline__ void mlp_forward(const MlpDev& m, const float* x, float* h1, float* h2,
+                                            float* q, float* z1, float* z2, float* wbuf,
+                                            float* part, uint64_t* bar, uint32_t& phase,
+                                            const LearnArgs& a) {
+  stage(wbuf, m.W[0], a.D0, a.H1, bar, phase);
+  dense_smem<TR>(wbuf, m.b[0], x, pad4(a.D0), a.H1, h1, z1, true, part);
+  __syncthreads();
+  stage(wbuf, m.W[1], a.H1, a.H2, bar, phase);
+  dense_smem<TR>(wbuf, m.b[1], h1, a.H1, a.H2, h2, z2, true, part);
+  __syncthreads();
+  stage(wbuf, m.W[2], a.H2, a.A, bar, phase);
+  dense_smem<TR>(wbuf, m.b[2], h2, a.H2, a.A, q, nullptr, false, part);
+  __syncthreads();
+}
+
+template <int TR>
+__global__ void __launch_bounds__(kLearnThreads)
+    ddqn_rows_kernel(const __grid_constant__ LearnArgs a) {
+  extern __shared__ __align__(16) float sm[];
+  const int D0 = a.D0, H1 = a.H1, H2 = a.H2, A = a.A, L0 = pad4(D0);
+  const int wmax = max(max(L0 * H1, H1 * H2), pad4(H2) * A);
+  float* wbuf = sm;                          // staged weights
+  float* part = wbuf + pad4(wmax);           // split-K partials (learn_part_floats)
+  float* xs = part + learn_part_floats<TR>(L0, H1, H2);  // TR x L0  s rows (zero-padded)
+  float* xs2 = xs + TR * L0;                 // TR x L0   s' rows
+  float* h1 = xs2 + TR * L0;                 // TR x H1
+  float* h2 = h1 + TR * H1;                  // TR x H2
+  float* z1 = h2 + TR * H2;                  // TR x H1   online(s) pre-activations
+  float* z2 = z1 + TR * H1;                  // TR x H2
+  float* q = z2 + TR * H2;                   // TR x A
+  float* dq = q + TR * A;                    // TR x A
+  float* d2 = dq + TR * A;                   // TR x H2
+  float* y = d2 + TR * H2;                   // TR
+  float* red = y + TR;                       // 2 x TR
+  uint64_t* bar = (uint64_t*)(sm + pad4((int)(red + 2 * TR - sm)));  // 16-byte aligned
+  uint32_t phase = 0;
+  if (threadIdx.x == 0) mbar_init(bar, 1);
+  const int row0 = blockIdx.x * TR;
+  for (int i = threadIdx.x; i < TR * L0; i += blockDim.x) {
+    const int r = i / L0, k = i - r * L0;
+    xs[i] = k < D0 ? a.s[(size_t)(row0 + r) * D0 + k] : 0.0f;
+    xs2[i] = k < D0 ? a.s2[(size_t)(row0 + r) * D0 + k] : 0.0f;
+  }
+  __syncthreads();
+  // ---- targets (ddqn.py:38-51): argmax of the online net, value of the target net
+  mlp_forward<TR>(a.on, xs2, h1, h2, q, nullptr, nullptr, wbuf, part, bar, phase, a);
+  if (threadIdx.x < TR) {
+    const int r = threadIdx.x;
+    int best = 0;
+    for (int j = 1; j < A; ++j)
+      if (q[r * A + j] > q[r * A + best]) best = j;  // first max, as np.argmax
+    y[r] = (float)best;
+  }
+  __syncthreads();
+  mlp_forward<TR>(a.tgt, xs2, h1, h2, q, nullptr, nullptr, wbuf, part, bar, phase, a);
+  if (threadIdx.x < TR) {
+    const int r = threadIdx.x;
+    const float boot = q[r * A + (int)y[r]];
+    const float nd = a.d[row0 + r] ? 0.0f : 1.0f;
+    y[r] = __fadd_rn(a.r[row0 + r], __fmul_rn(__fmul_rn(a.gamma, nd), boot));
+  }
+  __syncthreads();
+  // ---- online forward on s, cached (net.py:63-74); W3 stays staged below
+  mlp_forward<TR>(a.on, xs, h1, h2, q, z1, z2, wbuf, part, bar, phase, a);
+  // ---- Huber(1) on q[r, a_r] - y_r (net.py:83-115): mean over the batch
+  if (threadIdx.x < TR) {
+    const int r = threadIdx.x;
+    const int act = (int)a.a[row0 + r];
+    const float res = __fsub_rn(q[r * A + act], y[r]);
+    const float ab = fabsf(res);
+    red[r] = ab <= 1.0f ? __fmul_rn(__fmul_rn(0.5f, res), res) : __fsub_rn(ab, 0.5f);
+    red[TR + r] = ab;
+    const float g = __fdiv_rn(fminf(fmaxf(res, -1.0f), 1.0f), (float)a.B);
+    for (int j = 0; j < A; ++j) dq[r * A + j] = j == act ? g : 0.0f;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float l = 0.0f, m = 0.0f;
+    for (int r = 0; r < TR; ++r) {
+      l += red[r];
+      m += red[TR + r];
+    }
+    a.lpart[blockIdx.x * 2] = l;
+    a.lpart[blockIdx.x * 2 + 1] = m;
+  }
+  // activations and dq for the parameter-parallel gradient kernel
+  for (int i = threadIdx.x; i < TR * H1; i += blockDim.x) a.a1[(size_t)row0 * H1 + i] = h1[i];
+  for (int i = threadIdx.x; i < TR * H2; i += blockDim.x) a.a2[(size_t)row0 * H2 + i] = h2[i];
+  for (int i = threadIdx.x; i < TR * A; i += blockDim.x) a.dq[(size_t)row0 * A + i] = dq[i];
+  // ---- d2 = (dq W3^T) * [z2 > 0]   (W3 is still staged in wbuf)
+  for (int e = threadIdx.x; e < TR * H2; e += blockDim.x) {
+    const int r = e / H2, k = e - r * H2;
+    float acc = 0.0f;
+    for (int j = 0; j < A; ++j) acc = fmaf(dq[r * A + j], wbuf[k * A + j], acc);
+    const float v = z2[e] > 0.0f ? acc : 0.0f;
+    d2[e] = v;
+    a.d2[(size_t)row0 * H2 + e] = v;
+  }
+  __syncthreads();
+  // ---- d1 = (d2 W2^T) * [z1 > 0]: W2 re-staged; thread k walks row k starting
+  // at column k (rotated), so a warp's 32 rows hit 32 different banks
+  __syncthreads();
+  stage(wbuf, a.on.W[1], H1, H2, bar, phase);
+  for (int k = threadIdx.x; k < H1; k += blockDim.x) {
+    float acc[TR];
+#pragma unroll
+    for (int r = 0; r < TR; ++r) acc[r] = 0.0f;
+    const float* wrow = wbuf + k * H2;
+    int j = k % H2;
+    for (int jj = 0; jj < H2; ++jj) {
+      const float w = wrow[j];
+#pragma unroll
+      for (int r = 0; r < TR; ++r) acc[r] = fmaf(d2[r * H2 + j], w, acc[r]);
+      j = j + 1 == H2 ? 0 : j + 1;
+    }
+#pragma unroll
+    for (int r = 0; r < TR; ++r)
+      a.d1[(size_t)(row0 + r) * H1 + k] = z1[r * H1 + k] > 0.0f ? acc[r] : 0.0f;
+  }
+}
+
+// Weight gradients as small GEMMs over the batch, Adam fused into the epilogue.
+// A CTA owns a 16 (fan_in) x 32 (fan_out) tile of one weight matrix:
+//   gW[k][j] = sum_r act[r][k] del[r][j]   (W1: s, d1; W2: a1, d2; W3: a2, dq)
+// with the tile's columns of all B rows staged in shared memory (B x 48 floats);
+// each thread owns 1 x 2 outputs.  Tiles at k0 == 0 also own the bias gradient sum_r del[r][j].
+// The sums run in row order (deterministic).  Then adam_kernel's update
+// (net.py:141-161), gated on a finite loss (ddqn.py:66-71).  CTA 0 publishes
+// {loss, mean |td|}.
+constexpr int kGradTK = 16, kGradTJ = 32, kMaxGradTiles = 256;
+
+struct GradTiles {
+  int n;
+  uint8_t tensor[kMaxGradTiles];  // 0..2: W1 W2 W3
+  int16_t k0[kMaxGradTiles], j0[kMaxGradTiles];
+};
+
+__device__ __forceinline__ void adam_one(const AdamTensors& T, int k, int64_t e, float g,
+                                         float c1, float c2, float fb1, float fb2, float f1b1,
+                                         float f1b2, float flr, float feps) {
+  const float mm = __fadd_rn(__fmul_rn(T.m[k][e], fb1), __fmul_rn(f1b1, g));
+  const float vv = __fadd_rn(__fmul_rn(T.v[k][e], fb2), __fmul_rn(f1b2, __fmul_rn(g, g)));
+  T.m[k][e] = mm;
+  T.v[k][e] = vv;
+  const float upd = __fdiv_rn(__fmul_rn(flr, __fdiv_rn(mm, c1)),
+                              __fadd_rn(__fsqrt_rn(__fdiv_rn(vv, c2)), feps));
+  T.p[k][e] = __fsub_rn(T.p[k][e], upd);
+}
+
+__global__ void __launch_bounds__(256)
+    ddqn_grad_adam_kernel(const __grid_constant__ LearnArgs la,
+                          const __grid_constant__ AdamTensors T,
+                          const __grid_constant__ GradTiles tiles, int n_row_tiles,
+                          const double* step_dev, double lr, double b1, double b2, double eps,
+                          float* stats_out) {
+  extern __shared__ __align__(16) float gsm[];  // As: B x kGradTK, Ds: B x kGradTJ
+  float l = 0.0f, m = 0.0f;
+  for (int t = 0; t < n_row_tiles; ++t) {
+    l += la.lpart[2 * t];
+    m += la.lpart[2 * t + 1];
+  }
+  const float loss = l / (float)la.B, mad = m / (float)la.B;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    stats_out[0] = loss;
+    stats_out[1] = mad;
+  }
+  if (!isfinite(loss)) return;  // uniform across the grid
+  const int tk = tiles.tensor[blockIdx.x], k0 = tiles.k0[blockIdx.x], j0 = tiles.j0[blockIdx.x];
+  const float* act = tk == 0 ? la.s : tk == 1 ? la.a1 : la.a2;
+  const float* del = tk == 0 ? la.d1 : tk == 1 ? la.d2 : la.dq;
+  const int K = tk == 0 ? la.D0 : tk == 1 ? la.H1 : la.H2;
+  const int J = tk == 0 ? la.H1 : tk == 1 ? la.H2 : la.A;
+  const int kk = threadIdx.x >> 4, jp = threadIdx.x & 15;  // outputs (k0+kk, j0+2jp+{0,1})
+  float acc[2] = {0.f, 0.f};
+  float bacc[2] = {0.f, 0.f};
+  const bool bias_owner = k0 == 0 && kk == 0;
+  // the tile's columns of every batch row, staged once (many loads in flight)
+  float* As = gsm;
+  float* Ds = gsm + (size_t)la.B * kGradTK;
+  for (int i = threadIdx.x; i < la.B * kGradTK; i += blockDim.x) {
+    const int r = i / kGradTK, c = i % kGradTK;
+    As[i] = k0 + c < K ? act[(size_t)r * K + k0 + c] : 0.0f;
+  }
+  if ((J & 3) == 0 && (j0 & 3) == 0) {
+    for (int i = threadIdx.x; i < la.B * (kGradTJ / 4); i += blockDim.x) {
+      const int r = i / (kGradTJ / 4), c = 4 * (i % (kGradTJ / 4));
+      *(float4*)&Ds[r * kGradTJ + c] = j0 + c < J ? *(const float4*)&del[(size_t)r * J + j0 + c]
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  } else {
+    for (int i = threadIdx.x; i < la.B * kGradTJ; i += blockDim.x) {
+      const int r = i / kGradTJ, c = i % kGradTJ;
+      Ds[i] = j0 + c < J ? del[(size_t)r * J + j0 + c] : 0.0f;
+    }
+  }
+  __syncthreads();
+#pragma unroll 8
+  for (int r = 0; r < la.B; ++r) {
+    const float xv = As[r * kGradTK + kk];
+    const float2 dv = *(const float2*)&Ds[r * kGradTJ + 2 * jp];
+    acc[0] = fmaf(xv, dv.x, acc[0]);
+    acc[1] = fmaf(xv, dv.y, acc[1]);
+    if (bias_owner) {
+      bacc[0] += dv.x;
+      bacc[1] += dv.y;
+    }
+  }
+  const double t = *step_dev + 1.0;
+  const float c1 = (float)(1.0 - pow(b1, t));
+  const float c2 = (float)(1.0 - pow(b2, t));
+  const float fb1 = (float)b1, fb2 = (float)b2, f1b1 = (float)(1.0 - b1),
+              f1b2 = (float)(1.0 - b2), flr = (float)lr, feps = (float)eps;
+  const int k = k0 + kk;
+  if (k < K) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int j = j0 + 2 * jp + c;
+      if (j < J) adam_one(T, tk, (int64_t)k * J + j, acc[c], c1, c2, fb1, fb2, f1b1, f1b2, flr, feps);
+    }
+  }
+  if (bias_owner) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int j = j0 + 2 * jp + c;
+      if (j < J) adam_one(T, tk + 3, j, bacc[c], c1, c2, fb1, fb2, f1b1, f1b2, flr, feps);
+    }
+  }
+}
+
+__global__ void adam_tick_stats_kernel(double* step_dev, const float* stats) {
+  if (isfinite(stats[0])) *step_dev += 1.0;
+}
+
+template <int TR>
+size_t learn_smem_bytes(int D0, int H1, int H2, int A) {
+  const int L0 = pad4(D0);
+  const int wmax = std::max(std::max(L0 * H1, H1 * H2), pad4(H2) * A);
+  const size_t floats = (size_t)pad4(wmax) + learn_part_floats<TR>(L0, H1, H2) +
+                        (size_t)TR * (2 * L0 + 2 * H1 + 3 * H2 + 2 * A + 1) + 2 * TR;
+  return sizeof(float) * (size_t)pad4((int)floats) + 16;
+}
+
+}  // namespace sp

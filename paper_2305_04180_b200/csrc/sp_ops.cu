@@ -140,6 +140,10 @@ __global__ void rb_append_kernel(float* __restrict__ rs, int64_t* __restrict__ r
   }
 }
 
+// One warp per sampled row (8 rows per CTA): every lane draws the row's index
+// (Philox block ctr + i of (seed, stream_id, tag 2), replay.py:76), then the
+// lanes copy its columns coalesced.  All rows' random ring reads are in flight
+// at once instead of one thread walking a row serially.
 __global__ void rb_sample_kernel(const float* __restrict__ rs, const int64_t* __restrict__ ra,
                                  const float* __restrict__ rr, const float* __restrict__ rs2,
                                  const uint8_t* __restrict__ rd, int32_t dim, int64_t size,
@@ -147,26 +151,24 @@ __global__ void rb_sample_kernel(const float* __restrict__ rs, const int64_t* __
                                  float* __restrict__ s, int64_t* __restrict__ a,
                                  float* __restrict__ r, float* __restrict__ s2,
                                  uint8_t* __restrict__ dn, int64_t* __restrict__ idx_out) {
-  __shared__ int64_t idx[256];
-  const int64_t i0 = (int64_t)blockIdx.x * 256;
-  const int nb = (int)min((int64_t)256, batch - i0);
-  if ((int)threadIdx.x < nb) {
-    const int64_t i = i0 + threadIdx.x;
-    const Block4 b = stream_block(seed, stream_id, 2u, ctr + (uint64_t)i);
-    const int64_t k = draw_integer(b, 0, size);  // replay.py:76
-    idx[threadIdx.x] = k;
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= batch) return;
+  const Block4 b = stream_block(seed, stream_id, 2u, ctr + (uint64_t)i);
+  const int64_t k = draw_integer(b, 0, size);
+  if (lane == 0) {
     a[i] = ra[k];
     r[i] = rr[k];
     dn[i] = rd[k];
     if (idx_out) idx_out[i] = k;
   }
-  __syncthreads();
-  const int64_t flat = (int64_t)nb * dim;
-  for (int64_t f = threadIdx.x; f < flat; f += blockDim.x) {
-    const int64_t row = f / dim, c = f - row * dim;
-    const int64_t src = idx[row] * dim + c;
-    s[(i0 + row) * dim + c] = rs[src];
-    s2[(i0 + row) * dim + c] = rs2[src];
+  const float* src = rs + k * dim;
+  const float* src2 = rs2 + k * dim;
+  float* dst = s + i * dim;
+  float* dst2 = s2 + i * dim;
+  for (int c = lane; c < dim; c += 32) {
+    dst[c] = src[c];
+    dst2[c] = src2[c];
   }
 }
 

@@ -14,7 +14,7 @@ HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))
 def declared_symbols():
     text = open(HEADER).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(sp_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int64_t|int|const char\*)\s+(sp_\w+)\s*\(", text, flags=re.M)))
 
 
 def test_header_declares_the_boundary():
@@ -45,7 +45,7 @@ def test_struct_layouts_match_header(tmp_path):
         pytest.skip("gcc not available")
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "sparrow.h"', "int main(){"]
     expect = []
-    for cls in (_lib.SpConfig, _lib.SpMapDesc, _lib.SpRanges):
+    for cls in (_lib.SpConfig, _lib.SpMapDesc, _lib.SpRanges, _lib.SpMlp):
         name = cls.__name__
         lines.append(f'printf("%zu\\n", sizeof({name}));')
         expect.append(ctypes.sizeof(cls))

@@ -25,7 +25,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 N, TPS, B, CAP, LEARN_START, UPLOAD = 4096, 256.0, 256, 1_000_000, 30_000, 50
 
 
-def run_ours(seconds, eager=False):
+def run_ours(seconds, eager=False, learner="fused"):
     import torch
     from helpers import config, load_maps, ranges
     from paper_2305_04180_b200 import ReplayBuffer, VecEnv
@@ -34,7 +34,7 @@ def run_ours(seconds, eager=False):
     env = VecEnv(load_maps(16), N, ranges(0.3), config(32), check_actions=False)
     states = env.reset_all(0)
     algo = DdqnLearner(QNet.init(np.random.default_rng(0), (37, 256, 128, 5)), DdqnConfig(),
-                       graph=not eager)
+                       graph=not eager, fused=learner == "fused")
     sharer = Sharer(ReplayBuffer(CAP, 37))
     tfm = TfmConfig(N, TPS, B)
     t0 = time.perf_counter()
@@ -86,16 +86,19 @@ def main():
     ap.add_argument("--seconds", type=float, default=20.0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--eager", action="store_true", help="learner updates without CUDA graph")
+    ap.add_argument("--learner", default="fused", choices=["fused", "torch"],
+                    help="fused sp_ddqn_update kernels or the torch update")
     a = ap.parse_args()
     if a.impl == "ours":
-        sharer, wall = run_ours(a.seconds, a.eager)
+        sharer, wall = run_ours(a.seconds, a.eager, a.learner)
     else:
         sharer, wall = run_reference(a.seconds)
     tfm = sharer.tfm
     print(json.dumps({
         "workload": "cfg5: 4096 envs (16 maps, diversity 0.3, 32 beams) -> 1M replay -> "
                     "batch-256 DDQN [37,256,128,5], TPS 256 (rho 4096), learn_start 30000",
-        "impl": a.impl, "graph": a.impl == "ours" and not a.eager, "wall_s": wall, "t_step": sharer.t_step, "b_step": sharer.b_step,
+        "impl": a.impl, "graph": a.impl == "ours" and not a.eager,
+        "learner": a.learner if a.impl == "ours" else "reference numpy", "wall_s": wall, "t_step": sharer.t_step, "b_step": sharer.b_step,
         "env_steps_per_s": sharer.t_step / wall, "updates_per_s": sharer.b_step / wall,
         "measured_tps": sharer.measured_tps(B),
         "actor_period_ms": None if tfm.v_period_s is None else tfm.v_period_s * 1e3,

@@ -19,7 +19,7 @@ sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."
 B, D, CAP = 256, 37, 1_000_000
 
 
-def run_ours(updates, graph):
+def run_ours(updates, graph, fused=False):
     import torch
     from paper_2305_04180_b200 import PhiloxGenerator, ReplayBuffer
     from paper_2305_04180_b200.asl import DdqnLearner, QNet
@@ -32,7 +32,8 @@ def run_ours(updates, graph):
                      torch.randn(n, device=dev, generator=g),
                      torch.randn((n, D), device=dev, generator=g),
                      torch.rand(n, device=dev, generator=g) < 0.05)
-    algo = DdqnLearner(QNet.init(np.random.default_rng(0), (D, 256, 128, 5)), graph=graph)
+    algo = DdqnLearner(QNet.init(np.random.default_rng(0), (D, 256, 128, 5)), graph=graph,
+                       fused=fused)
     rng = PhiloxGenerator(1)
 
     def one():
@@ -47,7 +48,8 @@ def run_ours(updates, graph):
         one()
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    return {"impl": "ours", "graph": graph, "updates": updates, "updates_per_s": updates / dt,
+    return {"impl": "ours", "graph": graph, "fused": fused, "updates": updates,
+            "updates_per_s": updates / dt,
             "ms_per_update": dt / updates * 1e3}
 
 
@@ -78,8 +80,8 @@ def main():
     ap.add_argument("--updates", type=int, default=2000)
     ap.add_argument("--reference-updates", type=int, default=300)
     a = ap.parse_args()
-    for graph in (False, True):
-        print(json.dumps(run_ours(a.updates, graph)), flush=True)
+    for graph, fused in ((False, False), (True, False), (False, True), (True, True)):
+        print(json.dumps(run_ours(a.updates, graph, fused)), flush=True)
     print(json.dumps(run_reference(a.reference_updates)), flush=True)
 
 
