@@ -196,7 +196,8 @@ typedef struct SpMlp {
   float* b[3];
 } SpMlp;
 
-/* scratch (floats) sp_ddqn_update needs for a batch of `batch` rows */
+/* scratch (floats) sp_ddqn_update needs for a batch of `batch` rows, or -1 when the
+ * layer sizes / batch exceed the fused kernels (shared-memory staging limits) */
 int64_t sp_ddqn_scratch_floats(const int32_t* sizes, int64_t batch);
 /* One double-DQN update in three launches (row-parallel forward/deltas,
  * parameter-parallel gradient + gated Adam, step tick); replaces ddqn.py:54-77 (DdqnLearner.
@@ -206,7 +207,9 @@ int64_t sp_ddqn_scratch_floats(const int32_t* sizes, int64_t batch);
  * Adam step count (incremented on device when the update applies).  The update
  * applies only if the loss is finite (ddqn.py:66-71); stats_out (device, 2 f32)
  * receives {mean Huber loss, mean |td|}.  Requires D0 <= 128, H1, H2 <= 256,
- * A <= 16 and 16-byte aligned weights.  The target net is read only. */
+ * A <= 16, 16-byte aligned weights and sp_ddqn_scratch_floats(...) >= 0 (the
+ * three staged weight matrices fit in shared memory: e.g. [32|37,256,128,5]).
+ * The target net is read only. */
 int sp_ddqn_update(const SpMlp* online, const SpMlp* target, const float* s, const int64_t* a,
                    const float* r, const float* s2, const uint8_t* d, int64_t batch, float gamma,
                    float* const* m, float* const* v, double* step_dev, double lr, double beta1,

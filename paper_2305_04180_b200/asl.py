@@ -367,9 +367,6 @@ class _FusedUpdate:
         on, tg, ad = learner.online, learner.target, learner.adam
         if len(on.weights) != 3:
             raise ValueError("the fused learner kernel supports the 3-layer Q-net only")
-        if batch_size * (16 + 32) * 4 > 200 * 1024:
-            raise ValueError("fused learner: batch > 1066 rows exceeds the gradient-tile staging; "
-                             "use graph=True without fused")
         dev = on.weights[0].device
         b, d = int(batch_size), int(state_dim)
         self.batch_size, self.state_dim = b, d
@@ -384,7 +381,8 @@ class _FusedUpdate:
         sizes = (ctypes.c_int32 * 4)(*on.sizes)
         n = int(self._lib.sp_ddqn_scratch_floats(sizes, b))
         if n < 0:
-            raise ValueError("bad learner shapes")
+            raise ValueError(f"Q-net {on.sizes} with batch {b} exceeds the fused learner kernels' "
+                             "shared memory; use graph=True without fused")
         self.scratch = torch.empty(n, dtype=torch.float32, device=dev)
         for t in on.weights + on.biases + tg.weights + tg.biases:
             if not t.is_contiguous() or t.dtype != torch.float32:

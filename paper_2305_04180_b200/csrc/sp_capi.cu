@@ -993,8 +993,18 @@ int sp_adam_step(int n_tensors, float* const* params, const float* const* grads,
 
 static int learn_tr(int64_t batch) { return batch % 4 == 0 ? 4 : 1; }
 
+static size_t ddqn_rows_smem(const int32_t* sz, int64_t batch) {
+  return learn_tr(batch) == 4 ? learn_smem_bytes<4>(sz[0], sz[1], sz[2], sz[3])
+                              : learn_smem_bytes<1>(sz[0], sz[1], sz[2], sz[3]);
+}
+
 int64_t sp_ddqn_scratch_floats(const int32_t* sz, int64_t batch) {
   if (!sz || batch < 1) return -1;
+  // the fused kernels' limits (shared memory for the staged layers, tiles)
+  if (sz[0] < 1 || sz[0] > kLearnMaxD0 || sz[1] < 1 || sz[1] > kLearnMaxH || sz[2] < 1 ||
+      sz[2] > kLearnMaxH || sz[3] < 1 || sz[3] > kLearnMaxA || ddqn_rows_smem(sz, batch) > 227 * 1024 ||
+      (size_t)batch * (kGradTK + kGradTJ) * 4 > 200 * 1024)
+    return -1;
   const int64_t tiles = batch / learn_tr(batch);
   // a1, d1 (B x H1), a2, d2 (B x H2), dq (B x A), loss partials (tiles x 2)
   return batch * (2 * (int64_t)sz[1] + 2 * (int64_t)sz[2] + sz[3]) + 2 * tiles;
@@ -1020,6 +1030,7 @@ int sp_ddqn_update(const SpMlp* on, const SpMlp* tg, const float* s, const int64
     return fail(SP_EINVAL, "ddqn_update: each weight matrix must hold a multiple of 4 floats");
   if (batch < 1 || batch > (1 << 24)) return fail(SP_EINVAL, "ddqn_update: bad batch size");
   const int64_t need = sp_ddqn_scratch_floats(on->sizes, batch);
+  if (need < 0) return fail(SP_EINVAL, "ddqn_update: layer sizes / batch exceed the fused kernels");
   if (scratch_floats < need) return fail(SP_EINVAL, "ddqn_update: scratch too small");
   const int TR = learn_tr(batch);
   const int tiles = (int)(batch / TR);

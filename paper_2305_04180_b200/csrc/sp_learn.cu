@@ -1,9 +1,9 @@
 // sp_learn.cu -- one double-DQN update of the [D0, H1, H2, A] ReLU MLP in three
 // launches (the reference's ddqn.py:38-77 + net.py:63-161).
 //
-//   ddqn_rows_kernel   row-parallel, one CTA per TR-row tile of the batch.  Each
-//                      layer's weight matrix is staged whole into shared memory
-//                      with coalesced 16-byte loads (<= 133 KB), then:
+//   ddqn_rows_kernel   row-parallel, one CTA per TR-row tile of the batch.  The
+//                      weights are staged per layer into shared memory by TMA
+//                      bulk copies, triple-buffered (W1 | W2 | W3), then:
 //                        targets  y = r + gamma (1-d) Q_tgt(s', argmax Q_on(s'))
 //                        forward  Q_on(s) keeping activations
 //                        Huber(1) gradient dq on q[i, a_i] (mean over B)
@@ -51,25 +51,30 @@ __device__ __forceinline__ float relu_nan(float v) { return v < 0.0f ? 0.0f : v;
 
 __host__ __device__ __forceinline__ int pad4(int n) { return (n + 3) & ~3; }
 
-// Stage a (rows x cols) row-major weight matrix global -> shared with one TMA
-// bulk copy (cp.async.bulk + mbarrier, issued by thread 0), zero-filling rows
-// rows .. pad4(rows)-1 so a k-loop unrolled by 4 needs no tail.  Every thread
-// must call it (after a barrier that retired the buffer's previous readers);
-// on return the data is visible to the whole CTA.  rows * cols % 4 == 0 and a
-// 16-byte aligned source, checked by the host.
-__device__ __forceinline__ void stage(float* dst, const float* __restrict__ src, int rows, int cols,
-                                      uint64_t* bar, uint32_t& phase) {
-  const int n = rows * cols, np = pad4(rows) * cols;
-  for (int i = n + threadIdx.x; i < np; i += blockDim.x) dst[i] = 0.0f;
-  if (threadIdx.x == 0) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic writes
-    mbar_expect_tx(bar, (uint32_t)n * 4u);
-    tma_bulk_g2s(dst, src, (uint32_t)n * 4u, bar);
+// Weight staging, triple-buffered: one shared-memory buffer (and mbarrier)
+// per layer, each filled by a single TMA bulk copy (cp.async.bulk, issued by
+// thread 0).  Because each layer always uses its own buffer, the next pass's
+// layer-l weights stream in as soon as this pass's layer l is done, behind
+// the other layers' math.  The online net's W2/W3 stay resident after the
+// last pass for the backward.  W1's buffer holds pad4(D0) rows; the pad rows
+// are zeroed once and never written by the copies.
+struct Stager {
+  float* buf[3];
+  uint64_t* bar[3];
+  uint32_t phase[3];
+
+  // thread 0 only; the buffer's previous readers must have passed a barrier
+  __device__ __forceinline__ void issue(int l, const float* src, int n_floats) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(bar[l], (uint32_t)n_floats * 4u);
+    tma_bulk_g2s(buf[l], src, (uint32_t)n_floats * 4u, bar[l]);
   }
-  mbar_wait(bar, phase);
-  phase ^= 1u;
-  __syncthreads();  // the zero-filled pad rows
-}
+  // every thread
+  __device__ __forceinline__ void wait(int l) {
+    mbar_wait(bar[l], phase[l]);
+    phase[l] ^= 1u;
+  }
+};
 
 template <int TR>
 __host__ __device__ __forceinline__ int learn_part_floats(int L0, int H1, int H2) {
@@ -145,20 +150,26 @@ __device__ __forceinline__ void dense_smem(const float* Ws, const float* __restr
   }
 }
 
+// One forward pass over the TR rows.  `next` (nullable): the net of the next
+// pass, whose layer-l weights are issued into buffer l right after this pass
+// has finished layer l.
 template <int TR>
-__device__ __forceinline__ void mlp_forward(const MlpDev& m, const float* x, float* h1, float* h2,
-                                            float* q, float* z1, float* z2, float* wbuf,
-                                            float* part, uint64_t* bar, uint32_t& phase,
-                                            const LearnArgs& a) {
-  stage(wbuf, m.W[0], a.D0, a.H1, bar, phase);
-  dense_smem<TR>(wbuf, m.b[0], x, pad4(a.D0), a.H1, h1, z1, true, part);
+__device__ __forceinline__ void mlp_forward(const MlpDev& m, const MlpDev* next, const float* x,
+                                            float* h1, float* h2, float* q, float* z1, float* z2,
+                                            Stager& st, float* part, const LearnArgs& a) {
+  const int n[3] = {a.D0 * a.H1, a.H1 * a.H2, a.H2 * a.A};
+  st.wait(0);
+  dense_smem<TR>(st.buf[0], m.b[0], x, pad4(a.D0), a.H1, h1, z1, true, part);
   __syncthreads();
-  stage(wbuf, m.W[1], a.H1, a.H2, bar, phase);
-  dense_smem<TR>(wbuf, m.b[1], h1, a.H1, a.H2, h2, z2, true, part);
+  if (next && threadIdx.x == 0) st.issue(0, next->W[0], n[0]);
+  st.wait(1);
+  dense_smem<TR>(st.buf[1], m.b[1], h1, a.H1, a.H2, h2, z2, true, part);
   __syncthreads();
-  stage(wbuf, m.W[2], a.H2, a.A, bar, phase);
-  dense_smem<TR>(wbuf, m.b[2], h2, a.H2, a.A, q, nullptr, false, part);
+  if (next && threadIdx.x == 0) st.issue(1, next->W[1], n[1]);
+  st.wait(2);
+  dense_smem<TR>(st.buf[2], m.b[2], h2, a.H2, a.A, q, nullptr, false, part);
   __syncthreads();
+  if (next && threadIdx.x == 0) st.issue(2, next->W[2], n[2]);
 }
 
 template <int TR>
@@ -166,9 +177,11 @@ __global__ void __launch_bounds__(kLearnThreads)
     ddqn_rows_kernel(const __grid_constant__ LearnArgs a) {
   extern __shared__ __align__(16) float sm[];
   const int D0 = a.D0, H1 = a.H1, H2 = a.H2, A = a.A, L0 = pad4(D0);
-  const int wmax = max(max(L0 * H1, H1 * H2), pad4(H2) * A);
-  float* wbuf = sm;                          // staged weights
-  float* part = wbuf + pad4(wmax);           // split-K partials (learn_part_floats)
+  Stager st;
+  st.buf[0] = sm;                                  // W1: pad4(D0) x H1
+  st.buf[1] = st.buf[0] + pad4(L0 * H1);           // W2: H1 x H2
+  st.buf[2] = st.buf[1] + pad4(H1 * H2);           // W3: H2 x A
+  float* part = st.buf[2] + pad4(H2 * A);          // split-K partials (learn_part_floats)
   float* xs = part + learn_part_floats<TR>(L0, H1, H2);  // TR x L0  s rows (zero-padded)
   float* xs2 = xs + TR * L0;                 // TR x L0   s' rows
   float* h1 = xs2 + TR * L0;                 // TR x H1
@@ -180,9 +193,18 @@ __global__ void __launch_bounds__(kLearnThreads)
   float* d2 = dq + TR * A;                   // TR x H2
   float* y = d2 + TR * H2;                   // TR
   float* red = y + TR;                       // 2 x TR
-  uint64_t* bar = (uint64_t*)(sm + pad4((int)(red + 2 * TR - sm)));  // 16-byte aligned
-  uint32_t phase = 0;
-  if (threadIdx.x == 0) mbar_init(bar, 1);
+  uint64_t* bars = (uint64_t*)(sm + pad4((int)(red + 2 * TR - sm)));  // 16-byte aligned
+  for (int l = 0; l < 3; ++l) {
+    st.bar[l] = bars + l;
+    st.phase[l] = 0;
+  }
+  for (int i = D0 * H1 + threadIdx.x; i < L0 * H1; i += blockDim.x) st.buf[0][i] = 0.0f;
+  if (threadIdx.x == 0) {
+    for (int l = 0; l < 3; ++l) mbar_init(st.bar[l], 1);
+    st.issue(0, a.on.W[0], D0 * H1);  // the first pass's weights
+    st.issue(1, a.on.W[1], H1 * H2);
+    st.issue(2, a.on.W[2], H2 * A);
+  }
   const int row0 = blockIdx.x * TR;
   for (int i = threadIdx.x; i < TR * L0; i += blockDim.x) {
     const int r = i / L0, k = i - r * L0;
@@ -191,7 +213,7 @@ __global__ void __launch_bounds__(kLearnThreads)
   }
   __syncthreads();
   // ---- targets (ddqn.py:38-51): argmax of the online net, value of the target net
-  mlp_forward<TR>(a.on, xs2, h1, h2, q, nullptr, nullptr, wbuf, part, bar, phase, a);
+  mlp_forward<TR>(a.on, &a.tgt, xs2, h1, h2, q, nullptr, nullptr, st, part, a);
   if (threadIdx.x < TR) {
     const int r = threadIdx.x;
     int best = 0;
@@ -200,7 +222,7 @@ __global__ void __launch_bounds__(kLearnThreads)
     y[r] = (float)best;
   }
   __syncthreads();
-  mlp_forward<TR>(a.tgt, xs2, h1, h2, q, nullptr, nullptr, wbuf, part, bar, phase, a);
+  mlp_forward<TR>(a.tgt, &a.on, xs2, h1, h2, q, nullptr, nullptr, st, part, a);
   if (threadIdx.x < TR) {
     const int r = threadIdx.x;
     const float boot = q[r * A + (int)y[r]];
@@ -209,7 +231,7 @@ __global__ void __launch_bounds__(kLearnThreads)
   }
   __syncthreads();
   // ---- online forward on s, cached (net.py:63-74); W3 stays staged below
-  mlp_forward<TR>(a.on, xs, h1, h2, q, z1, z2, wbuf, part, bar, phase, a);
+  mlp_forward<TR>(a.on, nullptr, xs, h1, h2, q, z1, z2, st, part, a);
   // ---- Huber(1) on q[r, a_r] - y_r (net.py:83-115): mean over the batch
   if (threadIdx.x < TR) {
     const int r = threadIdx.x;
@@ -235,7 +257,8 @@ __global__ void __launch_bounds__(kLearnThreads)
   for (int i = threadIdx.x; i < TR * H1; i += blockDim.x) a.a1[(size_t)row0 * H1 + i] = h1[i];
   for (int i = threadIdx.x; i < TR * H2; i += blockDim.x) a.a2[(size_t)row0 * H2 + i] = h2[i];
   for (int i = threadIdx.x; i < TR * A; i += blockDim.x) a.dq[(size_t)row0 * A + i] = dq[i];
-  // ---- d2 = (dq W3^T) * [z2 > 0]   (W3 is still staged in wbuf)
+  // ---- d2 = (dq W3^T) * [z2 > 0]   (the online W3 is still staged)
+  const float* wbuf = st.buf[2];
   for (int e = threadIdx.x; e < TR * H2; e += blockDim.x) {
     const int r = e / H2, k = e - r * H2;
     float acc = 0.0f;
@@ -245,15 +268,16 @@ __global__ void __launch_bounds__(kLearnThreads)
     a.d2[(size_t)row0 * H2 + e] = v;
   }
   __syncthreads();
-  // ---- d1 = (d2 W2^T) * [z1 > 0]: W2 re-staged; thread k walks row k starting
-  // at column k (rotated), so a warp's 32 rows hit 32 different banks
+  // ---- d1 = (d2 W2^T) * [z1 > 0] with the online W2 still staged; thread k
+  // walks row k starting at column k (rotated), so a warp's 32 rows hit 32
+  // different banks
   __syncthreads();
-  stage(wbuf, a.on.W[1], H1, H2, bar, phase);
+  const float* w2s = st.buf[1];
   for (int k = threadIdx.x; k < H1; k += blockDim.x) {
     float acc[TR];
 #pragma unroll
     for (int r = 0; r < TR; ++r) acc[r] = 0.0f;
-    const float* wrow = wbuf + k * H2;
+    const float* wrow = w2s + k * H2;
     int j = k % H2;
     for (int jj = 0; jj < H2; ++jj) {
       const float w = wrow[j];
@@ -382,10 +406,10 @@ __global__ void adam_tick_stats_kernel(double* step_dev, const float* stats) {
 template <int TR>
 size_t learn_smem_bytes(int D0, int H1, int H2, int A) {
   const int L0 = pad4(D0);
-  const int wmax = std::max(std::max(L0 * H1, H1 * H2), pad4(H2) * A);
-  const size_t floats = (size_t)pad4(wmax) + learn_part_floats<TR>(L0, H1, H2) +
+  const size_t floats = (size_t)pad4(L0 * H1) + pad4(H1 * H2) + pad4(H2 * A) +
+                        learn_part_floats<TR>(L0, H1, H2) +
                         (size_t)TR * (2 * L0 + 2 * H1 + 3 * H2 + 2 * A + 1) + 2 * TR;
-  return sizeof(float) * (size_t)pad4((int)floats) + 16;
+  return sizeof(float) * (size_t)pad4((int)floats) + 3 * 8 + 16;
 }
 
 }  // namespace sp
