@@ -11,8 +11,9 @@ draws random actions the same way on the host).  A "step" = one
 (fixed envs per GPU), env ids sharded contiguously across ranks.
 
 * value   -- device time: K steps with actions already in HBM; each step timed
-             with CUDA events on the launching stream; L2 flushed (256 MiB
-             write) between timed steps, outside the events; max over ranks.
+             with CUDA events on the launching stream; L2 flushed between
+             timed steps outside the events (256 MiB write, then a 256 MiB
+             read so the flush's dirty lines drain outside too); max over ranks.
 * e2e     -- same metric through the public API with HOST buffers: per step
              pinned actions H2D, step, D2H of every StepBatch field; timed
              with CUDA events around copies + step.
@@ -235,6 +236,15 @@ def run_ours(args, rank, world, local_rank):
                     torch.empty((n, D), dtype=torch.float32, device=dev),
                     torch.empty(n, dtype=torch.int8, device=dev))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    clean = torch.zeros(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB, read-only
+
+    def flush_l2(k):
+        """Evict L2 outside the timed events: write 256 MiB (> 126 MB L2), then
+        read another 256 MiB so the write's dirty lines drain to DRAM here and
+        not inside the next timed step (which then starts from a clean, cold L2)."""
+        flush.fill_(k & 0xFF)
+        clean.sum()
+
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     stops = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     # the clock sampler runs from the warm-up (GPU already loaded) to the end
@@ -249,7 +259,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize(dev)
         wall0 = time.perf_counter()
         for k in range(K):
-            flush.fill_(k & 0xFF)  # evict L2 (256 MiB > 126 MB) outside the timed events
+            flush_l2(k)  # evict L2 (outside the timed events)
             starts[k].record(stream)
             env.step_device(acts[W + k].data_ptr(), out)
             stops[k].record(stream)
@@ -279,7 +289,7 @@ def run_ours(args, rank, world, local_rank):
     e_starts = [torch.cuda.Event(enable_timing=True) for _ in range(Ke)]
     e_stops = [torch.cuda.Event(enable_timing=True) for _ in range(Ke)]
     for k in range(Ke):
-        flush.fill_(k & 0xFF)
+        flush_l2(k)
         hb.actions.copy_(h_act[k])  # the step's inputs, already in pinned host memory
         e_starts[k].record(stream)
         res = env.step_host(hb.actions, hb)  # H2D actions, step, D2H of every field, sync
@@ -312,7 +322,7 @@ def run_ours(args, rank, world, local_rank):
                                    "32 LiDAR beams @300 cm, random actions, fused auto-reset",
                        "envs_per_gpu": n, "global_envs": n * world, "n_beams": N_BEAMS,
                        "n_maps": N_MAPS, "diversity": DIVERSITY, "parallelism": f"env-shard x{world}",
-                       "l2": "flushed (256 MiB write) between timed steps, outside the events",
+                       "l2": "flushed between timed steps, outside the events: 256 MiB write, then a 256 MiB read so the write-back of the dirty flush lines also happens outside",
                        "launch": info},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": Ke,

@@ -1100,4 +1100,13 @@ int sp_ddqn_update(const SpMlp* on, const SpMlp* tg, const float* s, const int64
   return SP_OK;
 }
 
+#ifdef SP_TIMING
+// debug builds only (not part of include/sparrow.h): per-CTA phase stamps
+int sp_debug_read_ts(unsigned long long* out, int n_ctas) {
+  SP_CUDA(cudaDeviceSynchronize());
+  SP_CUDA(cudaMemcpyFromSymbol(out, g_sp_ts, sizeof(unsigned long long) * 12 * (size_t)n_ctas));
+  return SP_OK;
+}
+#endif
+
 }  // extern "C"

@@ -598,17 +598,36 @@ __device__ __forceinline__ void write_rows(const EnvDev& d, const StepArgs& a, c
   }
 }
 
+// ---------------------------------------------- debug phase timestamps ---
+// Built only with -DSP_TIMING (tools/debug): thread 0 of each CTA stamps
+// %clock64 (SM cycles) at phase boundaries of the first chunk.
+#ifdef SP_TIMING
+__device__ unsigned long long g_sp_ts[1024][12];
+__device__ __forceinline__ void sp_stamp(int k) {
+  if (threadIdx.x == 0 && blockIdx.x < 1024) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+    g_sp_ts[blockIdx.x][k] = t;
+  }
+}
+#define SP_STAMP(k) sp_stamp(k)
+#else
+#define SP_STAMP(k)
+#endif
+
 // ------------------------------------------------------------ the kernel ---
 template <bool kSmem, bool kBordered>
 __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     env_step_kernel(const __grid_constant__ EnvDev d, const __grid_constant__ StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
+  SP_STAMP(0);
   double2* beam = (double2*)(smem + d.off_beam);
   uint64_t* bar = (uint64_t*)(smem + d.off_bar);
   const Chunk c = chunk_smem(smem + d.off_chunk, d.chunk_cap, d.slot_cap, d.D, d.R);
   for (int j = threadIdx.x; j < d.R; j += blockDim.x) beam[j] = d.beam_cs[j];
   if (threadIdx.x == 0 && kSmem) mbar_init(bar, 1);
   __syncthreads();
+  SP_STAMP(1);
   uint32_t phase = 0;
   const int64_t sb = d.cta_begin[blockIdx.x], se = d.cta_begin[blockIdx.x + 1];
   const int D = d.D;
@@ -620,6 +639,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     if (m != cur_map) {
       mv = bind_map<kSmem>(d, m, smem, bar, phase);
       cur_map = m;
+      SP_STAMP(2);
     }
     const MapConst mc = d.mconst[m];
     const int n = (int)min((int64_t)d.chunk_cap, min(se, d.map_off[m + 1]) - s0);
@@ -753,13 +773,16 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       d.ctr[s] = ctr;
     }
     __syncthreads();
+    SP_STAMP(3);
     const int n_slots = c.ctl[1];
     // ---- N: LiDAR noise + longest-first ray order; B: LiDAR rays ------------
     order_slots(c, n_slots);
     noise_phase(d, c, n_slots);
     __syncthreads();
+    SP_STAMP(4);
     ray_phase<kBordered, false>(mv, d, c, beam, n_slots, fin);
     __syncthreads();
+    SP_STAMP(5);
     // ---- C: reward, outputs, statistics ------------------------------------
     if (live) {
       const double rew = ev == 1 ? -10.0
@@ -787,6 +810,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       }
       d.ret[s] = ret;
     }
+    SP_STAMP(6);
     write_rows(d, a, c, s0, n);
     // ---- overflow pass: resets that did not fit the extra slots (rare) -----
     if (a.mode == MODE_STEP && c.ctl[3] > 0) {
@@ -814,6 +838,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       __syncthreads();
       write_rows(d, a, c, s0, n);
     }
+    SP_STAMP(7);
     s0 += n;
   }
 }

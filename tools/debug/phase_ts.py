@@ -1,0 +1,33 @@
+"""Per-CTA phase durations of env_step_kernel from the SP_TIMING variant (debug).
+SPARROW_LIB_PATH=variants/lib_timing.so python tools/debug/phase_ts.py"""
+import sys, os, ctypes
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", ".."))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "..", "tests"))
+import numpy as np, torch
+from helpers import config, load_maps, ranges
+from paper_2305_04180_b200 import VecEnv, _lib
+from paper_2305_04180_b200.vecenv import StepBatch
+lib = ctypes.CDLL(_lib.LIB_PATH)
+names = ["prologue", "bind_map", "phaseA", "order+noise", "rays", "phaseC", "rows"]
+for n in (4096, 16384, 65536):
+    env = VecEnv(load_maps(16), n, ranges(0.3), config(32), check_actions=False)
+    env.reset_all(0)
+    dev = env.device; D = env.state_dim
+    out = StepBatch(torch.empty((n, D), device=dev), torch.empty(n, dtype=torch.float64, device=dev),
+                    torch.empty(n, dtype=torch.bool, device=dev), torch.empty(n, dtype=torch.bool, device=dev),
+                    torch.empty((n, D), device=dev), torch.empty(n, dtype=torch.int8, device=dev))
+    acts = torch.randint(0, 5, (n,), device=dev)
+    for k in range(10):
+        env.step_device(acts.data_ptr(), out)
+    torch.cuda.synchronize()
+    ts = np.zeros((148, 12), np.uint64)
+    lib.sp_debug_read_ts(ts.ctypes.data_as(ctypes.c_void_p), 148)
+    ts = ts.astype(np.int64)
+    ts = (ts - ts[:, :1]) * (1000.0 / 1.965)  # cycles -> ns at 1.965 GHz (per-SM clocks)
+    ts[:, 0] = 0
+    t0 = ts[:, 0].min()
+    d = np.diff(ts, axis=1) / 1e3
+    print(f"n={n}: longest CTA {ts[:, 7].max() / 1e3:.1f} us (clock64)")
+    d = np.diff(ts[:, :8], axis=1) / 1e3
+    for i, nm in enumerate(names):
+        print(f"   {nm:12s} median {np.median(d[:, i]):6.2f} us  max {d[:, i].max():6.2f} us")
