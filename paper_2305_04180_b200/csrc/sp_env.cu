@@ -640,6 +640,12 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       mv = bind_map<kSmem>(d, m, smem, bar, phase);
       cur_map = m;
       SP_STAMP(2);
+#ifdef SP_TIMING
+      if (threadIdx.x == 0) {  // debug: this CTA's env count and map
+        g_sp_ts[blockIdx.x][8] = (unsigned long long)(se - sb);
+        g_sp_ts[blockIdx.x][9] = (unsigned long long)m;
+      }
+#endif
     }
     const MapConst mc = d.mconst[m];
     const int n = (int)min((int64_t)d.chunk_cap, min(se, d.map_off[m + 1]) - s0);

@@ -9,7 +9,7 @@ from paper_2305_04180_b200 import VecEnv, _lib
 from paper_2305_04180_b200.vecenv import StepBatch
 lib = ctypes.CDLL(_lib.LIB_PATH)
 names = ["prologue", "bind_map", "phaseA", "order+noise", "rays", "phaseC", "rows"]
-for n in (4096, 16384, 65536):
+for n in (65536,):
     env = VecEnv(load_maps(16), n, ranges(0.3), config(32), check_actions=False)
     env.reset_all(0)
     dev = env.device; D = env.state_dim
@@ -17,12 +17,13 @@ for n in (4096, 16384, 65536):
                     torch.empty(n, dtype=torch.bool, device=dev), torch.empty(n, dtype=torch.bool, device=dev),
                     torch.empty((n, D), device=dev), torch.empty(n, dtype=torch.int8, device=dev))
     acts = torch.randint(0, 5, (n,), device=dev)
-    for k in range(10):
+    for k in range(int(os.environ.get("STEPS", "10"))):
         env.step_device(acts.data_ptr(), out)
     torch.cuda.synchronize()
     ts = np.zeros((148, 12), np.uint64)
     lib.sp_debug_read_ts(ts.ctypes.data_as(ctypes.c_void_p), 148)
     ts = ts.astype(np.int64)
+    nenv, mapi = ts[:, 8].copy(), ts[:, 9].copy()
     ts = (ts - ts[:, :1]) * (1000.0 / 1.965)  # cycles -> ns at 1.965 GHz (per-SM clocks)
     ts[:, 0] = 0
     t0 = ts[:, 0].min()
@@ -31,3 +32,9 @@ for n in (4096, 16384, 65536):
     d = np.diff(ts[:, :8], axis=1) / 1e3
     for i, nm in enumerate(names):
         print(f"   {nm:12s} median {np.median(d[:, i]):6.2f} us  max {d[:, i].max():6.2f} us")
+    rays = d[:, 4]
+    print("   CTA envs: min %d max %d; CTAs spanning 2 maps: n/a; rays max/mean %.1f/%.1f us" % (nenv.min(), nenv.max(), rays.max(), rays.mean()))
+    print("   per-map: map  ctas  envs/cta  rays_us(mean)  rays_us/env")
+    for m in sorted(set(mapi.tolist())):
+        k = mapi == m
+        print(f"   {m:4d} {k.sum():5d} {nenv[k].mean():9.1f} {rays[k].mean():13.1f} {rays[k].mean() / nenv[k].mean():10.3f}")
