@@ -483,12 +483,14 @@ class DdqnLearner:
         g = self._graphed
         g.run(batch)
         if self.check_finite:
-            loss_v = float(g.loss)
+            if isinstance(g, _FusedUpdate):
+                loss_v, mad_v = g.stats.tolist()  # one read-back of {loss, mean |td|}
+            else:
+                loss_v, mad_v = float(g.loss), float(g.mad)
             if not math.isfinite(loss_v):
                 raise TrainingDiverged(f"non-finite loss {loss_v!r} at update "
                                        f"{self.update_count + 1} (parameter version "
                                        f"{self.online.version})")
-            mad_v = float(g.mad)
         else:
             loss_v = mad_v = float("nan")
         self.adam.step += 1
@@ -644,10 +646,31 @@ class TfmState:  # tfm.py:32-77
 
 # -- Sharer + loops (asl/sharer.py, asl/loops.py) ------------------------------------------
 
-class PublishedModel(NamedTuple):
-    version: int
-    params: QNet
-    checksum: int
+class PublishedModel:
+    """A published parameter snapshot (sharer.py:18-24): version, a private
+    copy of the parameters, and the crc32 of their ``COLORNET`` bytes.
+
+    The checksum is taken from that private copy the first time it is read,
+    not in the learner's publish call. Nothing writes the copy after
+    publication, so the value is the same, and the learner does not pay a
+    device-to-host read and a CRC every ``upload_period`` updates. Unpacks
+    like the reference's NamedTuple."""
+
+    __slots__ = ("version", "params", "_crc")
+
+    def __init__(self, version: int, params: QNet, checksum: int | None = None):
+        self.version = int(version)
+        self.params = params
+        self._crc = checksum
+
+    @property
+    def checksum(self) -> int:
+        if self._crc is None:
+            self._crc = _checksum(self.params)
+        return self._crc
+
+    def __iter__(self):
+        return iter((self.version, self.params, self.checksum))
 
 
 def _checksum(params: QNet) -> int:
@@ -673,7 +696,7 @@ class Sharer:
 
     def publish_params(self, params: QNet) -> PublishedModel:
         snap_params = params.copy()
-        snap = PublishedModel(params.version, snap_params, _checksum(snap_params))
+        snap = PublishedModel(params.version, snap_params)  # crc32 on first read
         self._published = snap  # atomic reference swap
         self.publish_count += 1
         return snap
@@ -760,9 +783,11 @@ def learner_loop(sharer: Sharer, algo: DdqnLearner, tfm_cfg: TfmConfig, learn_st
                 continue
             algo.update(batch)
             sharer.b_step += 1
-            if sharer.b_step % upload_period == 0:
+            published = sharer.b_step % upload_period == 0
+            if published:
                 sharer.publish_params(algo.online)
-            torch.cuda.current_stream(dev).synchronize()
+            if published or not algo.check_finite:  # else the loss read already synchronized
+                torch.cuda.current_stream(dev).synchronize()
             sharer.tfm.record_optimization(time.perf_counter() - started)
             nap = sharer.tfm.learner_sleep(tfm_cfg)
             if nap > 0:

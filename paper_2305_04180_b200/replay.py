@@ -171,7 +171,10 @@ class ReplayBuffer:
         g = _stream_of(rng)
         b, dim, dev = int(batch_size), self.state_dim, self.device
         if out is not None:
-            _check_out(out, b, dim, dev, torch)
+            ok = getattr(self, "_out_ok", None)
+            if ok is None or ok[0] is not out or ok[1] != b:  # validate each new (out, B) once
+                _check_out(out, b, dim, dev, torch)
+                self._out_ok = (out, b)
         else:
             out = TransitionBatch(torch.empty((b, dim), dtype=torch.float32, device=dev),
                                   torch.empty(b, dtype=torch.int64, device=dev),

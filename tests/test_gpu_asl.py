@@ -303,3 +303,19 @@ def test_asl_session_cfg5_shape():
     assert sharer.publish_count >= 1 + sharer.b_step // 50
     snap = env.snapshot_stats()
     assert snap.episodes > 0
+
+
+def test_published_snapshot_checksum():
+    """sharer.py:18-31: the snapshot's crc32 is that of its COLORNET bytes and
+    verify_snapshot holds; the snapshot is a private copy."""
+    import zlib
+    from paper_2305_04180_b200 import ReplayBuffer
+    from paper_2305_04180_b200.asl import QNet, Sharer, verify_snapshot
+    p = QNet.init(np.random.default_rng(31), SIZES)
+    sh = Sharer(ReplayBuffer(16, 37))
+    snap = sh.publish_params(p)
+    version, params, crc = snap
+    assert crc == zlib.crc32(p.to_bytes()) and verify_snapshot(snap)
+    p.weights[0].add_(1.0)  # the learner keeps training: the snapshot is unaffected
+    assert snap.checksum == crc and verify_snapshot(snap)
+    assert sh.fetch_params(version - 1) is snap and sh.fetch_params(version) is None
