@@ -302,12 +302,17 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   if (!cfg || !maps || !out || n_maps < 1) return fail(SP_EINVAL, "null argument");
   if (n_envs < 1) return fail(SP_EINVAL, "need at least one copy");  // vecenv.py:66-67
   if (cfg->n_beams < 1) return fail(SP_EINVAL, "n_beams must be >= 1");
+  if (!(cfg->max_range_cm > 0.0) || !(cfg->robot_radius_cm >= 0.0) || cfg->spawn_attempts < 1 ||
+      cfg->timeout_steps < 1)
+    return fail(SP_EINVAL, "config: max range > 0, radius >= 0, spawn attempts >= 1, timeout >= 1");
+  if (!cfg->beam_offsets) return fail(SP_EINVAL, "config: beam offsets missing");
   if (cfg->n_actions < 1 || cfg->n_actions > SP_MAX_ACTIONS)
     return fail(SP_EINVAL, "action table must have 1..15 entries");
   if (n_ranges != 1 && n_ranges != n_envs)
     return fail(SP_EINVAL, "need one DiversityRanges per lane");  // core.py:56-57
   const int H = maps[0].n_rows, W = maps[0].n_cols;
   const double cell = maps[0].cell_cm;
+  if (!(cell > 0.0)) return fail(SP_EINVAL, "cell size must be positive");
   for (int m = 0; m < n_maps; ++m)
     if (maps[m].n_rows != H || maps[m].n_cols != W || maps[m].cell_cm != cell)
       return fail(SP_EMAP, "all maps in one batch must share grid shape and cell size");

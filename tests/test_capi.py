@@ -71,3 +71,58 @@ def test_error_codes_and_version_without_gpu():
     assert "null" in _lib.last_error()
     assert lib.sp_rb_create(0, 4, 0, ctypes.byref(h)) == _lib.SP_EINVAL
     assert "capacity" in _lib.last_error()
+
+
+def test_env_create_validates_before_touching_the_device():
+    """sp_env_create rejects bad configs / maps with status codes and messages
+    before any CUDA call (so this runs without a GPU): vecenv.py:66-67,
+    core.py:56-66 errors."""
+    import numpy as np
+    lib = _lib.load()
+    offs = np.linspace(-1.0, 1.0, 4)
+
+    def cfg(**kw):
+        c = _lib.SpConfig()
+        c.n_beams, c.max_range_cm, c.robot_radius_cm, c.timeout_steps = 4, 300.0, 9.0, 1000
+        c.proximity_cm, c.n_actions, c.spawn_attempts, c.auto_reset = 30.0, 5, 256, 1
+        c.beam_offsets = offs.ctypes.data_as(_lib.c_dp)
+        for k, v in kw.items():
+            setattr(c, k, v)
+        return c
+
+    occ = np.ones((20, 20), np.uint8)
+
+    def desc(rows=20, cols=20, cell=1.0):
+        d = _lib.SpMapDesc()
+        d.n_rows, d.n_cols, d.cell_cm = rows, cols, cell
+        d.occupancy = occ.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
+        return d
+
+    rg = (_lib.SpRanges * 1)()
+    rg[0].delay[0], rg[0].delay[1] = 0, 0
+    h = ctypes.c_void_p()
+
+    def create(c, maps, n_envs=4, ranges=rg, n_ranges=1, midx=None):
+        arr = (_lib.SpMapDesc * len(maps))(*maps)
+        mp = None if midx is None else np.ascontiguousarray(midx, np.int32).ctypes.data_as(_lib.c_i32p)
+        return lib.sp_env_create(ctypes.byref(c), arr, len(maps), n_envs, mp, ranges, n_ranges,
+                                 0, 0, ctypes.byref(h))
+
+    cases = [
+        (lambda: create(cfg(n_beams=0), [desc()]), _lib.SP_EINVAL, b"n_beams"),
+        (lambda: create(cfg(max_range_cm=0.0), [desc()]), _lib.SP_EINVAL, b"max range"),
+        (lambda: create(cfg(n_actions=16), [desc()]), _lib.SP_EINVAL, b"action table"),
+        (lambda: create(cfg(), [desc()], n_envs=0), _lib.SP_EINVAL, b"at least one copy"),
+        (lambda: create(cfg(), [desc(), desc(rows=30)]), _lib.SP_EMAP, b"grid shape"),
+        (lambda: create(cfg(), [desc(cell=0.0)]), _lib.SP_EINVAL, b"cell size"),
+        (lambda: create(cfg(), [desc()], midx=[0, 1, 0, 0]), _lib.SP_EINVAL, b"map_index"),
+        (lambda: create(cfg(), [desc()], n_ranges=2), _lib.SP_EINVAL, b"DiversityRanges"),
+    ]
+    for call, want, msg in cases:
+        rc = call()
+        assert rc == want, (rc, want, msg)
+        assert msg in lib.sp_last_error(), lib.sp_last_error()
+    bad = (_lib.SpRanges * 1)()
+    bad[0].delay[0], bad[0].delay[1] = 0, 65
+    assert create(cfg(), [desc()], ranges=bad) == _lib.SP_EINVAL
+    assert b"delay" in lib.sp_last_error()
