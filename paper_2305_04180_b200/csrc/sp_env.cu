@@ -410,22 +410,45 @@ __device__ __forceinline__ void set_error(const EnvDev& d, int code, int64_t row
 // LiDAR noise (core.py:237-241): every listed slot needs R standard normals
 // from blocks nctr[slot] .. nctr[slot]+nb-1 of its stream.  One work item per
 // Philox block, spread over the whole CTA; z is staged in the obs row.
-__device__ __forceinline__ void noise_phase(const EnvDev& d, const Chunk& c, int n_slots) {
-  const int nb = d.nb, R = d.R, D = d.D;
+// z ~ N(0,1) of one noise block (4 beams) of `slot` into its staging row
+__device__ __forceinline__ void noise_block(const EnvDev& d, const Chunk& c, int slot, int b) {
+  const Block4 blk = stream_block(d.seed, c.gid[slot], 0u, c.nctr[slot] + (uint64_t)b);
+  float z[4];
+  draw_normals4(blk, z);
+  float* row = c.stage + slot * d.D + 5 + 4 * b;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    if (4 * b + u < d.R) row[u] = z[u];
+}
+
+// The LiDAR noise of env slots 0..n-1 computed by the threads that have no env
+// in phase A, while phase A runs (env slot = its env's chunk index): a post-step scan draws from the env's
+// counter at step start (c.nctr/c.gid snapshot at chunk start), and only z is
+// staged (sigma is applied when the ray retires), so nothing here depends on
+// phase A.  first = the first idle thread.
+__device__ __forceinline__ void prenoise(const EnvDev& d, const Chunk& c, int n, int first) {
+  const int nb = d.nb;
+  const int idle = (int)blockDim.x - first;
+  for (int it = (int)threadIdx.x - first; it < n * nb; it += idle) {
+    const int k = d.nb_shift >= 0 ? (it >> d.nb_shift) : it / nb;
+    noise_block(d, c, k, it - k * nb);
+  }
+}
+
+// slots below `pre` (env slots) were pre-noised during phase A (prenoise)
+__device__ __forceinline__ void noise_phase(const EnvDev& d, const Chunk& c, int n_slots,
+                                            int pre = 0) {
+  const int nb = d.nb;
   const int items = n_slots * nb;
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
     const int k = d.nb_shift >= 0 ? (it >> d.nb_shift) : it / nb;
     const int b = it - k * nb;
     const int slot = c.list[k];
-    const Block4 blk = stream_block(d.seed, c.gid[slot], 0u, c.nctr[slot] + (uint64_t)b);
-    float z[4];
-    draw_normals4(blk, z);
-    float* row = c.stage + slot * D + 5 + 4 * b;
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (4 * b + u < R) row[u] = z[u];
+    if (slot < pre) continue;
+    noise_block(d, c, slot, b);
   }
 }
+
 
 // reward.py:33-37
 __device__ __forceinline__ double bearing_error(double x, double y, double h, double gx,
@@ -657,7 +680,17 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     uint64_t ctr = act ? d.ctr[s] : 0;
     __syncthreads();  // the previous chunk is fully written out
     if (threadIdx.x < 4) c.ctl[threadIdx.x] = 0;
+    // idle threads pre-noise the first kpre env slots during phase A: about
+    // 12 blocks per idle thread fit in phase A's latency (more would make
+    // them its tail); the rest is done after phase A
+    const int kpre = a.mode == MODE_STEP
+                         ? min(n, 12 * max(0, (int)blockDim.x - n) / d.nb) : 0;
+    if (act && e < kpre) {  // the post-step scan's noise stream (add_slot writes the same)
+      c.nctr[e] = ctr;
+      c.gid[e] = gid;
+    }
     __syncthreads();
+    if (kpre > 0 && !act) prenoise(d, c, kpre, n);
 
     // ---- A: physics, collision, events, reward partial, resets -----------
     bool live = false, ended = false;
@@ -783,7 +816,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     const int n_slots = c.ctl[1];
     // ---- N: LiDAR noise + longest-first ray order; B: LiDAR rays ------------
     order_slots(c, n_slots);
-    noise_phase(d, c, n_slots);
+    noise_phase(d, c, n_slots, kpre);
     __syncthreads();
     SP_STAMP(4);
     ray_phase<kBordered, false>(mv, d, c, beam, n_slots, fin);
