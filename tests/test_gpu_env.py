@@ -477,3 +477,13 @@ def test_n1_matches_single_env():  # test_vecenv.py:27-39
         out = env.step(a)
         assert np.array_equal(b.store_states[0].cpu().numpy(), out.state)
         assert float(b.rewards[0]) == out.reward
+
+
+def test_render_ascii_marks_robot():  # env.py:109-110
+    env = make_env(40)
+    env.reset(5)
+    place(env, 12.5, 20.5, 0.0)
+    txt = env.render_ascii()
+    rows = txt.splitlines()
+    assert len(rows) == 40 and sum(r.count("R") for r in rows) == 1
+    assert rows[40 - 1 - 20][12] == "R"
