@@ -14,6 +14,7 @@
  *                       (SimBatch.__init__; map stacking core.py:62-71)
  *   sp_env_reset_all    vecenv.py:84-92 (VecEnv.reset_all) -> core.py:114-161
  *   sp_env_step         vecenv.py:94-116 (VecEnv.step_batch) -> core.py:165-219
+ *   sp_env_step_host    the same with host buffers (numpy in/out contract)
  *                       (SimBatch.step_all) incl. fused auto-reset core.py:114-161
  *   sp_env_stats_*      vecenv.py:120-141 (snapshot_stats, first_episode_outcomes)
  *   sp_env_read_state   sim/core.py:88-108 SoA attributes (read-only views)
@@ -101,6 +102,17 @@ int sp_env_reset_all(SpEnv* env, uint64_t seed, float* states /* dev (N, 5+R) */
 int sp_env_step(SpEnv* env, const int64_t* actions /* dev (N) */, float* states,
                 float* store_states, double* rewards, uint8_t* dones, uint8_t* truncated,
                 int8_t* events, void* stream);
+/* Host-buffer step: the reference's numpy step_batch contract (vecenv.py:94-116)
+ * for callers holding host memory.  h_actions: N int64; h_out: one contiguous
+ * block of sp_env_host_out_bytes(env) bytes laid out as
+ *   rewards f64[N] | states f32[N][5+R] | store_states f32[N][5+R] |
+ *   dones u8[N] | truncated u8[N] | events i8[N].
+ * One H2D copy of the actions, the fused step, one D2H copy of the block, all
+ * on `stream` (device staging owned by the handle); returns after the stream
+ * synchronized.  Page-locked host memory lets the copies run at full PCIe
+ * bandwidth.  Invalid actions are reported by sp_env_check as after sp_env_step. */
+int64_t sp_env_host_out_bytes(SpEnv* env);
+int sp_env_step_host(SpEnv* env, const int64_t* h_actions, void* h_out, void* stream);
 /* Sticky device error word from the last step (SP_OK if none); syncs `stream`. */
 int sp_env_check(SpEnv* env, void* stream, int64_t* err_env);
 /* 1 if any lane waits for a reset (auto_reset=0 path; core.py:171-174); syncs. */

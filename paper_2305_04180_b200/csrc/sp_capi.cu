@@ -133,6 +133,7 @@ struct SpEnv {
   int64_t* h_scan = nullptr;  // pinned staging for scan offsets (n_maps + 1 + n_sm + 1)
   int64_t* d_scan = nullptr;
   cudaEvent_t scan_copied = nullptr;
+  uint8_t* d_host_stage = nullptr;  // sp_env_step_host: actions | output block (device)
   std::mutex mu;
 
   template <class T>
@@ -575,6 +576,37 @@ int sp_env_step(SpEnv* env, const int64_t* actions, float* states, float* store_
   a.truncated = truncated;
   a.events = events;
   return launch_env(env, a, (cudaStream_t)stream);
+}
+
+int64_t sp_env_host_out_bytes(SpEnv* env) {
+  if (!env) return -1;
+  return env->n * (8 + 2 * 4 * (int64_t)env->D + 3);
+}
+
+int sp_env_step_host(SpEnv* env, const int64_t* h_actions, void* h_out, void* stream) {
+  if (!env || !h_actions || !h_out) return fail(SP_EINVAL, "null argument");
+  DevDeviceGuard guard(env->device);
+  const int64_t n = env->n, D = env->D, out_bytes = sp_env_host_out_bytes(env);
+  if (!env->d_host_stage) {
+    uint8_t* p = nullptr;
+    const int rc = env->alloc(&p, (size_t)(8 * n + out_bytes));
+    if (rc != SP_OK) return rc;
+    env->d_host_stage = p;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* dev_act = env->d_host_stage;
+  uint8_t* o = env->d_host_stage + 8 * n;  // output block, 8-byte aligned
+  SP_CUDA(cudaMemcpyAsync(dev_act, h_actions, 8 * n, cudaMemcpyHostToDevice, st));
+  double* rewards = (double*)o;
+  float* states = (float*)(o + 8 * n);
+  float* store = states + n * D;
+  uint8_t* dones = (uint8_t*)(store + n * D);
+  const int rc = sp_env_step(env, (const int64_t*)dev_act, states, store, rewards, dones,
+                             dones + n, (int8_t*)(dones + 2 * n), stream);
+  if (rc != SP_OK) return rc;
+  SP_CUDA(cudaMemcpyAsync(h_out, o, out_bytes, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  return SP_OK;
 }
 
 int sp_env_check(SpEnv* env, void* stream, int64_t* err_env) {

@@ -45,13 +45,10 @@ class StepBatch(NamedTuple):  # vecenv.py:24-30
 
 
 class HostStep(NamedTuple):
-    """Buffers of ``VecEnv.step_host``: page-locked host side + device twins."""
-    actions: "torch.Tensor"    # (N,) int64, pinned
-    out: StepBatch             # pinned host tensors, StepBatch dtypes
-    d_actions: "torch.Tensor"  # device staging
-    d_out: StepBatch
-    h_flat: "torch.Tensor"     # the storage behind ``out`` / ``d_out``
-    d_flat: "torch.Tensor"
+    """Page-locked buffers of ``VecEnv.step_host``."""
+    actions: "torch.Tensor"    # (N,) int64
+    out: StepBatch             # views into h_flat, StepBatch dtypes
+    h_flat: "torch.Tensor"     # the sp_env_step_host output block
 
 
 @dataclass
@@ -329,36 +326,31 @@ class VecEnv:
         return out
 
     def host_buffers(self) -> "HostStep":
-        """Page-locked host buffers (and their device twins) for ``step_host``.
-        Every output field is a view into one flat buffer per side, so the
-        results come back in a single D2H copy."""
+        """Page-locked host buffers for ``step_host``. The outputs are views into
+        one flat block in ``sp_env_step_host``'s layout (include/sparrow.h)."""
         torch = self._torch
         n, d = self.n_copies, self.state_dim
+        total = int(self._lib.sp_env_host_out_bytes(self._h))
+        h_flat = torch.empty(total, dtype=torch.uint8).pin_memory()
         fields = ((n, torch.float64, 8), ((n, d), torch.float32, 4), ((n, d), torch.float32, 4),
                   (n, torch.bool, 1), (n, torch.bool, 1), (n, torch.int8, 1))
-        total = sum(int(np.prod(sh)) * sz for sh, _, sz in fields)
-
-        def views(flat):
-            out, off = [], 0
-            for sh, dt, sz in fields:
-                nb = int(np.prod(sh)) * sz
-                out.append(flat[off:off + nb].view(dt).view(sh))
-                off += nb
-            r, st, ss, dn, tr, ev = out
-            return StepBatch(st, r, dn, tr, ss, ev)
-        h_flat = torch.empty(total, dtype=torch.uint8).pin_memory()
-        d_flat = torch.empty(total, dtype=torch.uint8, device=self.device)
-        return HostStep(torch.empty(n, dtype=torch.int64).pin_memory(), views(h_flat),
-                        torch.empty(n, dtype=torch.int64, device=self.device), views(d_flat),
-                        h_flat, d_flat)
+        views, off = [], 0
+        for sh, dt, sz in fields:
+            nb = int(np.prod(sh)) * sz
+            views.append(h_flat[off:off + nb].view(dt).view(sh))
+            off += nb
+        assert off == total
+        r, st, ss, dn, tr, ev = views
+        return HostStep(torch.empty(n, dtype=torch.int64).pin_memory(),
+                        StepBatch(st, r, dn, tr, ss, ev), h_flat)
 
     def step_host(self, actions, bufs: "HostStep | None" = None) -> StepBatch:
         """The reference's numpy ``step_batch`` (vecenv.py:94-116): host actions
-        in, a StepBatch of numpy arrays out. One H2D copy of the actions, the
-        fused step, and one D2H copy per field from/to page-locked buffers, all
-        on the current stream; returns once it has synchronized. The arrays are
-        views of ``bufs`` (default: buffers owned by this env), so the next call
-        overwrites them. ``actions`` may already be ``bufs.actions``."""
+        in, a StepBatch of numpy arrays out, through ``sp_env_step_host``: one
+        H2D copy, the fused step and one D2H copy of a flat page-locked block
+        in a single C call that returns after the stream synchronized. The
+        arrays are views of ``bufs`` (default: buffers owned by this env), so the
+        next call overwrites them. ``actions`` may already be ``bufs.actions``."""
         if not self._seeded:
             raise EpisodeTerminated("reset_all(seed) must be called before stepping")
         torch = self._torch
@@ -381,10 +373,8 @@ class VecEnv:
                                                         ctypes.byref(flag)), "step")
             if flag.value:
                 raise EpisodeTerminated("some lanes finished their episode; reset before stepping")
-        bufs.d_actions.copy_(bufs.actions, non_blocking=True)
-        self.step_device(bufs.d_actions.data_ptr(), bufs.d_out)
-        bufs.h_flat.copy_(bufs.d_flat, non_blocking=True)
-        torch.cuda.current_stream(self.device).synchronize()
+        _lib.check(self._lib.sp_env_step_host(self._h, bufs.actions.data_ptr(),
+                                              bufs.h_flat.data_ptr(), self._stream()), "step")
         return StepBatch(*(t.numpy() for t in bufs.out))
 
     def step_device(self, actions_ptr: int, out: StepBatch) -> None:

@@ -487,3 +487,37 @@ def test_render_ascii_marks_robot():  # env.py:109-110
     rows = txt.splitlines()
     assert len(rows) == 40 and sum(r.count("R") for r in rows) == 1
     assert rows[40 - 1 - 20][12] == "R"
+
+
+def test_c_abi_host_step_with_pageable_buffers():
+    """sp_env_step_host straight from numpy (pageable) memory: the documented
+    block layout, the same results as the device step."""
+    import ctypes
+    from paper_2305_04180_b200 import VecEnv, _lib
+    maps = load_maps(2)
+    n = 257
+    a_env = VecEnv(maps, n, ranges(0.3), config(32))
+    b_env = VecEnv(maps, n, ranges(0.3), config(32))
+    a_env.reset_all(9)
+    b_env.reset_all(9)
+    D = b_env.state_dim
+    nbytes = int(b_env._lib.sp_env_host_out_bytes(b_env._h))
+    assert nbytes == n * (8 + 8 * D + 3)
+    block = np.zeros(nbytes, np.uint8)
+    for t in range(25):
+        acts = np.ascontiguousarray(random_actions(9, np.arange(n), t), np.int64)
+        x = a_env.step_batch(acts)
+        _lib.check(b_env._lib.sp_env_step_host(b_env._h, acts.ctypes.data, block.ctypes.data,
+                                               b_env._stream()), "step_host")
+        off = 0
+        rew = block[off:off + 8 * n].view(np.float64); off += 8 * n
+        st = block[off:off + 4 * n * D].view(np.float32).reshape(n, D); off += 4 * n * D
+        ss = block[off:off + 4 * n * D].view(np.float32).reshape(n, D); off += 4 * n * D
+        dn, tr, ev = block[off:off + n], block[off + n:off + 2 * n], block[off + 2 * n:].view(np.int8)
+        assert np.array_equal(x.rewards.cpu().numpy(), rew)
+        assert np.array_equal(x.states.cpu().numpy(), st)
+        assert np.array_equal(x.store_states.cpu().numpy(), ss)
+        assert np.array_equal(x.dones.cpu().numpy(), dn.astype(bool))
+        assert np.array_equal(x.truncated.cpu().numpy(), tr.astype(bool))
+        assert np.array_equal(x.events.cpu().numpy(), ev)
+    del ctypes
