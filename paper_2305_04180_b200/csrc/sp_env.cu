@@ -381,26 +381,39 @@ __device__ __forceinline__ uint8_t scan_bucket(const EnvDev& d, int32_t hread) {
   return (uint8_t)work_bucket(sum / (uint32_t)d.R_pad);
 }
 
-__device__ __forceinline__ void order_slots(const Chunk& c, int n_slots) {
+// The threads that cooperate on a phase: the whole CTA (barrier 0 =
+// __syncthreads) or a warp-aligned group with its own named barrier.
+struct Grp {
+  int tid, n, id;
+  __device__ __forceinline__ void sync() const {
+    if (id == 0)
+      __syncthreads();
+    else
+      asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+  }
+};
+__device__ __forceinline__ Grp cta_grp() { return Grp{(int)threadIdx.x, (int)blockDim.x, 0}; }
+
+__device__ __forceinline__ void order_slots(const Chunk& c, int n_slots, const Grp& g) {
   int* cnt = c.ctl + 4;
   int* off = c.ctl + 12;
-  if (threadIdx.x < 8) cnt[threadIdx.x] = 0;
-  __syncthreads();
-  for (int k = threadIdx.x; k < n_slots; k += blockDim.x) atomicAdd(&cnt[c.sbucket[c.reg[k]]], 1);
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  if (g.tid < 8) cnt[g.tid] = 0;
+  g.sync();
+  for (int k = g.tid; k < n_slots; k += g.n) atomicAdd(&cnt[c.sbucket[c.reg[k]]], 1);
+  g.sync();
+  if (g.tid == 0) {
     int acc = 0;
     for (int b = 0; b < 8; ++b) {
       off[b] = acc;
       acc += cnt[b];
     }
   }
-  __syncthreads();
-  for (int k = threadIdx.x; k < n_slots; k += blockDim.x) {
+  g.sync();
+  for (int k = g.tid; k < n_slots; k += g.n) {
     const int slot = c.reg[k];
     c.list[atomicAdd(&off[c.sbucket[slot]], 1)] = slot;
   }
-  __syncthreads();  // c.list complete before anyone dispatches from it
+  g.sync();  // c.list complete before anyone dispatches from it
 }
 
 __device__ __forceinline__ void set_error(const EnvDev& d, int code, int64_t row) {
@@ -436,11 +449,11 @@ __device__ __forceinline__ void prenoise(const EnvDev& d, const Chunk& c, int n,
 }
 
 // slots below `pre` (env slots) were pre-noised during phase A (prenoise)
-__device__ __forceinline__ void noise_phase(const EnvDev& d, const Chunk& c, int n_slots,
-                                            int pre = 0) {
+__device__ __forceinline__ void noise_phase(const EnvDev& d, const Chunk& c, int n_slots, int pre,
+                                            const Grp& g) {
   const int nb = d.nb;
   const int items = n_slots * nb;
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+  for (int it = g.tid; it < items; it += g.n) {
     const int k = d.nb_shift >= 0 ? (it >> d.nb_shift) : it / nb;
     const int b = it - k * nb;
     const int slot = c.list[k];
@@ -606,10 +619,10 @@ enum : uint8_t {
 // n x D floats so every lane stores (full SIMT), consecutive lanes hitting
 // consecutive addresses of the same output row.
 __device__ __forceinline__ void write_rows(const EnvDev& d, const StepArgs& a, const Chunk& c,
-                                           int64_t s0, int n) {
+                                           int64_t s0, int n, const Grp& g) {
   const int D = d.D;
   const int total = n * D;
-  for (int f = threadIdx.x; f < total; f += blockDim.x) {
+  for (int f = g.tid; f < total; f += g.n) {
     const int e = (int)(((uint64_t)(uint32_t)f * d.d_magic) >> 40);  // f / D
     const int k = f - e * D;
     const uint8_t w = c.wmode[e];
@@ -619,6 +632,149 @@ __device__ __forceinline__ void write_rows(const EnvDev& d, const StepArgs& a, c
     if (w != W_STATE) a.store_states[o] = own;
     if (w != W_RESET_OV) a.states[o] = w == W_RESET_X ? c.stage[c.xslot[e] * D + k] : own;
   }
+}
+
+// Phase A of one env in MODE_STEP (core.py:165-206 + vecenv.py:96-114): delay
+// queue, kinematics, collision, events, the reward without its proximity term,
+// the obs header, the post-step scan's slot (e) and, for a finished episode,
+// the fused auto-reset with its fresh scan in an extra slot (cap.. slot_cap-1).
+// ctr advances past the draws used; the caller stores it.
+struct StepA {
+  bool live = false, ended = false;
+  int8_t ev = 0;
+  int32_t step_end = 0;  // episode length before any reset
+  double partial = 0.0;  // shaped reward minus the proximity term
+};
+
+__device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, const MapView& mv,
+                                          const MapConst& mc, const Chunk& c, int e, int64_t s,
+                                          int64_t row, uint32_t gid, uint64_t& ctr, int cap,
+                                          int slot_cap) {
+  StepA r;
+  const int64_t av = a.actions[row];
+  if (av < 0 || av >= d.n_actions) {
+    set_error(d, SP_EACTION, row);
+  } else if (d.needs_reset[s]) {
+    set_error(d, SP_EEPISODE, row);
+  } else {
+    r.live = true;
+    double x = d.x[s], y = d.y[s], h = d.h[s], vl = d.vl[s], va = d.va[s];
+    const double k = d.pk[s], dt = d.pdt[s], vml = d.pvl[s], vma = d.pva[s];
+    const int32_t delay = d.delay[s];
+    int32_t step = d.step[s];
+    // delay queue (core.py:176-182): matured = action issued `delay` steps ago
+    uint32_t code = (uint32_t)av;
+    if (delay > 0) {
+      const int q = delay - 1;
+      const uint64_t h0 = d.hist[s];
+      const uint64_t w = q < 16 ? h0 : d.hist[(int64_t)(q >> 4) * d.n + s];
+      code = (uint32_t)(w >> (4 * (q & 15))) & 15u;
+      const int nw = (delay + 15) >> 4;
+      uint64_t carry = (uint64_t)av;
+      for (int wi = 0; wi < nw; ++wi) {
+        const uint64_t cur = wi == 0 ? h0 : d.hist[(int64_t)wi * d.n + s];
+        d.hist[(int64_t)wi * d.n + s] = (cur << 4) | carry;
+        carry = cur >> 60;
+      }
+    }
+    const double mv_ = d.action_v[code], mw_ = d.action_w[code];
+    // apply_kinematics (kinematics.py:22-36)
+    const double omk = dsub(1.0, k);
+    vl = dclip(dadd(dmul(k, vl), dmul(omk, mv_)), -vml, vml);
+    va = dclip(dadd(dmul(k, va), dmul(omk, mw_)), -vma, vma);
+    // integrate_unicycle (kinematics.py:39-63)
+    double sin0, cos0, sin1, cos1;
+    sincos(h, &sin0, &cos0);
+    const double h1 = dadd(h, dmul(va, dt));
+    sincos(h1, &sin1, &cos1);
+    double ddx, ddy;
+    if (fabs(va) >= 1e-6) {
+      const double radius = ddiv(vl, va);
+      ddx = dmul(radius, dsub(sin1, sin0));
+      ddy = dmul(-radius, dsub(cos1, cos0));
+    } else {
+      ddx = dmul(dmul(vl, cos0), dt);
+      ddy = dmul(dmul(vl, sin0), dt);
+    }
+    x = dadd(x, ddx);
+    y = dadd(y, ddy);
+    h = wrap_angle(h1);
+    // events (core.py:189-201)
+    const bool coll = disc_hits(mv, d, x, y);
+    const double gdx = dsub(mc.goal_x, x), gdy = dsub(mc.goal_y, y);
+    const double d1 = __dsqrt_rn(dadd(dmul(gdx, gdx), dmul(gdy, gdy)));
+    const bool arrived = !coll && d1 <= mc.goal_r;
+    step += 1;
+    const bool timed_out = !coll && !arrived && step >= d.timeout;
+    r.ev = coll ? 1 : (arrived ? 2 : (timed_out ? 3 : 0));
+    r.ended = coll || arrived || timed_out;
+    // shaped reward without the proximity term (reward.py:55-73) + obs header
+    const double alpha = bearing_error(x, y, h, mc.goal_x, mc.goal_y);
+    if (r.ev == 0 || r.ev == 3) {
+      const double d2 = cross_track(x, y, d.sx[s], d.sy[s], mc.goal_x, mc.goal_y);
+      const double r_d1 = dclip(dsub(1.0, ddiv(d1, mc.plan_dist)), 0.0, 1.0);
+      const double r_d2 = dclip(dsub(1.0, ddiv(d2, mc.plan_dist)), 0.0, 1.0);
+      const double r_v = vl > ddiv(vml, 2.0) ? 1.0 : 0.0;
+      const double r_a = dclip(dsub(1.0, ddiv(dmul(2.0, fabs(alpha)), SP_PI)), -1.0, 1.0);
+      r.partial = dadd(dadd(dadd(dmul(0.3, r_d1), dmul(0.1, r_d2)), dmul(0.3, r_v)),
+                     dmul(0.3, r_a));
+    }
+    header_row(mc, x, y, alpha, d.c0[s], d.s0[s], vl, va, vml, vma, c.stage + e * d.D);
+    // the post-step scan (core.py:203-206); cos/sin of h1 == of wrap(h1)
+    add_slot(d, c, e, x, y, cos1, sin1, d.psig[s], gid, ctr, (int32_t)s,
+             r.ended && d.auto_reset ? -1 : (int32_t)s);
+    ctr += d.nb;
+    d.x[s] = x; d.y[s] = y; d.h[s] = h; d.vl[s] = vl; d.va[s] = va;
+    d.step[s] = step;
+    r.step_end = step;
+    c.wmode[e] = W_KEEP;
+    if (r.ended && d.auto_reset) {  // fused auto-reset (vecenv.py:113-114)
+      const int k2 = atomicAdd(&c.ctl[2], 1);
+      if (k2 < slot_cap - cap) {
+        const int xs = cap + k2;
+        if (reset_env(d, mv, mc, s, gid, ctr, c, xs)) {
+          c.xslot[e] = xs;
+          c.wmode[e] = W_RESET_X;
+        } else {
+          set_error(d, SP_EMAP, row);
+        }
+      } else {
+        c.wmode[e] = W_RESET_OV;  // extra slots exhausted: second pass below
+        atomicAdd(&c.ctl[3], 1);
+      }
+    }
+  }
+  return r;
+}
+
+// Phase C of one env in MODE_STEP (vecenv.py:96-112): reward with the
+// proximity term from its scan, the per-env outputs and the VecEnv statistics.
+__device__ __forceinline__ void finish_env(const EnvDev& d, const StepArgs& a, const Chunk& c,
+                                           int e, int64_t s, int64_t row, const StepA& r) {
+  const double rew = r.ev == 1 ? -10.0
+                   : r.ev == 2 ? 75.0
+                             : dadd(r.partial, dmul(0.1, c.prox[e] ? -1.0 : 0.0));
+  a.rewards[row] = rew;
+  a.dones[row] = (uint8_t)(r.ev == 1 || r.ev == 2);
+  a.truncated[row] = (uint8_t)(r.ev == 3);
+  a.events[row] = r.ev;
+  double ret = dadd(d.ret[s], rew);  // vecenv.py:96-112
+  if (r.ended) {
+    d.episodes[s] += 1;
+    d.return_sum[s] = dadd(d.return_sum[s], ret);
+    if (r.ev == 2) d.arrivals[s] += 1;
+    const unsigned long long kk = atomicAdd(d.rec_count, 1ull);
+    d.rec_ret[kk % d.rec_cap] = ret;
+    d.rec_key[kk % d.rec_cap] = (a.step_index << 32) | (uint64_t)row;
+    if (d.first_event[s] < 0) {
+      d.first_event[s] = r.ev;
+      d.first_ret[s] = ret;
+      d.first_steps[s] = r.step_end;
+    }
+    ret = 0.0;
+    if (!d.auto_reset || c.wmode[e] == W_RESET_OV) d.needs_reset[s] = 1;
+  }
+  d.ret[s] = ret;
 }
 
 // ---------------------------------------------- debug phase timestamps ---
@@ -716,107 +872,20 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
         d.ctr[s] = ctr;
       }
     } else if (act) {
-      const int64_t av = a.actions[row];
-      if (av < 0 || av >= d.n_actions) {
-        set_error(d, SP_EACTION, row);
-      } else if (d.needs_reset[s]) {
-        set_error(d, SP_EEPISODE, row);
-      } else {
-        live = true;
-        double x = d.x[s], y = d.y[s], h = d.h[s], vl = d.vl[s], va = d.va[s];
-        const double k = d.pk[s], dt = d.pdt[s], vml = d.pvl[s], vma = d.pva[s];
-        const int32_t delay = d.delay[s];
-        int32_t step = d.step[s];
-        // delay queue (core.py:176-182): matured = action issued `delay` steps ago
-        uint32_t code = (uint32_t)av;
-        if (delay > 0) {
-          const int q = delay - 1;
-          const uint64_t h0 = d.hist[s];
-          const uint64_t w = q < 16 ? h0 : d.hist[(int64_t)(q >> 4) * d.n + s];
-          code = (uint32_t)(w >> (4 * (q & 15))) & 15u;
-          const int nw = (delay + 15) >> 4;
-          uint64_t carry = (uint64_t)av;
-          for (int wi = 0; wi < nw; ++wi) {
-            const uint64_t cur = wi == 0 ? h0 : d.hist[(int64_t)wi * d.n + s];
-            d.hist[(int64_t)wi * d.n + s] = (cur << 4) | carry;
-            carry = cur >> 60;
-          }
-        }
-        const double mv_ = d.action_v[code], mw_ = d.action_w[code];
-        // apply_kinematics (kinematics.py:22-36)
-        const double omk = dsub(1.0, k);
-        vl = dclip(dadd(dmul(k, vl), dmul(omk, mv_)), -vml, vml);
-        va = dclip(dadd(dmul(k, va), dmul(omk, mw_)), -vma, vma);
-        // integrate_unicycle (kinematics.py:39-63)
-        double sin0, cos0, sin1, cos1;
-        sincos(h, &sin0, &cos0);
-        const double h1 = dadd(h, dmul(va, dt));
-        sincos(h1, &sin1, &cos1);
-        double ddx, ddy;
-        if (fabs(va) >= 1e-6) {
-          const double radius = ddiv(vl, va);
-          ddx = dmul(radius, dsub(sin1, sin0));
-          ddy = dmul(-radius, dsub(cos1, cos0));
-        } else {
-          ddx = dmul(dmul(vl, cos0), dt);
-          ddy = dmul(dmul(vl, sin0), dt);
-        }
-        x = dadd(x, ddx);
-        y = dadd(y, ddy);
-        h = wrap_angle(h1);
-        // events (core.py:189-201)
-        const bool coll = disc_hits(mv, d, x, y);
-        const double gdx = dsub(mc.goal_x, x), gdy = dsub(mc.goal_y, y);
-        const double d1 = __dsqrt_rn(dadd(dmul(gdx, gdx), dmul(gdy, gdy)));
-        const bool arrived = !coll && d1 <= mc.goal_r;
-        step += 1;
-        const bool timed_out = !coll && !arrived && step >= d.timeout;
-        ev = coll ? 1 : (arrived ? 2 : (timed_out ? 3 : 0));
-        ended = coll || arrived || timed_out;
-        // shaped reward without the proximity term (reward.py:55-73) + obs header
-        const double alpha = bearing_error(x, y, h, mc.goal_x, mc.goal_y);
-        if (ev == 0 || ev == 3) {
-          const double d2 = cross_track(x, y, d.sx[s], d.sy[s], mc.goal_x, mc.goal_y);
-          const double r_d1 = dclip(dsub(1.0, ddiv(d1, mc.plan_dist)), 0.0, 1.0);
-          const double r_d2 = dclip(dsub(1.0, ddiv(d2, mc.plan_dist)), 0.0, 1.0);
-          const double r_v = vl > ddiv(vml, 2.0) ? 1.0 : 0.0;
-          const double r_a = dclip(dsub(1.0, ddiv(dmul(2.0, fabs(alpha)), SP_PI)), -1.0, 1.0);
-          partial = dadd(dadd(dadd(dmul(0.3, r_d1), dmul(0.1, r_d2)), dmul(0.3, r_v)),
-                         dmul(0.3, r_a));
-        }
-        header_row(mc, x, y, alpha, d.c0[s], d.s0[s], vl, va, vml, vma, c.stage + e * D);
-        // the post-step scan (core.py:203-206); cos/sin of h1 == of wrap(h1)
-        add_slot(d, c, e, x, y, cos1, sin1, d.psig[s], gid, ctr, (int32_t)s,
-                 ended && d.auto_reset ? -1 : (int32_t)s);
-        ctr += d.nb;
-        d.x[s] = x; d.y[s] = y; d.h[s] = h; d.vl[s] = vl; d.va[s] = va;
-        d.step[s] = step;
-        step_end = step;
-        c.wmode[e] = W_KEEP;
-        if (ended && d.auto_reset) {  // fused auto-reset (vecenv.py:113-114)
-          const int k2 = atomicAdd(&c.ctl[2], 1);
-          if (k2 < d.slot_cap - d.chunk_cap) {
-            const int xs = d.chunk_cap + k2;
-            if (reset_env(d, mv, mc, s, gid, ctr, c, xs)) {
-              c.xslot[e] = xs;
-              c.wmode[e] = W_RESET_X;
-            } else {
-              set_error(d, SP_EMAP, row);
-            }
-          } else {
-            c.wmode[e] = W_RESET_OV;  // extra slots exhausted: second pass below
-            atomicAdd(&c.ctl[3], 1);
-          }
-        }
-      }
+      const StepA r = step_env(d, a, mv, mc, c, e, s, row, gid, ctr, d.chunk_cap, d.slot_cap);
+      live = r.live;
+      ended = r.ended;
+      ev = r.ev;
+      step_end = r.step_end;
+      partial = r.partial;
       d.ctr[s] = ctr;
     }
     __syncthreads();
     SP_STAMP(3);
     const int n_slots = c.ctl[1];
     // ---- N: LiDAR noise + longest-first ray order; B: LiDAR rays ------------
-    order_slots(c, n_slots);
-    noise_phase(d, c, n_slots, kpre);
+    order_slots(c, n_slots, cta_grp());
+    noise_phase(d, c, n_slots, kpre, cta_grp());
     __syncthreads();
     SP_STAMP(4);
     ray_phase<kBordered, false>(mv, d, c, beam, n_slots, fin);
@@ -824,33 +893,16 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     SP_STAMP(5);
     // ---- C: reward, outputs, statistics ------------------------------------
     if (live) {
-      const double rew = ev == 1 ? -10.0
-                       : ev == 2 ? 75.0
-                                 : dadd(partial, dmul(0.1, c.prox[e] ? -1.0 : 0.0));
-      a.rewards[row] = rew;
-      a.dones[row] = (uint8_t)(ev == 1 || ev == 2);
-      a.truncated[row] = (uint8_t)(ev == 3);
-      a.events[row] = ev;
-      double ret = dadd(d.ret[s], rew);  // vecenv.py:96-112
-      if (ended) {
-        d.episodes[s] += 1;
-        d.return_sum[s] = dadd(d.return_sum[s], ret);
-        if (ev == 2) d.arrivals[s] += 1;
-        const unsigned long long kk = atomicAdd(d.rec_count, 1ull);
-        d.rec_ret[kk % d.rec_cap] = ret;
-        d.rec_key[kk % d.rec_cap] = (a.step_index << 32) | (uint64_t)row;
-        if (d.first_event[s] < 0) {
-          d.first_event[s] = ev;
-          d.first_ret[s] = ret;
-          d.first_steps[s] = step_end;
-        }
-        ret = 0.0;
-        if (!d.auto_reset || c.wmode[e] == W_RESET_OV) d.needs_reset[s] = 1;
-      }
-      d.ret[s] = ret;
+      StepA r;
+      r.live = live;
+      r.ended = ended;
+      r.ev = ev;
+      r.step_end = step_end;
+      r.partial = partial;
+      finish_env(d, a, c, e, s, row, r);
     }
     SP_STAMP(6);
-    write_rows(d, a, c, s0, n);
+    write_rows(d, a, c, s0, n, cta_grp());
     // ---- overflow pass: resets that did not fit the extra slots (rare) -----
     if (a.mode == MODE_STEP && c.ctl[3] > 0) {
       __syncthreads();
@@ -870,12 +922,12 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       }
       __syncthreads();
       const int n2 = c.ctl[1];
-      order_slots(c, n2);
-      noise_phase(d, c, n2);
+      order_slots(c, n2, cta_grp());
+      noise_phase(d, c, n2, 0, cta_grp());
       __syncthreads();
       ray_phase<kBordered, false>(mv, d, c, beam, n2, fin);
       __syncthreads();
-      write_rows(d, a, c, s0, n);
+      write_rows(d, a, c, s0, n, cta_grp());
     }
     SP_STAMP(7);
     s0 += n;
@@ -936,6 +988,7 @@ __global__ void __launch_bounds__(SP_SCAN_THREADS, SP_CTAS_PER_SM)
     s0 += n;
   }
 }
+
 
 }  // namespace sp
 
