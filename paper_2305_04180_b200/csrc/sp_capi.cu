@@ -410,6 +410,7 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
     mconst[m].goal_y = maps[m].goal_y;
     mconst[m].goal_r = maps[m].goal_radius;
     mconst[m].plan_dist = maps[m].planning_dist;
+    mconst[m].inv_plan = 1.0 / maps[m].planning_dist;
     for (int k = 0; k < 4; ++k) mconst[m].spawn[k] = maps[m].spawn[k];
   }
   std::vector<double2> beam(env->R);

@@ -15,6 +15,7 @@
 
 #define SP_PI 3.141592653589793
 #define SP_TWO_PI 6.283185307179586
+#define SP_INV_PI 0.3183098861837907  // 1 / SP_PI, correctly rounded
 #define SP_FULL 0xffffffffu
 
 namespace sp {
@@ -90,9 +91,17 @@ __device__ __forceinline__ double dclip(double v, double lo, double hi) {
   return fmin(fmax(v, lo), hi);
 }
 
-// kinematics.py:17-19: pi - np.mod(pi - a, 2 pi)   (np.mod = fmod + sign fix)
+// kinematics.py:17-19: pi - np.mod(pi - a, 2 pi)   (np.mod = fmod + sign fix).
+// For |pi - a| < 4 pi (every heading update) fmod's exact remainder is b or
+// b - 2 pi, and b - 2 pi is exact there (Sterbenz), so the fast path gives the
+// same bits without the fmod loop; anything else takes the general path.
 __device__ __forceinline__ double wrap_angle(double a) {
-  double b = dsub(SP_PI, a);
+  const double b = dsub(SP_PI, a);
+  if (b > -SP_TWO_PI && b < 2.0 * SP_TWO_PI) {
+    if (b == 0.0) return SP_PI;                                  // m = +0
+    if (b < 0.0) return dsub(SP_PI, dadd(b, SP_TWO_PI));         // sign fix
+    return dsub(SP_PI, b < SP_TWO_PI ? b : dsub(b, SP_TWO_PI));  // fmod, exact
+  }
   double m = fmod(b, SP_TWO_PI);
   if (m != 0.0) {
     if (m < 0.0) m = dadd(m, SP_TWO_PI);

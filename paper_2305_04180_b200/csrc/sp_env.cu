@@ -481,24 +481,24 @@ __device__ __forceinline__ double cross_track(double x, double y, double sx, dou
   return __dsqrt_rn(dadd(dmul(ex, ex), dmul(ey, ey)));
 }
 
-// core.py:243-258 columns 0..4 (LiDAR columns come from the ray phase)
-__device__ __forceinline__ void header_row(const MapConst& mc, double x, double y, double alpha,
-                                           double c0, double s0, double vl, double va, double vml,
-                                           double vma, float* row) {
-  const double rx = dsub(mc.goal_x, x), ry = dsub(mc.goal_y, y);
-  row[0] = (float)ddiv(dadd(dmul(c0, rx), dmul(s0, ry)), mc.plan_dist);
-  row[1] = (float)ddiv(dadd(dmul(-s0, rx), dmul(c0, ry)), mc.plan_dist);
-  row[2] = (float)ddiv(alpha, SP_PI);
-  row[3] = (float)ddiv(vl, vml);
-  row[4] = (float)ddiv(va, vma);
-}
-
 // v / m for v in [0, m] from the reciprocal plus one exact-residual correction
 // (Markstein): the correctly rounded quotient without a DDIV.
 __device__ __forceinline__ double div_by(double v, double m, double inv_m) {
   const double q = v * inv_m;
   const double r = fma(-q, m, v);
   return fma(r, inv_m, q);
+}
+
+// core.py:243-258 columns 0..4 (LiDAR columns come from the ray phase)
+__device__ __forceinline__ void header_row(const MapConst& mc, double x, double y, double alpha,
+                                           double c0, double s0, double vl, double va, double vml,
+                                           double vma, float* row) {
+  const double rx = dsub(mc.goal_x, x), ry = dsub(mc.goal_y, y);
+  row[0] = (float)div_by(dadd(dmul(c0, rx), dmul(s0, ry)), mc.plan_dist, mc.inv_plan);
+  row[1] = (float)div_by(dadd(dmul(-s0, rx), dmul(c0, ry)), mc.plan_dist, mc.inv_plan);
+  row[2] = (float)div_by(alpha, SP_PI, SP_INV_PI);
+  row[3] = (float)ddiv(vl, vml);
+  row[4] = (float)ddiv(va, vma);
 }
 
 // Finish functor of the ray phase: noisy normalized obs into the staging row
@@ -712,10 +712,11 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
     const double alpha = bearing_error(x, y, h, mc.goal_x, mc.goal_y);
     if (r.ev == 0 || r.ev == 3) {
       const double d2 = cross_track(x, y, d.sx[s], d.sy[s], mc.goal_x, mc.goal_y);
-      const double r_d1 = dclip(dsub(1.0, ddiv(d1, mc.plan_dist)), 0.0, 1.0);
-      const double r_d2 = dclip(dsub(1.0, ddiv(d2, mc.plan_dist)), 0.0, 1.0);
-      const double r_v = vl > ddiv(vml, 2.0) ? 1.0 : 0.0;
-      const double r_a = dclip(dsub(1.0, ddiv(dmul(2.0, fabs(alpha)), SP_PI)), -1.0, 1.0);
+      const double r_d1 = dclip(dsub(1.0, div_by(d1, mc.plan_dist, mc.inv_plan)), 0.0, 1.0);
+      const double r_d2 = dclip(dsub(1.0, div_by(d2, mc.plan_dist, mc.inv_plan)), 0.0, 1.0);
+      const double r_v = vl > dmul(vml, 0.5) ? 1.0 : 0.0;  // vml / 2, exact
+      const double r_a = dclip(dsub(1.0, div_by(dmul(2.0, fabs(alpha)), SP_PI, SP_INV_PI)), -1.0,
+                               1.0);
       r.partial = dadd(dadd(dadd(dmul(0.3, r_d1), dmul(0.1, r_d2)), dmul(0.3, r_v)),
                      dmul(0.3, r_a));
     }

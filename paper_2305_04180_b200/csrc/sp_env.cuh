@@ -18,6 +18,7 @@ namespace sp {
 struct MapConst {
   double goal_x, goal_y, goal_r, plan_dist;
   double spawn[4];
+  double inv_plan;  // 1 / plan_dist (correctly rounded; quotients use div_by)
 };
 
 // Everything the step kernel reads, by value (kernel parameter).
