@@ -9,7 +9,7 @@ within 1e-5 relative (+ fp32-resolution absolute floor, see helpers.py).
 import numpy as np
 import pytest
 
-from helpers import ATOL_OBS, ATOL_REWARD, assert_close, config, golden, load_maps, ranges
+from helpers import ATOL_OBS, ATOL_REWARD, assert_close, config, golden, load_maps, make_map, ranges
 from oracle.philox_shim import random_actions
 
 pytestmark = pytest.mark.gpu
@@ -142,3 +142,40 @@ def test_fast_marcher_hit_cells(n_beams, max_range):
     mism = cells != wcells
     assert mism.sum() == 0, f"{mism.sum()} hit cells differ of {mism.size}"
     assert_close(got, want, rtol=1e-9, atol=1e-9, what="ranges")
+
+
+def _vs_oracle_run(maps, n, div, steps, seed, n_beams=32):
+    from oracle.oracle import OracleVecEnv
+    cfg = config(n_beams)
+    gpu = _vec(maps, n, ranges(div), cfg)
+    cpu = OracleVecEnv(maps, n, ranges(div), cfg)
+    assert_close(gpu.reset_all(seed).cpu().numpy(), cpu.reset_all(seed), atol=ATOL_OBS, what="reset")
+    for t in range(steps):
+        a = random_actions(seed, np.arange(n), t)
+        g = gpu.step_batch(a)
+        c = cpu.step_batch(a)
+        assert np.array_equal(g.events.cpu().numpy(), c.events), f"events step {t}"
+        assert_close(g.rewards.cpu().numpy(), c.rewards, atol=ATOL_REWARD, what=f"reward {t}")
+        assert_close(g.states.cpu().numpy(), c.states, atol=ATOL_OBS, what=f"states {t}")
+        assert_close(g.store_states.cpu().numpy(), c.store_states, atol=ATOL_OBS, what=f"store {t}")
+    return gpu
+
+
+def test_maps_too_large_for_shared_memory():
+    """1100 x 1100-cell maps: the block table (302 KB) does not fit in shared
+    memory, so the kernel reads the tables through L1/L2 (kSmem = false)."""
+    from paper_2305_04180_b200.mapgen import generate_maps
+    maps = generate_maps(2, seed=3, size_cm=1100, density=0.05)
+    _vs_oracle_run(maps, 96, 0.3, 12, seed=77)  # 302 KB table > 227 KB: the HBM path
+
+
+def test_more_maps_than_ctas():
+    """200 small maps > 148 CTAs: CTAs span several maps and rebind their
+    shared-memory tables between chunks."""
+    rng = np.random.default_rng(5)
+    maps = []
+    for _ in range(200):  # blocks in the upper band, clear of the spawn square (18..27)
+        xs, ys = rng.integers(4, 34, 3), rng.integers(38, 52, 3)  # goal disc at (42, 42)
+        maps.append(make_map(60, blocks=[(int(x), int(y), int(x) + 4, int(y) + 3)
+                                         for x, y in zip(xs, ys)]))
+    _vs_oracle_run(maps, 600, 0.3, 15, seed=91)
