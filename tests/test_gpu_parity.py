@@ -179,3 +179,9 @@ def test_more_maps_than_ctas():
         maps.append(make_map(60, blocks=[(int(x), int(y), int(x) + 4, int(y) + 3)
                                          for x, y in zip(xs, ys)]))
     _vs_oracle_run(maps, 600, 0.3, 15, seed=91)
+
+
+def test_vs_oracle_256_beams():
+    """R = 256 (D = 261): the widest cfg4 scan, 64 noise blocks per scan and
+    the smallest chunk capacity, stepped against the C oracle."""
+    _vs_oracle_run(load_maps(4), 300, 0.3, 10, seed=13, n_beams=256)

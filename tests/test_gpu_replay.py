@@ -206,3 +206,17 @@ def test_concurrent_append_sample_rows_never_torn():  # test_replay.py:113-158
     stop.set()
     p.join()
     assert not errors, errors[0]
+
+
+def test_capacity_one_ring_and_empty_append():
+    """Edge sizes: a one-slot ring keeps only the newest row; an empty batch
+    is a no-op."""
+    from paper_2305_04180_b200 import PhiloxGenerator
+    buf = rb(1)
+    buf.append_batch(*batch_of(0))
+    assert len(buf) == 0
+    for k in range(3):
+        buf.append_batch(*batch_of(1, offset=10 * k))
+        assert len(buf) == 1
+        got = buf.sample(1, PhiloxGenerator(k))  # B <= size, as replay.py:73-75 gates
+        assert got.states.cpu().numpy()[:, 0].tolist() == [10.0 * k]
