@@ -172,6 +172,13 @@ int sp_rb_append(SpReplay* rb, const float* states, const int64_t* actions, cons
 int sp_rb_sample(SpReplay* rb, int64_t batch, uint64_t seed, uint32_t stream_id, uint64_t ctr,
                  float* states, int64_t* actions, float* rewards, float* next_states,
                  uint8_t* dones, int64_t* idx_out, void* stream);
+/* sample with the fill level and the first Philox block read from device memory
+ * (*d_ctr, advanced by batch on the device afterwards): the same draws as
+ * sp_rb_sample(..., ctr = *d_ctr, ...), but CUDA-graph capturable.  The caller
+ * gates on sp_rb_size >= batch (BufferNotReady) and orders it after appends. */
+int sp_rb_sample_dev(SpReplay* rb, int64_t batch, uint64_t seed, uint32_t stream_id,
+                     uint64_t* d_ctr, float* states, int64_t* actions, float* rewards,
+                     float* next_states, uint8_t* dones, int64_t* idx_out, void* stream);
 int sp_rb_size(SpReplay* rb, int64_t* size, int64_t* cursor);
 /* gather rows [0, size) in storage order */
 int sp_rb_gather(SpReplay* rb, float* states, int64_t* actions, float* rewards,

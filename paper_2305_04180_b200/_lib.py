@@ -103,6 +103,8 @@ SIGNATURES = [
                                     ctypes.c_int64, c_vp]),
     ("sp_rb_sample", ctypes.c_int, [c_vp, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint32,
                                     ctypes.c_uint64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    ("sp_rb_sample_dev", ctypes.c_int, [c_vp, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint32,
+                                        c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     ("sp_rb_size", ctypes.c_int, [c_vp, c_i64p, c_i64p]),
     ("sp_rb_gather", ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     ("sp_philox_fill", ctypes.c_int, [ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint32,

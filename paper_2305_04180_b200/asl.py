@@ -360,7 +360,8 @@ class _FusedUpdate:
     Optionally the three launches replay as one CUDA graph. Same static-batch
     and device-step contract as ``_GraphedUpdate``."""
 
-    def __init__(self, learner: "DdqnLearner", batch_size: int, state_dim: int, graph: bool):
+    def __init__(self, learner: "DdqnLearner", batch_size: int, state_dim: int, graph: bool,
+                 sampler=None):
         from paper_2305_04180_b200.replay import TransitionBatch
         torch = _torch()
         self.learner = learner
@@ -400,6 +401,12 @@ class _FusedUpdate:
         arr = ctypes.c_void_p * 6
         self._m = arr(*[t.data_ptr() for t in ad.m_weights + ad.m_biases])
         self._v = arr(*[t.data_ptr() for t in ad.v_weights + ad.v_biases])
+        # optional replay source sampled inside the graph (update_from):
+        # (buffer, rng) with rng's Philox counter mirrored on the device
+        self.sampler = sampler
+        self.d_ctr = None
+        if sampler is not None:
+            self.d_ctr = torch.full((), int(sampler[1].ctr), dtype=torch.int64, device=dev)
         self.graph = None
         if graph:
             side = torch.cuda.Stream(dev)
@@ -412,6 +419,8 @@ class _FusedUpdate:
             for x, y in zip(state, saved):
                 x.copy_(y)
             self.t.fill_(float(ad.step))
+            if self.d_ctr is not None:
+                self.d_ctr.fill_(int(sampler[1].ctr))
             self.graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
                 self._launch()
@@ -427,6 +436,8 @@ class _FusedUpdate:
     def _launch(self) -> None:
         lr, ad, bt = self.learner, self.learner.adam, self.batch
         dev = lr.online.weights[0].device
+        if self.sampler is not None:  # the batch comes straight from the replay ring
+            self.sampler[0].sample_dev(self.batch_size, self.sampler[1], self.d_ctr, bt)
         _lib.check(self._lib.sp_ddqn_update(
             ctypes.byref(self._on), ctypes.byref(self._tg), bt.states.data_ptr(),
             bt.actions.data_ptr(), bt.rewards.data_ptr(), bt.next_states.data_ptr(),
@@ -472,16 +483,22 @@ class DdqnLearner:
         if not (self.graph or self.fused):
             return None
         g = self._graphed
-        if g is None or g.batch_size != batch_size or g.state_dim != state_dim:
+        if (g is None or g.batch_size != batch_size or g.state_dim != state_dim
+                or getattr(g, "sampler", None)):
             g = self._graphed = (_FusedUpdate(self, batch_size, state_dim, self.graph)
                                  if self.fused else _GraphedUpdate(self, batch_size, state_dim))
         return g.batch
 
     def _update_graphed(self, batch) -> UpdateStats:
         b, d = int(batch.states.shape[0]), int(batch.states.shape[1])
-        self.graph_batch(b, d)
         g = self._graphed
+        if g is None or g.batch_size != b or g.state_dim != d or getattr(g, "sampler", None):
+            g = self._graphed = (_FusedUpdate(self, b, d, self.graph) if self.fused
+                                 else _GraphedUpdate(self, b, d))
         g.run(batch)
+        return self._finish_update(g)
+
+    def _finish_update(self, g) -> UpdateStats:
         if self.check_finite:
             if isinstance(g, _FusedUpdate):
                 loss_v, mad_v = g.stats.tolist()  # one read-back of {loss, mean |td|}
@@ -500,6 +517,35 @@ class DdqnLearner:
         if synced:
             self.target.copy_from(self.online)
         return UpdateStats(loss_v, mad_v, self.online.version, synced)
+
+    def update_from(self, buffer, rng, batch_size: int | None = None) -> UpdateStats:
+        """Sample a batch from ``buffer`` with ``rng`` and update: the
+        learner's step (loops.py:83-88). With ``fused=True, graph=True`` the
+        sample (``sp_rb_sample_dev``) and the update replay as one CUDA graph.
+        The Philox counter advances on the device and is mirrored in
+        ``rng.ctr``, so the draws equal ``buffer.sample(B, rng)``. Raises
+        BufferNotReady like ``ReplayBuffer.sample``."""
+        b = int(batch_size or self.config.batch_size)
+        d = int(buffer.state_dim)
+        if not (self.fused and self.graph) or not hasattr(rng, "ctr"):
+            return self.update(buffer.sample(b, rng, out=self.graph_batch(b, d)))
+        g = self._graphed
+        if (g is None or g.batch_size != b or g.state_dim != d or g.sampler is None
+                or g.sampler[0] is not buffer or g.sampler[1] is not rng):
+            g = self._graphed = _FusedUpdate(self, b, d, True, sampler=(buffer, rng))
+            g.ctr_mirror = int(rng.ctr)
+        with buffer._lock:
+            if len(buffer) < b:
+                from paper_2305_04180_b200.replay import BufferNotReady
+                raise BufferNotReady(f"buffer holds {len(buffer)} transitions, need {b}")
+            if int(rng.ctr) != g.ctr_mirror:  # rng also drew elsewhere: resync the device copy
+                g.d_ctr.fill_(int(rng.ctr))
+            buffer._order_after(buffer._last_append)
+            g.graph.replay()
+            rng.ctr += b
+            g.ctr_mirror = int(rng.ctr)
+            buffer._last_sample = buffer._record()
+        return self._finish_update(g)
 
     def update(self, batch) -> UpdateStats:
         if self.graph or self.fused:
@@ -775,13 +821,10 @@ def learner_loop(sharer: Sharer, algo: DdqnLearner, tfm_cfg: TfmConfig, learn_st
                 continue
             started = time.perf_counter()
             try:
-                batch = sharer.buffer.sample(batch_size, rng,
-                                             out=algo.graph_batch(batch_size,
-                                                                  sharer.buffer.state_dim))
+                algo.update_from(sharer.buffer, rng, batch_size)  # sample + update
             except BufferNotReady:
                 time.sleep(_IDLE_POLL_S)
                 continue
-            algo.update(batch)
             sharer.b_step += 1
             published = sharer.b_step % upload_period == 0
             if published:

@@ -161,9 +161,10 @@ struct SpReplay {
   float *s = nullptr, *r = nullptr, *s2 = nullptr;
   int64_t* a = nullptr;
   uint8_t* dn = nullptr;
+  int64_t* d_size = nullptr;  // device copy of `size` (written by the append kernel)
   std::mutex mu;
   ~SpReplay() {
-    cudaFree(s); cudaFree(r); cudaFree(s2); cudaFree(a); cudaFree(dn);
+    cudaFree(s); cudaFree(r); cudaFree(s2); cudaFree(a); cudaFree(dn); cudaFree(d_size);
   }
 };
 
@@ -894,7 +895,8 @@ int sp_rb_create(int64_t capacity, int32_t state_dim, int device, SpReplay** out
   if (cudaMalloc(&rb->s, rows * state_dim * 4) != cudaSuccess ||
       cudaMalloc(&rb->s2, rows * state_dim * 4) != cudaSuccess ||
       cudaMalloc(&rb->r, rows * 4) != cudaSuccess || cudaMalloc(&rb->a, rows * 8) != cudaSuccess ||
-      cudaMalloc(&rb->dn, rows) != cudaSuccess) {
+      cudaMalloc(&rb->dn, rows) != cudaSuccess || cudaMalloc(&rb->d_size, 8) != cudaSuccess ||
+      cudaMemset(rb->d_size, 0, 8) != cudaSuccess) {
     delete rb;
     return fail(SP_ENOMEM, "replay allocation failed");
   }
@@ -927,12 +929,13 @@ int sp_rb_append(SpReplay* rb, const float* states, const int64_t* actions, cons
   DevDeviceGuard guard(rb->device);
   std::lock_guard<std::mutex> lk(rb->mu);
   const int64_t flat = n * rb->dim;
+  const int64_t new_size = std::min(rb->size + n, rb->cap);
   rb_append_kernel<<<grid_for(flat, 256), 256, 0, (cudaStream_t)stream>>>(
       rb->s, rb->a, rb->r, rb->s2, rb->dn, rb->cap, rb->dim, rb->cursor, states, actions, rewards,
-      reward_is_f64, next_states, dones, n);
+      reward_is_f64, next_states, dones, n, rb->d_size, new_size);
   SP_CUDA(cudaGetLastError());
   rb->cursor = (rb->cursor + n) % rb->cap;  // replay.py:66-67
-  rb->size = std::min(rb->size + n, rb->cap);
+  rb->size = new_size;
   return SP_OK;
 }
 
@@ -950,7 +953,25 @@ int sp_rb_sample(SpReplay* rb, int64_t batch, uint64_t seed, uint32_t stream_id,
   const int blocks = (int)((batch + 7) / 8);  // one warp per row
   rb_sample_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
       rb->s, rb->a, rb->r, rb->s2, rb->dn, rb->dim, rb->size, batch, seed, stream_id, ctr, states,
-      actions, rewards, next_states, dones, idx_out);
+      actions, rewards, next_states, dones, idx_out, nullptr, nullptr);
+  SP_CUDA(cudaGetLastError());
+  return SP_OK;
+}
+
+int sp_rb_sample_dev(SpReplay* rb, int64_t batch, uint64_t seed, uint32_t stream_id,
+                     uint64_t* d_ctr, float* states, int64_t* actions, float* rewards,
+                     float* next_states, uint8_t* dones, int64_t* idx_out, void* stream) {
+  if (!rb || !d_ctr) return fail(SP_EINVAL, "null argument");
+  if (batch < 1) return SP_OK;
+  if (!states || !actions || !rewards || !next_states || !dones) return fail(SP_EINVAL, "null argument");
+  DevDeviceGuard guard(rb->device);
+  const int blocks = (int)((batch + 7) / 8);
+  cudaStream_t st = (cudaStream_t)stream;
+  rb_sample_kernel<<<blocks, 256, 0, st>>>(rb->s, rb->a, rb->r, rb->s2, rb->dn, rb->dim, 0, batch,
+                                           seed, stream_id, 0, states, actions, rewards,
+                                           next_states, dones, idx_out, rb->d_size, d_ctr);
+  SP_CUDA(cudaGetLastError());
+  rb_ctr_advance_kernel<<<1, 1, 0, st>>>(d_ctr, batch);
   SP_CUDA(cudaGetLastError());
   return SP_OK;
 }

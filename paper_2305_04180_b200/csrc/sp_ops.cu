@@ -122,8 +122,10 @@ __global__ void rb_append_kernel(float* __restrict__ rs, int64_t* __restrict__ r
                                  int64_t cursor, const float* __restrict__ s,
                                  const int64_t* __restrict__ a, const void* __restrict__ r,
                                  int r_f64, const float* __restrict__ s2,
-                                 const uint8_t* __restrict__ dn, int64_t n) {
+                                 const uint8_t* __restrict__ dn, int64_t n,
+                                 int64_t* __restrict__ d_size, int64_t new_size) {
   const int64_t flat = n * dim, ring = cap * dim, base = cursor * dim;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *d_size = new_size;  // the ring's fill, on device
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < flat;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t dst = base + i;
@@ -144,16 +146,23 @@ __global__ void rb_append_kernel(float* __restrict__ rs, int64_t* __restrict__ r
 // (Philox block ctr + i of (seed, stream_id, tag 2), replay.py:76), then the
 // lanes copy its columns coalesced.  All rows' random ring reads are in flight
 // at once instead of one thread walking a row serially.
+// d_size / d_ctr (nullable): read the fill and the first Philox block from
+// device memory instead (sp_rb_sample_dev: graph-capturable sampling).
 __global__ void rb_sample_kernel(const float* __restrict__ rs, const int64_t* __restrict__ ra,
                                  const float* __restrict__ rr, const float* __restrict__ rs2,
                                  const uint8_t* __restrict__ rd, int32_t dim, int64_t size,
                                  int64_t batch, uint64_t seed, uint32_t stream_id, uint64_t ctr,
                                  float* __restrict__ s, int64_t* __restrict__ a,
                                  float* __restrict__ r, float* __restrict__ s2,
-                                 uint8_t* __restrict__ dn, int64_t* __restrict__ idx_out) {
+                                 uint8_t* __restrict__ dn, int64_t* __restrict__ idx_out,
+                                 const int64_t* __restrict__ d_size,
+                                 const uint64_t* __restrict__ d_ctr) {
   const int lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (i >= batch) return;
+  if (d_size) size = *d_size;
+  if (d_ctr) ctr = *d_ctr;
+  if (size < 1) return;  // nothing stored (the caller gates on its host-side size)
   const Block4 b = stream_block(seed, stream_id, 2u, ctr + (uint64_t)i);
   const int64_t k = draw_integer(b, 0, size);
   if (lane == 0) {
@@ -171,6 +180,8 @@ __global__ void rb_sample_kernel(const float* __restrict__ rs, const int64_t* __
     dst2[c] = src2[c];
   }
 }
+
+__global__ void rb_ctr_advance_kernel(uint64_t* ctr, int64_t n) { *ctr += (uint64_t)n; }
 
 __global__ void rb_gather_kernel(const float* __restrict__ rs, const int64_t* __restrict__ ra,
                                  const float* __restrict__ rr, const float* __restrict__ rs2,

@@ -193,6 +193,25 @@ class ReplayBuffer:
             self._last_sample = self._record()
         return (out, idx) if return_indices else out
 
+    def sample_dev(self, batch_size: int, rng, d_ctr, out: TransitionBatch) -> None:
+        """Enqueue ``sp_rb_sample_dev``: the draws of ``sample(batch_size, rng)``
+        with the first Philox block read from the device counter ``d_ctr``
+        (uint64 scalar tensor, advanced by batch_size on the device) and the
+        fill level read on the device, so the launch can sit inside a CUDA
+        graph. The caller gates on ``len(self) >= batch_size`` and orders the
+        stream after appends (``DdqnLearner.update_from``)."""
+        g = _stream_of(rng)
+        b = int(batch_size)
+        ok = getattr(self, "_out_ok", None)
+        if ok is None or ok[0] is not out or ok[1] != b:
+            _check_out(out, b, self.state_dim, self.device, self._torch)
+            self._out_ok = (out, b)
+        _lib.check(self._lib.sp_rb_sample_dev(self._h, b, g.seed, g.lane, d_ctr.data_ptr(),
+                                              out.states.data_ptr(), out.actions.data_ptr(),
+                                              out.rewards.data_ptr(), out.next_states.data_ptr(),
+                                              out.dones.data_ptr(), None, _lib.stream_ptr(self.device)),
+                   "sample_dev")
+
     def snapshot(self) -> TransitionBatch:
         """All stored transitions in storage order (replay.py:81-87)."""
         torch = self._torch

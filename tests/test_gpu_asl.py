@@ -319,3 +319,36 @@ def test_published_snapshot_checksum():
     p.weights[0].add_(1.0)  # the learner keeps training: the snapshot is unaffected
     assert snap.checksum == crc and verify_snapshot(snap)
     assert sh.fetch_params(version - 1) is snap and sh.fetch_params(version) is None
+
+
+def test_update_from_samples_inside_the_graph():
+    """DdqnLearner.update_from with fused+graph: sp_rb_sample_dev inside the
+    CUDA graph draws the same rows as ReplayBuffer.sample with the same
+    PhiloxGenerator (the device counter is mirrored in rng.ctr), so weights
+    match a fused learner fed by host-side sampling bit for bit; draws made
+    with the rng elsewhere are picked up."""
+    import torch
+    from paper_2305_04180_b200 import BufferNotReady, PhiloxGenerator, ReplayBuffer
+    from paper_2305_04180_b200.asl import DdqnLearner, QNet
+    buf = ReplayBuffer(5000, 37)
+    with pytest.raises(BufferNotReady):
+        DdqnLearner(QNet.init(np.random.default_rng(8), SIZES), fused=True, graph=True).update_from(
+            buf, PhiloxGenerator(1), 64)
+    s, a, r, s2, d = _tb(_batch(np.random.default_rng(6), 3000))
+    buf.append_batch(s, a, r, s2, d)
+    gl = DdqnLearner(QNet.init(np.random.default_rng(8), SIZES), fused=True, graph=True)
+    hl = DdqnLearner(QNet.init(np.random.default_rng(8), SIZES), fused=True)
+    g_rng, h_rng = PhiloxGenerator(9, 3), PhiloxGenerator(9, 3)
+    for k in range(8):
+        if k == 4:  # both streams draw outside update_from: the device counter resyncs
+            buf.sample(32, g_rng)
+            buf.sample(32, h_rng)
+        if k == 6:  # more rows arrive between updates (device fill level follows)
+            s, a, r, s2, d = _tb(_batch(np.random.default_rng(60 + k), 1000))
+            buf.append_batch(s, a, r, s2, d)
+        sg = gl.update_from(buf, g_rng, 256)
+        sh = hl.update(buf.sample(256, h_rng))
+        assert g_rng.ctr == h_rng.ctr
+        assert sg.loss == sh.loss and sg.version == sh.version
+    for w, wh in zip(gl.online.weights + gl.online.biases, hl.online.weights + hl.online.biases):
+        assert torch.equal(w, wh)

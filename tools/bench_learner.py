@@ -19,7 +19,7 @@ sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."
 B, D, CAP = 256, 37, 1_000_000
 
 
-def run_ours(updates, graph, fused=False):
+def run_ours(updates, graph, fused=False, in_graph_sample=False):
     import torch
     from paper_2305_04180_b200 import PhiloxGenerator, ReplayBuffer
     from paper_2305_04180_b200.asl import DdqnLearner, QNet
@@ -37,8 +37,11 @@ def run_ours(updates, graph, fused=False):
     rng = PhiloxGenerator(1)
 
     def one():
-        batch = buf.sample(B, rng, out=algo.graph_batch(B, D))
-        algo.update(batch)  # reads the loss: one sync per update, as the learner loop does
+        if in_graph_sample:  # learner_loop's path: sample + update in one graph replay
+            algo.update_from(buf, rng, B)
+        else:
+            batch = buf.sample(B, rng, out=algo.graph_batch(B, D))
+            algo.update(batch)  # reads the loss: one sync per update, as the learner loop does
 
     for _ in range(20):
         one()
@@ -48,7 +51,8 @@ def run_ours(updates, graph, fused=False):
         one()
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    return {"impl": "ours", "graph": graph, "fused": fused, "updates": updates,
+    return {"impl": "ours", "graph": graph, "fused": fused, "sample_in_graph": in_graph_sample,
+            "updates": updates,
             "updates_per_s": updates / dt,
             "ms_per_update": dt / updates * 1e3}
 
@@ -80,8 +84,9 @@ def main():
     ap.add_argument("--updates", type=int, default=2000)
     ap.add_argument("--reference-updates", type=int, default=300)
     a = ap.parse_args()
-    for graph, fused in ((False, False), (True, False), (False, True), (True, True)):
-        print(json.dumps(run_ours(a.updates, graph, fused)), flush=True)
+    for graph, fused, ig in ((False, False, False), (True, False, False), (False, True, False),
+                             (True, True, False), (True, True, True)):
+        print(json.dumps(run_ours(a.updates, graph, fused, ig)), flush=True)
     print(json.dumps(run_reference(a.reference_updates)), flush=True)
 
 
