@@ -352,10 +352,10 @@ class _GraphedUpdate:
 class _FusedUpdate:
     """One DDQN update as ``sp_ddqn_update``: two hand-written kernels plus a
     one-thread step tick (csrc/sp_learn.cu), instead of ~100 small torch ones.
-    - ``ddqn_rows_kernel``: one CTA per 4-row tile, weights TMA-staged per layer.
+    - ``ddqn_rows_kernel``: one CTA per 2-row tile, weights TMA-staged per layer.
       It computes the targets, the cached forward, the Huber gradient and the
       layer deltas.
-    - ``ddqn_grad_adam_kernel``: the weight gradients as 16x32 tiles over the
+    - ``ddqn_grad_adam_kernel``: the weight gradients as 16x16 tiles over the
       batch (fixed row order), with the finite-gated Adam step in the epilogue.
     Optionally the three launches replay as one CUDA graph. Same static-batch
     and device-step contract as ``_GraphedUpdate``."""

@@ -1050,10 +1050,12 @@ int sp_adam_step(int n_tensors, float* const* params, const float* const* grads,
   return SP_OK;
 }
 
-static int learn_tr(int64_t batch) { return batch % 4 == 0 ? 4 : 1; }
+// rows per CTA of ddqn_rows_kernel: 2 (128 CTAs at B = 256) measured best
+// (per-CTA serial work halves; the extra weight staging streams from L2)
+static int learn_tr(int64_t batch) { return batch % 2 == 0 ? 2 : 1; }
 
 static size_t ddqn_rows_smem(const int32_t* sz, int64_t batch) {
-  return learn_tr(batch) == 4 ? learn_smem_bytes<4>(sz[0], sz[1], sz[2], sz[3])
+  return learn_tr(batch) == 2 ? learn_smem_bytes<2>(sz[0], sz[1], sz[2], sz[3])
                               : learn_smem_bytes<1>(sz[0], sz[1], sz[2], sz[3]);
 }
 
@@ -1110,11 +1112,11 @@ int sp_ddqn_update(const SpMlp* on, const SpMlp* tg, const float* s, const int64
   la.lpart = la.dq + batch * A;
   la.gamma = gamma;
   cudaStream_t st = (cudaStream_t)stream;
-  if (TR == 4) {
-    const size_t sm = learn_smem_bytes<4>(D0, H1, H2, A);
-    SP_CUDA(cudaFuncSetAttribute(ddqn_rows_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (TR == 2) {
+    const size_t sm = learn_smem_bytes<2>(D0, H1, H2, A);
+    SP_CUDA(cudaFuncSetAttribute(ddqn_rows_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sm));
-    ddqn_rows_kernel<4><<<tiles, kLearnThreads, sm, st>>>(la);
+    ddqn_rows_kernel<2><<<tiles, kLearnThreads, sm, st>>>(la);
   } else {
     const size_t sm = learn_smem_bytes<1>(D0, H1, H2, A);
     SP_CUDA(cudaFuncSetAttribute(ddqn_rows_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,

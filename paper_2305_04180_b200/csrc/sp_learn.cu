@@ -292,14 +292,14 @@ __global__ void __launch_bounds__(kLearnThreads)
 }
 
 // Weight gradients as small GEMMs over the batch, Adam fused into the epilogue.
-// A CTA owns a 16 (fan_in) x 32 (fan_out) tile of one weight matrix:
+// A CTA owns a 16 (fan_in) x 16 (fan_out) tile of one weight matrix:
 //   gW[k][j] = sum_r act[r][k] del[r][j]   (W1: s, d1; W2: a1, d2; W3: a2, dq)
-// with the tile's columns of all B rows staged in shared memory (B x 48 floats);
-// each thread owns 1 x 2 outputs.  Tiles at k0 == 0 also own the bias gradient sum_r del[r][j].
+// with the tile's columns of all B rows staged in shared memory (B x 32 floats);
+// each thread owns one output.  Tiles at k0 == 0 also own the bias gradient sum_r del[r][j].
 // The sums run in row order (deterministic).  Then adam_kernel's update
 // (net.py:141-161), gated on a finite loss (ddqn.py:66-71).  CTA 0 publishes
 // {loss, mean |td|}.
-constexpr int kGradTK = 16, kGradTJ = 32, kMaxGradTiles = 256;
+constexpr int kGradTK = 16, kGradTJ = 16, kMaxGradTiles = 512;
 
 struct GradTiles {
   int n;
@@ -326,12 +326,25 @@ __global__ void __launch_bounds__(256)
                           const double* step_dev, double lr, double b1, double b2, double eps,
                           float* stats_out) {
   extern __shared__ __align__(16) float gsm[];  // As: B x kGradTK, Ds: B x kGradTJ
-  float l = 0.0f, m = 0.0f;
-  for (int t = 0; t < n_row_tiles; ++t) {
-    l += la.lpart[2 * t];
-    m += la.lpart[2 * t + 1];
+  __shared__ float stat_s[2];
+  if (threadIdx.x < 32) {  // the row tiles' loss partials: lane-strided sums + xor tree
+    float l = 0.0f, m = 0.0f;
+    for (int t = threadIdx.x; t < n_row_tiles; t += 32) {
+      l += la.lpart[2 * t];
+      m += la.lpart[2 * t + 1];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      l += __shfl_xor_sync(SP_FULL, l, o);
+      m += __shfl_xor_sync(SP_FULL, m, o);
+    }
+    if (threadIdx.x == 0) {
+      stat_s[0] = l / (float)la.B;
+      stat_s[1] = m / (float)la.B;
+    }
   }
-  const float loss = l / (float)la.B, mad = m / (float)la.B;
+  __syncthreads();
+  const float loss = stat_s[0], mad = stat_s[1];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     stats_out[0] = loss;
     stats_out[1] = mad;
@@ -342,9 +355,8 @@ __global__ void __launch_bounds__(256)
   const float* del = tk == 0 ? la.d1 : tk == 1 ? la.d2 : la.dq;
   const int K = tk == 0 ? la.D0 : tk == 1 ? la.H1 : la.H2;
   const int J = tk == 0 ? la.H1 : tk == 1 ? la.H2 : la.A;
-  const int kk = threadIdx.x >> 4, jp = threadIdx.x & 15;  // outputs (k0+kk, j0+2jp+{0,1})
-  float acc[2] = {0.f, 0.f};
-  float bacc[2] = {0.f, 0.f};
+  const int kk = threadIdx.x >> 4, jp = threadIdx.x & 15;  // output (k0+kk, j0+jp)
+  float acc = 0.f, bacc = 0.f;
   const bool bias_owner = k0 == 0 && kk == 0;
   // the tile's columns of every batch row, staged once (many loads in flight)
   float* As = gsm;
@@ -368,35 +380,18 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
 #pragma unroll 8
   for (int r = 0; r < la.B; ++r) {
-    const float xv = As[r * kGradTK + kk];
-    const float2 dv = *(const float2*)&Ds[r * kGradTJ + 2 * jp];
-    acc[0] = fmaf(xv, dv.x, acc[0]);
-    acc[1] = fmaf(xv, dv.y, acc[1]);
-    if (bias_owner) {
-      bacc[0] += dv.x;
-      bacc[1] += dv.y;
-    }
+    const float dv = Ds[r * kGradTJ + jp];
+    acc = fmaf(As[r * kGradTK + kk], dv, acc);
+    if (bias_owner) bacc += dv;
   }
   const double t = *step_dev + 1.0;
   const float c1 = (float)(1.0 - pow(b1, t));
   const float c2 = (float)(1.0 - pow(b2, t));
   const float fb1 = (float)b1, fb2 = (float)b2, f1b1 = (float)(1.0 - b1),
               f1b2 = (float)(1.0 - b2), flr = (float)lr, feps = (float)eps;
-  const int k = k0 + kk;
-  if (k < K) {
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int j = j0 + 2 * jp + c;
-      if (j < J) adam_one(T, tk, (int64_t)k * J + j, acc[c], c1, c2, fb1, fb2, f1b1, f1b2, flr, feps);
-    }
-  }
-  if (bias_owner) {
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int j = j0 + 2 * jp + c;
-      if (j < J) adam_one(T, tk + 3, j, bacc[c], c1, c2, fb1, fb2, f1b1, f1b2, flr, feps);
-    }
-  }
+  const int k = k0 + kk, j = j0 + jp;
+  if (k < K && j < J) adam_one(T, tk, (int64_t)k * J + j, acc, c1, c2, fb1, fb2, f1b1, f1b2, flr, feps);
+  if (bias_owner && j < J) adam_one(T, tk + 3, j, bacc, c1, c2, fb1, fb2, f1b1, f1b2, flr, feps);
 }
 
 __global__ void adam_tick_stats_kernel(double* step_dev, const float* stats) {
