@@ -141,6 +141,10 @@ int sp_env_write_state(SpEnv* env, int field, const double* host_in, void* strea
 int sp_env_reset_lanes(SpEnv* env, const uint8_t* mask, float* states, void* stream);
 int sp_env_map_info(SpEnv* env, int64_t* slot_of_env /* host n_envs, may be NULL */,
                     int64_t* smem_bytes, int32_t* threads_per_cta, int32_t* ctas);
+/* Launch partition (diagnostics): the step kernel's CTA slot cuts (host
+ * ctas+1, may be NULL) and the SM cycles each CTA took in the last step (host
+ * ctas, may be NULL).  Synchronizes the device. */
+int sp_env_launch_info(SpEnv* env, int64_t* cuts, uint32_t* cta_cycles);
 
 /* LiDAR scan with the fused step's marcher on caller poses (no noise).
  * Queries must be grouped by map: query q of map m lies in

@@ -88,6 +88,7 @@ SIGNATURES = [
     ("sp_env_write_state", ctypes.c_int, [c_vp, ctypes.c_int, c_dp, c_vp]),
     ("sp_env_reset_lanes", ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     ("sp_env_map_info", ctypes.c_int, [c_vp, c_i64p, c_i64p, c_i32p, c_i32p]),
+    ("sp_env_launch_info", ctypes.c_int, [c_vp, c_i64p, c_vp]),
     ("sp_env_scan", ctypes.c_int, [c_vp, ctypes.c_int64, c_i64p, c_vp, c_vp, c_vp, c_vp, c_vp,
                                    c_vp]),
     ("sp_cast_rays", ctypes.c_int,
@@ -147,7 +148,10 @@ def load() -> ctypes.CDLL:
             f"{LIB_PATH} is missing: build it with `python -m paper_2305_04180_b200.build` "
             "(there is no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH)
+    variant = "SPARROW_LIB_PATH" in os.environ  # A/B builds may predate newer entry points
     for name, res, args in SIGNATURES:
+        if variant and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -56,8 +56,9 @@ struct DevDeviceGuard {
 
 // 2x2-block table: a block holding an occupied (or out-of-grid) cell stores
 // 0x80 | mask (bit (dy*2+dx) = cell (2by+dy, 2bx+dx) occupied); a free block
-// stores r = (chessboard distance to the nearest such block) - 1, clamped to
-// 127: the (2r+1)^2 blocks around it are all free.
+// stores k = 2r + 1, r = (chessboard distance to the nearest such block) - 1
+// clamped to 63: the k x k blocks centred on it are all free (the march uses
+// k as is: the box's far cell is (ix | 1) + sx * k).
 void build_block_table(const uint8_t* occ, int H, int W, int Hb, int Wb, uint8_t* out) {
   const int INF = 1 << 29;
   std::vector<int> dist((size_t)Hb * Wb);
@@ -97,7 +98,7 @@ void build_block_table(const uint8_t* occ, int H, int W, int Hb, int Wb, uint8_t
       }
     }
   for (size_t i = 0; i < dist.size(); ++i)
-    out[i] = mask[i] ? (uint8_t)(0x80u | mask[i]) : (uint8_t)std::min(dist[i] - 1, 127);
+    out[i] = mask[i] ? (uint8_t)(0x80u | mask[i]) : (uint8_t)(2 * std::min(dist[i] - 1, 63) + 1);
 }
 
 // every map's border row/column fully occupied (GridMap's invariant,
@@ -366,7 +367,7 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   d.n_actions = cfg->n_actions;
   {
     const int K = (int)std::ceil(cfg->robot_radius_cm / cell);
-    d.need_r = (K + 1) / 2;
+    d.need_k = 2 * ((K + 1) / 2) + 1;
   }
   for (int c = 0; c <= SP_MAX_ACTIONS; ++c) {
     d.action_v[c] = c < cfg->n_actions ? cfg->action_table[2 * c] : 0.0;
@@ -492,6 +493,7 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   int64_t* dcta = nullptr;
   {
     int rc2 = env->alloc(&dcta, plan.cta_begin.size());
+    if (!rc2) rc2 = env->alloc(&d.cta_cyc, plan.cta_begin.size());
     if (rc2) { delete env; return rc2; }
     cudaMemcpy(dcta, plan.cta_begin.data(), 8 * plan.cta_begin.size(), cudaMemcpyHostToDevice);
   }
@@ -813,6 +815,16 @@ int sp_env_map_info(SpEnv* env, int64_t* slot_of_env, int64_t* smem_bytes, int32
   if (smem_bytes) *smem_bytes = (int64_t)env->smem;
   if (threads) *threads = env->threads;
   if (ctas) *ctas = env->grid;
+  return SP_OK;
+}
+
+int sp_env_launch_info(SpEnv* env, int64_t* cuts, uint32_t* cta_cycles) {
+  if (!env) return fail(SP_EINVAL, "null argument");
+  DevDeviceGuard guard(env->device);
+  std::lock_guard<std::mutex> lk(env->mu);
+  SP_CUDA(cudaDeviceSynchronize());
+  if (cuts) SP_CUDA(cudaMemcpy(cuts, env->d.cta_begin, 8 * (size_t)(env->grid + 1), cudaMemcpyDeviceToHost));
+  if (cta_cycles) SP_CUDA(cudaMemcpy(cta_cycles, env->d.cta_cyc, 4 * (size_t)env->grid, cudaMemcpyDeviceToHost));
   return SP_OK;
 }
 

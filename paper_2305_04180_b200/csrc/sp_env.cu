@@ -75,6 +75,10 @@ struct MapView {
   __device__ __forceinline__ uint32_t code(int ix, int iy) const {
     return blk[(iy >> 1) * Wb + (ix >> 1)];
   }
+  // the same byte sign-extended: < 0 for a mixed block, else the box side
+  __device__ __forceinline__ int scode(int ix, int iy) const {
+    return ((const int8_t*)blk)[(iy >> 1) * Wb + (ix >> 1)];
+  }
   __device__ __forceinline__ uint32_t word(int ix, int iy) const {
     return bits[iy * WW + (ix >> 5)];
   }
@@ -88,8 +92,8 @@ __device__ __forceinline__ bool disc_hits(const MapView& mv, const EnvDev& d, do
     return true;  // :124-126
   const int cx = (int)floor(x * d.inv_cell), cy = (int)floor(y * d.inv_cell);
   if (cx >= 0 && cx < d.W && cy >= 0 && cy < d.H) {
-    const uint32_t code = mv.code(cx, cy);  // free box of radius code covers the bbox?
-    if ((code & 0x80u) == 0u && code >= (uint32_t)d.need_r) return false;
+    const uint32_t code = mv.code(cx, cy);  // free box of side code covers the bbox?
+    if ((code & 0x80u) == 0u && code >= (uint32_t)d.need_k) return false;
   }
   int ix0 = (int)floor(ddiv(dsub(x, r), cell)); if (ix0 < 0) ix0 = 0;  // :128-135
   int ix1 = (int)floor(ddiv(dadd(x, r), cell)); if (ix1 > d.W - 1) ix1 = d.W - 1;
@@ -153,7 +157,7 @@ __device__ __forceinline__ int floor_i(double v) {  // floor(v), |v| < 2^31
 // One march step, branch-free: every lane of the warp executes it, and only
 // `live` rays commit.  The block byte is either 0x80 | the occupancy mask of
 // the block's 2x2 cells (then the step is one cell, as _cy.pyx:89-96), or the
-// radius r of the free (2r+1)^2-block box around it (then the ray leaves the
+// side k = 2r+1 of the free k x k-block box around it (then the ray leaves the
 // whole box).  Either way the ray exits through the face with the smaller
 // parameter (ties to x, as tmx <= tmy does) into the cell containing the
 // exit point.  Returns true when a live ray finished.  r.t then holds the
@@ -167,12 +171,12 @@ __device__ __forceinline__ bool ray_step(Ray& r, bool live, const MapView& mv, c
   const bool occupied = cellwise && ((code >> (((r.iy & 1) << 1) | (r.ix & 1))) & 1u);
   // last cell of the free region on each axis: the cell itself, or the box's
   // far cell (ix | 1) + sx * (2r + 1) - fx, written as a face index below
-  const int k = (int)(code << 1) + 1;  // 2r + 1 (unused when cellwise)
-  const int fx = (r.sx + 1) >> 1, fy = (r.sy + 1) >> 1;  // 1 when moving +
+  const int k = (int)code;  // box side 2r + 1 in blocks (unused when cellwise)
+  const int fx = max(r.sx, 0), fy = max(r.sy, 0);  // 1 when moving +
   const int face_x = cellwise ? r.ix + fx : (r.ix | 1) + r.sx * k;
   const int face_y = cellwise ? r.iy + fy : (r.iy | 1) + r.sy * k;
-  const double tx = (i2d(face_x) - r.x0) * r.idx;
-  const double ty = (i2d(face_y) - r.y0) * r.idy;
+  const double tx = ((double)face_x - r.x0) * r.idx;
+  const double ty = ((double)face_y - r.y0) * r.idy;
   const bool xs = tx <= ty;
   const double t = xs ? tx : ty;
   // the cell on the other axis at the exit point, clamped between the current
@@ -809,11 +813,18 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
   __syncthreads();
   SP_STAMP(1);
   uint32_t phase = 0;
+  if (threadIdx.x == 0) bar[1] = (uint64_t)clock64();  // CTA start (kept in smem, not a register)
   const int64_t sb = d.cta_begin[blockIdx.x], se = d.cta_begin[blockIdx.x + 1];
   const int D = d.D;
   const FinObs fin{c, D, d.R_pad, d.max_range, d.inv_max_range, d.proximity, d.lastq};
   int m = 0, cur_map = -1;
+  // shared-memory tables always sit at the start of smem: seeding the view with
+  // that address lets the march fold the table base into its LDS offsets
   MapView mv{};
+  if constexpr (kSmem) {
+    mv.blk = smem;
+    mv.bits = (const uint32_t*)(smem + d.blk_bytes);
+  }
   for (int64_t s0 = sb; s0 < se;) {
     while (d.map_off[m + 1] <= s0) ++m;
     if (m != cur_map) {
@@ -933,6 +944,11 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     SP_STAMP(7);
     s0 += n;
   }
+  if (a.mode == MODE_STEP) {  // per-CTA duration (launch diagnostics: sp_env_launch_info)
+    __syncthreads();
+    if (threadIdx.x == 0)
+      d.cta_cyc[blockIdx.x] = (uint32_t)min(clock64() - (long long)bar[1], (long long)UINT32_MAX);
+  }
 }
 
 // Standalone LiDAR scan on caller poses (cfg4): the same marcher, no noise.
@@ -964,7 +980,13 @@ __global__ void __launch_bounds__(SP_SCAN_THREADS, SP_CTAS_PER_SM)
   uint32_t phase = 0;
   const int64_t sb = q.cta_begin[blockIdx.x], se = q.cta_begin[blockIdx.x + 1];
   int m = 0, cur_map = -1;
+  // shared-memory tables always sit at the start of smem: seeding the view with
+  // that address lets the march fold the table base into its LDS offsets
   MapView mv{};
+  if constexpr (kSmem) {
+    mv.blk = smem;
+    mv.bits = (const uint32_t*)(smem + d.blk_bytes);
+  }
   for (int64_t s0 = sb; s0 < se;) {
     while (q.qoff[m + 1] <= s0) ++m;
     if (m != cur_map) {

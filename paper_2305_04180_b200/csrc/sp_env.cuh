@@ -29,7 +29,7 @@ struct EnvDev {
   int32_t n_maps;
   double cell, inv_cell, max_range, radius, proximity;
   int32_t timeout, spawn_attempts, auto_reset, n_actions;
-  int32_t need_r;         // block-box radius that proves "no disc collision"
+  int32_t need_k;         // block-box side 2r+1 that proves "no disc collision"
   uint32_t blk_bytes;     // per-map block table bytes (16-byte padded)
   uint32_t bits_bytes;    // per-map bitmap bytes
   uint32_t map_bytes;     // blk_bytes + bits_bytes
@@ -63,6 +63,7 @@ struct EnvDev {
   unsigned long long* rec_count;
   uint64_t rec_cap;
   int32_t* err;           // [0] status, [1] env row
+  uint32_t* cta_cyc;      // grid: SM cycles each CTA took in the last MODE_STEP launch
   // launch geometry
   const int64_t* cta_begin;  // grid + 1 slot boundaries (map-aligned when possible)
   int32_t chunk_cap;      // envs per CTA chunk (<= threads per CTA)

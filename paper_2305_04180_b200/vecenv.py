@@ -479,6 +479,16 @@ class VecEnv:
                                   ctypes.byref(ctas))
         return {"smem_bytes": smem.value, "threads_per_cta": thr.value, "ctas": ctas.value}
 
+    def partition(self) -> dict:
+        """The step kernel's CTA slot cuts and the SM cycles each CTA took in
+        the last step (diagnostics; synchronizes the device)."""
+        g = self.launch_info()["ctas"]
+        cuts = np.zeros(g + 1, np.int64)
+        cyc = np.zeros(g, np.uint32)
+        _lib.check(self._lib.sp_env_launch_info(self._h, cuts.ctypes.data_as(_lib.c_i64p),
+                                                cyc.ctypes.data), "launch_info")
+        return {"cuts": cuts, "cta_cycles": cyc}
+
     def scan_raw(self, qoff: np.ndarray, x, y, heading, ranges, hit_cell=None) -> None:
         """Raw launch: device float64 x/y/heading already grouped by map
         (``qoff`` host int64 offsets, n_maps + 1), outputs preallocated."""
