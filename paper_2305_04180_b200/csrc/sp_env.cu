@@ -241,6 +241,11 @@ __device__ __forceinline__ bool ray_setup(Ray& r, double x0, double y0, double c
 struct Chunk {
   double *px, *py, *ch, *sh, *sig;  // per slot: scan origin, heading cos/sin, noise std
   uint64_t* nctr;  // per slot: first Philox block of the slot's LiDAR noise
+  double* retp;    // per env: episode return before this step (prefetched in phase A)
+  double* part;    // per env: shaped reward without its proximity term
+  int32_t* rowi;   // per env: caller row
+  int32_t* send;   // per env: episode length before any reset
+  int8_t* evs;     // per env: event awaiting phase C, or -1 (nothing left to do)
   uint32_t* gid;   // per slot: the env's stream lane (global env id)
   int32_t* list;   // slots in dispatch order (longest predicted scan first)
   int32_t* reg;    // slots in registration order
@@ -263,7 +268,9 @@ __device__ __forceinline__ Chunk chunk_smem(uint8_t* base, int cap, int slots, i
   c.sh = c.ch + slots;
   c.sig = c.sh + slots;
   c.nctr = (uint64_t*)(c.sig + slots);
-  c.stage = (float*)(c.nctr + slots);
+  c.retp = (double*)(c.nctr + slots);
+  c.part = c.retp + cap;
+  c.stage = (float*)(c.part + cap);
   c.gid = (uint32_t*)(c.stage + (size_t)slots * D);
   c.list = (int32_t*)(c.gid + slots);
   c.reg = c.list + slots;
@@ -271,8 +278,11 @@ __device__ __forceinline__ Chunk chunk_smem(uint8_t* base, int cap, int slots, i
   c.hwrite = c.hread + slots;
   c.xslot = c.hwrite + slots;
   c.ctl = c.xslot + cap;
-  c.wmode = (uint8_t*)(c.ctl + 20);
-  c.prox = c.wmode + cap;
+  c.rowi = c.ctl + 20;
+  c.send = c.rowi + cap;
+  c.wmode = (uint8_t*)(c.send + cap);
+  c.evs = (int8_t*)(c.wmode + cap);
+  c.prox = (uint8_t*)(c.evs + cap);
   c.sbucket = c.prox + slots;
   (void)R;
   return c;
@@ -631,7 +641,7 @@ __device__ __forceinline__ void write_rows(const EnvDev& d, const StepArgs& a, c
     const int k = f - e * D;
     const uint8_t w = c.wmode[e];
     if (w == W_NONE) continue;
-    const int64_t o = d.env_of_slot[s0 + e] * D + k;
+    const int64_t o = (int64_t)c.rowi[e] * D + k;
     const float own = c.stage[e * D + k];
     if (w != W_STATE) a.store_states[o] = own;
     if (w != W_RESET_OV) a.states[o] = w == W_RESET_X ? c.stage[c.xslot[e] * D + k] : own;
@@ -752,29 +762,33 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
   return r;
 }
 
-// Phase C of one env in MODE_STEP (vecenv.py:96-112): reward with the
-// proximity term from its scan, the per-env outputs and the VecEnv statistics.
+// The per-env outputs and VecEnv statistics of one live env in MODE_STEP
+// (vecenv.py:96-112), given the episode return before the step.  The reward
+// is terminal (-10 / +75) or the shaped partial plus the proximity term from
+// the env's scan, so collisions and arrivals finish in phase A and only
+// running / timed-out envs wait for phase C.
 __device__ __forceinline__ void finish_env(const EnvDev& d, const StepArgs& a, const Chunk& c,
-                                           int e, int64_t s, int64_t row, const StepA& r) {
-  const double rew = r.ev == 1 ? -10.0
-                   : r.ev == 2 ? 75.0
-                             : dadd(r.partial, dmul(0.1, c.prox[e] ? -1.0 : 0.0));
+                                           int e, int64_t s, int64_t row, int8_t ev,
+                                           double partial, int32_t step_end, double ret_prev) {
+  const double rew = ev == 1 ? -10.0
+                   : ev == 2 ? 75.0
+                             : dadd(partial, dmul(0.1, c.prox[e] ? -1.0 : 0.0));
   a.rewards[row] = rew;
-  a.dones[row] = (uint8_t)(r.ev == 1 || r.ev == 2);
-  a.truncated[row] = (uint8_t)(r.ev == 3);
-  a.events[row] = r.ev;
-  double ret = dadd(d.ret[s], rew);  // vecenv.py:96-112
-  if (r.ended) {
+  a.dones[row] = (uint8_t)(ev == 1 || ev == 2);
+  a.truncated[row] = (uint8_t)(ev == 3);
+  a.events[row] = ev;
+  double ret = dadd(ret_prev, rew);  // vecenv.py:96-112
+  if (ev != 0) {
     d.episodes[s] += 1;
     d.return_sum[s] = dadd(d.return_sum[s], ret);
-    if (r.ev == 2) d.arrivals[s] += 1;
+    if (ev == 2) d.arrivals[s] += 1;
     const unsigned long long kk = atomicAdd(d.rec_count, 1ull);
     d.rec_ret[kk % d.rec_cap] = ret;
     d.rec_key[kk % d.rec_cap] = (a.step_index << 32) | (uint64_t)row;
     if (d.first_event[s] < 0) {
-      d.first_event[s] = r.ev;
+      d.first_event[s] = ev;
       d.first_ret[s] = ret;
-      d.first_steps[s] = r.step_end;
+      d.first_steps[s] = step_end;
     }
     ret = 0.0;
     if (!d.auto_reset || c.wmode[e] == W_RESET_OV) d.needs_reset[s] = 1;
@@ -853,6 +867,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     // them its tail); the rest is done after phase A
     const int kpre = a.mode == MODE_STEP
                          ? min(n, 12 * max(0, (int)blockDim.x - n) / d.nb) : 0;
+    if (act) c.rowi[e] = (int32_t)row;
     if (act && e < kpre) {  // the post-step scan's noise stream (add_slot writes the same)
       c.nctr[e] = ctr;
       c.gid[e] = gid;
@@ -861,13 +876,10 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     if (kpre > 0 && !act) prenoise(d, c, kpre, n);
 
     // ---- A: physics, collision, events, reward partial, resets -----------
-    bool live = false, ended = false;
-    int8_t ev = 0;
-    int32_t step_end = 0;  // episode length before any reset in phase A
-    double partial = 0.0;
     if (act) {
       c.xslot[e] = -1;
       c.wmode[e] = W_NONE;
+      c.evs[e] = -1;
     }
     if (a.mode != MODE_STEP) {
       const bool want = a.mode == MODE_RESET_ALL || (act && a.reset_mask[row] != 0);
@@ -884,13 +896,19 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
         d.ctr[s] = ctr;
       }
     } else if (act) {
+      const double ret_prev = d.ret[s];  // issued early: only the outputs wait on it
       const StepA r = step_env(d, a, mv, mc, c, e, s, row, gid, ctr, d.chunk_cap, d.slot_cap);
-      live = r.live;
-      ended = r.ended;
-      ev = r.ev;
-      step_end = r.step_end;
-      partial = r.partial;
       d.ctr[s] = ctr;
+      if (r.live) {
+        if (r.ev == 1 || r.ev == 2) {  // terminal reward: no scan needed
+          finish_env(d, a, c, e, s, row, r.ev, 0.0, r.step_end, ret_prev);
+        } else {
+          c.evs[e] = r.ev;
+          c.part[e] = r.partial;
+          c.send[e] = r.step_end;
+          c.retp[e] = ret_prev;
+        }
+      }
     }
     __syncthreads();
     SP_STAMP(3);
@@ -903,16 +921,9 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     ray_phase<kBordered, false>(mv, d, c, beam, n_slots, fin);
     __syncthreads();
     SP_STAMP(5);
-    // ---- C: reward, outputs, statistics ------------------------------------
-    if (live) {
-      StepA r;
-      r.live = live;
-      r.ended = ended;
-      r.ev = ev;
-      r.step_end = step_end;
-      r.partial = partial;
-      finish_env(d, a, c, e, s, row, r);
-    }
+    // ---- C: reward, outputs, statistics of running / timed-out envs --------
+    if (act && c.evs[e] >= 0)
+      finish_env(d, a, c, e, s, c.rowi[e], c.evs[e], c.part[e], c.send[e], c.retp[e]);
     SP_STAMP(6);
     write_rows(d, a, c, s0, n, cta_grp());
     // ---- overflow pass: resets that did not fit the extra slots (rare) -----
@@ -922,10 +933,11 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       __syncthreads();
       if (act && c.wmode[e] == W_RESET_OV) {
         uint64_t ctr2 = d.ctr[s];
-        if (reset_env(d, mv, mc, s, gid, ctr2, c, e)) {
+        const int64_t row2 = c.rowi[e];
+        if (reset_env(d, mv, mc, s, (uint32_t)(d.env_id_offset + row2), ctr2, c, e)) {
           c.wmode[e] = W_STATE;
         } else {
-          set_error(d, SP_EMAP, row);
+          set_error(d, SP_EMAP, row2);
           c.wmode[e] = W_NONE;
         }
         d.ctr[s] = ctr2;
