@@ -154,8 +154,10 @@ __device__ __forceinline__ int floor_i(double v) {  // floor(v), |v| < 2^31
   return __double2loint(__dadd_rd(v, 4503599627370496.0));
 }
 
-// One march step, branch-free: every lane of the warp executes it, and only
-// `live` rays commit.  The block byte is either 0x80 | the occupancy mask of
+// One march step, branch-free: every lane of the warp executes it.  A
+// finished ray is a fixed point (it stays in its occupied cell, or re-derives
+// the same over-range exit without moving), so idle and finished rays can keep
+// stepping without a liveness test.  The block byte is either 0x80 | the occupancy mask of
 // the block's 2x2 cells (then the step is one cell, as _cy.pyx:89-96), or the
 // side k = 2r+1 of the free k x k-block box around it (then the ray leaves the
 // whole box).  Either way the ray exits through the face with the smaller
@@ -165,7 +167,7 @@ __device__ __forceinline__ int floor_i(double v) {  // floor(v), |v| < 2^31
 // (ray_range), and ray_hit() recovers the occupied cell it stopped in.
 // kBordered: every map has an occupied border, so no step can leave the grid.
 template <bool kBordered>
-__device__ __forceinline__ bool ray_step(Ray& r, bool live, const MapView& mv, const EnvDev& d) {
+__device__ __forceinline__ bool ray_step(Ray& r, const MapView& mv, const EnvDev& d) {
   const uint32_t code = mv.code(r.ix, r.iy);
   const bool cellwise = code >= 0x80u;
   const bool occupied = cellwise && ((code >> (((r.iy & 1) << 1) | (r.ix & 1))) & 1u);
@@ -190,15 +192,28 @@ __device__ __forceinline__ bool ray_step(Ray& r, bool live, const MapView& mv, c
   const bool over = t > d.max_range;  // :97-99
   const bool out = !kBordered && ((unsigned)nx >= (unsigned)d.W || (unsigned)ny >= (unsigned)d.H);
   const bool finished = occupied || over || out;
-  r.n += live ? 1 : 0;
-  if (live && !occupied) {
+  if (!occupied) {
     r.t = t;
     if (!finished) {
       r.ix = nx;
       r.iy = ny;
+      r.n += 1;
     }
   }
-  return live && finished;
+  return finished;
+}
+
+// A parked ray: a finished fixed point for the lanes of a ray slot with no
+// ray (on bordered maps cell (0, 0) is occupied; otherwise the ray drifts out
+// of the grid or past max_range and stops there).
+__device__ __forceinline__ void ray_park(Ray& r) {
+  r.ix = r.iy = 0;
+  r.sx = r.sy = 1;
+  r.n = 0;
+  r.x0 = r.y0 = 0.5;
+  r.dx = r.dy = 1.0;
+  r.idx = r.idy = 1.0;
+  r.t = 0.0;
 }
 
 // range of a finished ray (the over-range exit clips to max_range)
@@ -308,29 +323,26 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
   const int total = n_env * R;
   const int lane = threadIdx.x & 31;
   const unsigned lt = lanemask_lt();
-  bool act_a = false, act_b = false, done_a = false, done_b = false;
+  // busy: the slot holds a ray not yet retired; fin: the slot's ray has
+  // finished (parked slots count as finished)
+  bool busy_a = false, busy_b = false, fin_a = true, fin_b = true;
   bool drained = total == 0;
   int ea = 0, ja = 0, eb = 0, jb = 0;
   Ray ra, rb;
-  ra.ix = ra.iy = rb.ix = rb.iy = 0;
-  ra.sx = ra.sy = rb.sx = rb.sy = 1;
-  ra.n = rb.n = 0;
-  ra.x0 = ra.y0 = rb.x0 = rb.y0 = 0.5;
-  ra.dx = ra.dy = rb.dx = rb.dy = 1.0;
-  ra.idx = ra.idy = rb.idx = rb.idy = 1.0;
-  ra.t = rb.t = 0.0;
+  ray_park(ra);
+  ray_park(rb);
   for (;;) {
-    const unsigned ia = __ballot_sync(SP_FULL, !act_a);
-    const unsigned ib = __ballot_sync(SP_FULL, !act_b);
+    const unsigned ia = __ballot_sync(SP_FULL, fin_a);
+    const unsigned ib = __ballot_sync(SP_FULL, fin_b);
     const int na = __popc(ia), n_idle = na + __popc(ib);
     if (n_idle >= d.refill_min || drained) {
-      if (done_a) {
-        fin(ea, ja, ray_range(ra, d), kHit ? ray_hit(ra, mv, d) : -1, ra.n);
-        done_a = false;
+      if (busy_a && fin_a) {  // steps taken = moves + the finishing step
+        fin(ea, ja, ray_range(ra, d), kHit ? ray_hit(ra, mv, d) : -1, ra.n + 1);
+        busy_a = false;
       }
-      if (done_b) {
-        fin(eb, jb, ray_range(rb, d), kHit ? ray_hit(rb, mv, d) : -1, rb.n);
-        done_b = false;
+      if (busy_b && fin_b) {
+        fin(eb, jb, ray_range(rb, d), kHit ? ray_hit(rb, mv, d) : -1, rb.n + 1);
+        busy_b = false;
       }
       if (drained) {
         if ((ia & ib) == SP_FULL) break;
@@ -341,33 +353,39 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
         if (base + n_idle >= total) drained = true;
         const int my_a = base + __popc(ia & lt);
         const int my_b = base + na + __popc(ib & lt);
-        if (!act_a && my_a < total) {
+        if (fin_a && my_a < total) {
           const int g = div_r(my_a, d);
           ea = c.list[g];
           ja = my_a - g * R;
-          act_a = !ray_setup(ra, c.px[ea], c.py[ea], c.ch[ea], c.sh[ea], beam[ja], d);
-          done_a = !act_a;
+          if (ray_setup(ra, c.px[ea], c.py[ea], c.ch[ea], c.sh[ea], beam[ja], d)) {
+            fin(ea, ja, 0.0, -1, 1);  // origin outside the grid: range 0 (_cy.pyx:37-39)
+            ray_park(ra);
+          } else {
+            busy_a = true;
+            fin_a = false;
+          }
         }
-        if (!act_b && my_b < total) {
+        if (fin_b && my_b < total) {
           const int g = div_r(my_b, d);
           eb = c.list[g];
           jb = my_b - g * R;
-          act_b = !ray_setup(rb, c.px[eb], c.py[eb], c.ch[eb], c.sh[eb], beam[jb], d);
-          done_b = !act_b;
+          if (ray_setup(rb, c.px[eb], c.py[eb], c.ch[eb], c.sh[eb], beam[jb], d)) {
+            fin(eb, jb, 0.0, -1, 1);
+            ray_park(rb);
+          } else {
+            busy_b = true;
+            fin_b = false;
+          }
         }
       }
     }
     // two march steps per slot between refill checks (halves the loop's
     // vote/branch overhead per step); a ray that finishes in the first step
-    // sits out the second (live = act)
+    // stays put in the second
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-      const bool fa = ray_step<kBordered>(ra, act_a, mv, d);
-      const bool fb = ray_step<kBordered>(rb, act_b, mv, d);
-      act_a = act_a && !fa;
-      act_b = act_b && !fb;
-      done_a = done_a || fa;
-      done_b = done_b || fb;
+      fin_a = ray_step<kBordered>(ra, mv, d);
+      fin_b = ray_step<kBordered>(rb, mv, d);
     }
   }
 }
