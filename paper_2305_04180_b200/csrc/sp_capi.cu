@@ -55,7 +55,8 @@ struct DevDeviceGuard {
 };
 
 // 2x2-block table: a block holding an occupied (or out-of-grid) cell stores
-// 0x80 | mask (bit (dy*2+dx) = cell (2by+dy, 2bx+dx) occupied); a free block
+// 0x80 | mask, where cell (ix, iy) = (2bx+dx, 2by+dy) is bit (ix + 2 iy) & 3
+// = dx + 2 ((bx + dy) & 1) (the march tests it with one shift-add); a free block
 // stores k = 2r + 1, r = (chessboard distance to the nearest such block) - 1
 // clamped to 63: the k x k blocks centred on it are all free (the march uses
 // k as is: the box's far cell is (ix | 1) + sx * k).
@@ -69,7 +70,7 @@ void build_block_table(const uint8_t* occ, int H, int W, int Hb, int Wb, uint8_t
       for (int dy = 0; dy < 2; ++dy)
         for (int dx = 0; dx < 2; ++dx) {
           const int iy = 2 * by + dy, ix = 2 * bx + dx;
-          if (iy >= H || ix >= W || occ[(size_t)iy * W + ix]) mk |= (uint8_t)(1u << (dy * 2 + dx));
+          if (iy >= H || ix >= W || occ[(size_t)iy * W + ix]) mk |= (uint8_t)(1u << ((ix + 2 * iy) & 3));
         }
       mask[(size_t)by * Wb + bx] = mk;
       // outside the block grid counts as blocked: distance to the border

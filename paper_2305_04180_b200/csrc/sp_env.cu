@@ -168,9 +168,9 @@ __device__ __forceinline__ int floor_i(double v) {  // floor(v), |v| < 2^31
 // kBordered: every map has an occupied border, so no step can leave the grid.
 template <bool kBordered>
 __device__ __forceinline__ bool ray_step(Ray& r, const MapView& mv, const EnvDev& d) {
-  const uint32_t code = mv.code(r.ix, r.iy);
-  const bool cellwise = code >= 0x80u;
-  const bool occupied = cellwise && ((code >> (((r.iy & 1) << 1) | (r.ix & 1))) & 1u);
+  const int code = mv.scode(r.ix, r.iy);  // < 0: mixed block
+  const bool cellwise = code < 0;
+  const bool occupied = cellwise && ((code >> ((r.ix + (r.iy << 1)) & 3)) & 1);
   // last cell of the free region on each axis: the cell itself, or the box's
   // far cell (ix | 1) + sx * (2r + 1) - fx, written as a face index below
   const int k = (int)code;  // box side 2r + 1 in blocks (unused when cellwise)
@@ -226,7 +226,7 @@ __device__ __forceinline__ double ray_range(const Ray& r, const EnvDev& d) {
 __device__ __forceinline__ int ray_hit(const Ray& r, const MapView& mv, const EnvDev& d) {
   if ((unsigned)r.ix >= (unsigned)d.W || (unsigned)r.iy >= (unsigned)d.H) return -1;
   const uint32_t code = mv.code(r.ix, r.iy);
-  const bool occ = code >= 0x80u && ((code >> (((r.iy & 1) << 1) | (r.ix & 1))) & 1u);
+  const bool occ = code >= 0x80u && ((code >> ((r.ix + (r.iy << 1)) & 3)) & 1u);
   return occ ? r.iy * d.W + r.ix : -1;
 }
 
