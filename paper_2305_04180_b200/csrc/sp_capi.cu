@@ -229,7 +229,7 @@ static int extra_slots(int cap) { return std::max(32, cap / 8); }
 static size_t chunk_bytes(int cap, int D, int R) {
   const size_t slots = (size_t)cap + extra_slots(cap);
   (void)R;
-  return slots * (74 + 4 * (size_t)D) + 30 * (size_t)cap + 96;
+  return slots * (78 + 4 * (size_t)D) + 30 * (size_t)cap + 96;
 }
 
 static Plan plan_launch(SpEnv* env, const std::vector<int64_t>& off, bool staging = true) {
@@ -446,8 +446,11 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   TRY(env->alloc(&d.step, n));
   TRY(env->alloc(&d.delay, n));
   TRY(env->alloc(&d.needs_reset, n, 1));
-  d.R_pad = (env->R + 3) & ~3;
-  TRY(env->alloc(&d.lastq, n * (size_t)d.R_pad, 0x18));  // no history yet: 24 steps
+  TRY(env->alloc(&d.qsum, n));
+  {  // no history yet: 24 steps per beam (scans without history sort longest)
+    std::vector<uint32_t> q(n, 24u * (uint32_t)env->R);
+    cudaMemcpy(d.qsum, q.data(), 4 * n, cudaMemcpyHostToDevice);
+  }
   TRY(env->alloc(&d.episodes, n));
   TRY(env->alloc(&d.arrivals, n));
   TRY(env->alloc(&d.first_event, n, 0xff));

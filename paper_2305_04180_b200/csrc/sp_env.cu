@@ -266,6 +266,7 @@ struct Chunk {
   int32_t* reg;    // slots in registration order
   int32_t* hread;  // per slot: global slot whose step-count history predicts this scan, or -1
   int32_t* hwrite; // per slot: global slot whose history this scan refreshes, or -1
+  uint32_t* qacc;  // per slot: march steps its rays took (shared atomics)
   int32_t* xslot;  // per env: post-reset slot, -1 if none
   uint8_t* wmode;  // per env: which rows to write (see kernel)
   uint8_t* prox;   // per slot: some ray ended closer than the proximity range
@@ -291,7 +292,8 @@ __device__ __forceinline__ Chunk chunk_smem(uint8_t* base, int cap, int slots, i
   c.reg = c.list + slots;
   c.hread = c.reg + slots;
   c.hwrite = c.hread + slots;
-  c.xslot = c.hwrite + slots;
+  c.qacc = (uint32_t*)(c.hwrite + slots);
+  c.xslot = (int32_t*)(c.qacc + slots);
   c.ctl = c.xslot + cap;
   c.rowi = c.ctl + 20;
   c.send = c.rowi + cap;
@@ -404,13 +406,17 @@ __device__ __forceinline__ int work_bucket(uint32_t steps) {
 // predicted bucket of one scan (called by the thread that registers it)
 __device__ __forceinline__ uint8_t scan_bucket(const EnvDev& d, int32_t hread) {
   if (hread < 0) return 0;
-  const uint32_t* q = (const uint32_t*)(d.lastq + (int64_t)hread * d.R_pad);
-  uint32_t sum = 0;
-  for (int w = 0; w < (d.R + 3) >> 2; ++w) {
-    const uint32_t v = q[w];
-    sum += (v & 0xff) + ((v >> 8) & 0xff) + ((v >> 16) & 0xff) + (v >> 24);
+  return (uint8_t)work_bucket(d.qsum[hread] / (uint32_t)d.R);
+}
+
+// Refresh the lanes' step-count history from this chunk's scans (after a ray
+// phase, before its slots are reused): the n_slots registered slots c.reg[].
+__device__ __forceinline__ void store_history(const EnvDev& d, const Chunk& c, int n_slots) {
+  for (int k = threadIdx.x; k < n_slots; k += blockDim.x) {
+    const int slot = c.reg[k];
+    const int hw = c.hwrite[slot];
+    if (hw >= 0) d.qsum[hw] = c.qacc[slot];
   }
-  return (uint8_t)work_bucket(sum / (uint32_t)d.R_pad);
 }
 
 // The threads that cooperate on a phase: the whole CTA (barrier 0 =
@@ -538,17 +544,15 @@ __device__ __forceinline__ void header_row(const MapConst& mc, double x, double 
 // is "some ray < 30", core.py:205).
 struct FinObs {
   Chunk c;
-  int D, R_pad;
+  int D;
   double max_range, inv_max_range, proximity;
-  uint8_t* lastq;
   __device__ __forceinline__ void operator()(int slot, int j, double t, int, int steps) const {
     float* rowp = c.stage + slot * D;
     const double z = (double)rowp[5 + j];
     const double v = dclip(dadd(t, dadd(0.0, dmul(c.sig[slot], z))), 0.0, max_range);
     rowp[5 + j] = (float)div_by(v, max_range, inv_max_range);
     if (t < proximity) c.prox[slot] = 1;
-    const int hw = c.hwrite[slot];
-    if (hw >= 0) lastq[(int64_t)hw * R_pad + j] = (uint8_t)min(steps, 254);
+    atomicAdd(&c.qacc[slot], (uint32_t)steps);
   }
 };
 
@@ -591,6 +595,7 @@ __device__ __forceinline__ void add_slot(const EnvDev& d, const Chunk& c, int sl
   c.gid[slot] = gid;
   c.nctr[slot] = nctr;
   c.prox[slot] = 0;
+  c.qacc[slot] = 0;
   c.reg[atomicAdd(&c.ctl[1], 1)] = slot;
 }
 
@@ -848,7 +853,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
   if (threadIdx.x == 0) bar[1] = (uint64_t)clock64();  // CTA start (kept in smem, not a register)
   const int64_t sb = d.cta_begin[blockIdx.x], se = d.cta_begin[blockIdx.x + 1];
   const int D = d.D;
-  const FinObs fin{c, D, d.R_pad, d.max_range, d.inv_max_range, d.proximity, d.lastq};
+  const FinObs fin{c, D, d.max_range, d.inv_max_range, d.proximity};
   int m = 0, cur_map = -1;
   // shared-memory tables always sit at the start of smem: seeding the view with
   // that address lets the march fold the table base into its LDS offsets
@@ -939,6 +944,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     ray_phase<kBordered, false>(mv, d, c, beam, n_slots, fin);
     __syncthreads();
     SP_STAMP(5);
+    store_history(d, c, n_slots);
     // ---- C: reward, outputs, statistics of running / timed-out envs --------
     if (act && c.evs[e] >= 0)
       finish_env(d, a, c, e, s, c.rowi[e], c.evs[e], c.part[e], c.send[e], c.retp[e]);
@@ -969,6 +975,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       __syncthreads();
       ray_phase<kBordered, false>(mv, d, c, beam, n2, fin);
       __syncthreads();
+      store_history(d, c, n2);
       write_rows(d, a, c, s0, n, cta_grp());
     }
     SP_STAMP(7);

@@ -392,6 +392,31 @@ def test_many_resets_in_one_step_use_the_overflow_pass():
         assert_close(g.store_states.cpu().numpy(), c.store_states, atol=ATOL_OBS, what="store")
 
 
+def test_mass_timeouts_across_all_ctas():
+    """4096 lanes on 16 maps (every CTA busy) all time out on the same steps:
+    every chunk takes the reset path at once (reset slots, step-count history
+    of reset scans) and the rows still match the oracle."""
+    from paper_2305_04180_b200 import VecEnv
+    from oracle.oracle import OracleVecEnv
+    from helpers import ATOL_OBS, assert_close
+    import torch
+    maps = load_maps(16)
+    cfg = config(32, timeout_steps=4)
+    n = 4096
+    gpu = VecEnv(maps, n, ranges(0.3), cfg)
+    cpu = OracleVecEnv(maps, n, ranges(0.3), cfg)
+    gpu.reset_all(5)
+    cpu.reset_all(5)
+    for t in range(13):
+        a = np.zeros(n, dtype=np.int64)  # slow turns: lanes survive to the timeout
+        g, c = gpu.step_batch(a), cpu.step_batch(a)
+        torch.cuda.synchronize()
+        assert np.array_equal(g.events.cpu().numpy(), c.events), t
+        assert_close(g.states.cpu().numpy(), c.states, atol=ATOL_OBS, what=f"states {t}")
+        assert_close(g.store_states.cpu().numpy(), c.store_states, atol=ATOL_OBS, what="store")
+    gpu.check()
+
+
 def test_step_host_matches_device_step():
     """VecEnv.step_host (numpy in, numpy StepBatch out through page-locked
     buffers) gives the same StepBatch as the device path."""
