@@ -17,6 +17,8 @@ for n in (65536,):
                     torch.empty(n, dtype=torch.bool, device=dev), torch.empty(n, dtype=torch.bool, device=dev),
                     torch.empty((n, D), device=dev), torch.empty(n, dtype=torch.int8, device=dev))
     acts = torch.randint(0, 5, (n,), device=dev)
+    if os.environ.get("ACTIONS") == "turn":  # no collisions: phase A without resets
+        acts = torch.zeros(n, dtype=torch.int64, device=dev)
     for k in range(int(os.environ.get("STEPS", "10"))):
         env.step_device(acts.data_ptr(), out)
     torch.cuda.synchronize()
