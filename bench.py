@@ -280,6 +280,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2305_04180_b200.dist import pooled_stats
     t0 = time.perf_counter()
     pooled = pooled_stats(env)
+    pooled["recent_returns"] = len(pooled["recent_returns"])  # the count, not the list
     t_allreduce_ms = (time.perf_counter() - t0) * 1e3
 
     # ---- e2e through the public API with host buffers -----------------------

@@ -124,6 +124,10 @@ int sp_env_stats_read(SpEnv* env, int64_t* episodes, int64_t* arrivals, double* 
                       void* stream);
 /* last <=256 finished-episode returns in (step, env) order (vecenv.py:79,105) */
 int sp_env_recent_returns(SpEnv* env, double* out256, int32_t* n_out, void* stream);
+/* The same with each return's order key (step << 32) | global env id, so the
+ * shards of a multi-GPU run merge into the single-process deque (dist.py). */
+int sp_env_recent_returns_keyed(SpEnv* env, double* out256, uint64_t* keys256, int32_t* n_out,
+                                void* stream);
 int sp_env_stats_reset(SpEnv* env, int clear_recent, void* stream);
 /* device totals {episodes, arrivals, return_sum} as 3 doubles (all-reduce payload) */
 int sp_env_stats_totals(SpEnv* env, double* dev_out3, void* stream);

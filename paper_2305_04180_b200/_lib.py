@@ -82,6 +82,7 @@ SIGNATURES = [
     ("sp_env_any_needs_reset", ctypes.c_int, [c_vp, c_vp, c_i32p]),
     ("sp_env_stats_read", ctypes.c_int, [c_vp, c_i64p, c_i64p, c_dp, c_i8p, c_dp, c_i64p, c_vp]),
     ("sp_env_recent_returns", ctypes.c_int, [c_vp, c_dp, c_i32p, c_vp]),
+    ("sp_env_recent_returns_keyed", ctypes.c_int, [c_vp, c_dp, c_vp, c_i32p, c_vp]),
     ("sp_env_stats_reset", ctypes.c_int, [c_vp, ctypes.c_int, c_vp]),
     ("sp_env_stats_totals", ctypes.c_int, [c_vp, c_vp, c_vp]),
     ("sp_env_read_state", ctypes.c_int, [c_vp, ctypes.c_int, c_dp, c_vp]),

@@ -678,7 +678,15 @@ int sp_env_stats_read(SpEnv* env, int64_t* episodes, int64_t* arrivals, double* 
   return SP_OK;
 }
 
+int sp_env_recent_returns_keyed(SpEnv* env, double* out256, uint64_t* keys256, int32_t* n_out,
+                                void* stream);
+
 int sp_env_recent_returns(SpEnv* env, double* out256, int32_t* n_out, void* stream) {
+  return sp_env_recent_returns_keyed(env, out256, nullptr, n_out, stream);
+}
+
+int sp_env_recent_returns_keyed(SpEnv* env, double* out256, uint64_t* keys256, int32_t* n_out,
+                                void* stream) {
   if (!env || !out256 || !n_out) return fail(SP_EINVAL, "null argument");
   DevDeviceGuard guard(env->device);
   cudaStream_t st = (cudaStream_t)stream;
@@ -701,7 +709,13 @@ int sp_env_recent_returns(SpEnv* env, double* out256, int32_t* n_out, void* stre
               return x.first < y.first;
             });
   const size_t take = std::min<size_t>(256, items.size());
-  for (size_t i = 0; i < take; ++i) out256[i] = items[items.size() - take + i].second;
+  for (size_t i = 0; i < take; ++i) {
+    const auto& it = items[items.size() - take + i];
+    out256[i] = it.second;
+    if (keys256)  // (step << 32) | global env id: merges across shards (dist.py)
+      keys256[i] = (it.first & ~0xffffffffull) |
+                   (uint64_t)(uint32_t)((it.first & 0xffffffffull) + (uint64_t)env->d.env_id_offset);
+  }
   *n_out = (int32_t)take;
   return SP_OK;
 }

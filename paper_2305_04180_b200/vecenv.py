@@ -435,6 +435,17 @@ class VecEnv:
                                                    ctypes.byref(n), self._stream()), "stats")
         return buf[: n.value].tolist()
 
+    def recent_returns_keyed(self):
+        """(keys, returns) of the last <= 256 episode returns, keys =
+        (step << 32) | global env id in append order (dist.merge_recent_returns)."""
+        buf = np.empty(256, np.float64)
+        keys = np.empty(256, np.uint64)
+        n = ctypes.c_int32(0)
+        _lib.check(self._lib.sp_env_recent_returns_keyed(
+            self._h, buf.ctypes.data_as(_lib.c_dp), keys.ctypes.data, ctypes.byref(n),
+            self._stream()), "stats")
+        return keys[: n.value].copy(), buf[: n.value].copy()
+
     def snapshot_stats(self, reset: bool = False) -> StatsSnapshot:  # vecenv.py:120-132
         self.check()
         st = self._per_copy_arrays()

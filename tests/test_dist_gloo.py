@@ -78,3 +78,43 @@ def test_two_rank_sharding_matches_single_process(tmp_path):
         assert np.array_equal(z["obs"], obs[:, off:off + n]), f"rank {r} lanes differ"
         np.testing.assert_allclose(z["totals"], want, rtol=1e-12)
     assert want[0] > 0
+
+
+def _gather_run(rank, world, port, out):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    from paper_2305_04180_b200.dist import gather_recent_returns
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # rank r's lanes are global ids r*1000 + i; uneven counts per rank
+    n = 200 + 70 * rank
+    steps = np.arange(n) // 7
+    ids = rank * 1000 + np.arange(n) % 7
+    keys = (steps.astype(np.uint64) << np.uint64(32)) | ids.astype(np.uint64)
+    vals = rank * 1e3 + np.arange(n, dtype=np.float64)
+    merged = gather_recent_returns(keys[-256:], vals[-256:])
+    np.save(os.path.join(out, f"gather{rank}.npy"), np.array(merged))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_recent_returns_gather(tmp_path):
+    """dist.gather_recent_returns (world size 2, gloo): every rank gets the
+    merged (step, global env id)-ordered last 256 returns of all ranks."""
+    import torch.multiprocessing as mp
+    from paper_2305_04180_b200.dist import merge_recent_returns
+    port = _free_port()
+    mp.start_processes(_gather_run, args=(2, port, str(tmp_path)), nprocs=2, join=True,
+                       start_method="spawn")
+    shards = []
+    for rank in range(2):
+        n = 200 + 70 * rank
+        steps = np.arange(n) // 7
+        ids = rank * 1000 + np.arange(n) % 7
+        keys = (steps.astype(np.uint64) << np.uint64(32)) | ids.astype(np.uint64)
+        vals = rank * 1e3 + np.arange(n, dtype=np.float64)
+        shards.append((keys[-256:], vals[-256:]))
+    want = merge_recent_returns(shards)
+    assert len(want) == 256
+    for rank in range(2):
+        assert np.load(tmp_path / f"gather{rank}.npy").tolist() == want

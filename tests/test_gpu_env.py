@@ -279,6 +279,33 @@ def test_lanes_are_independent_of_batch_and_shard():  # test_vecenv.py:42-67 (+ 
     assert np.array_equal(fs[:, 7:8], so)
 
 
+def test_sharded_recent_returns_merge_into_the_single_run_deque():  # vecenv.py:79, 109
+    """Shards' keyed recent returns (step, global env id) merge into exactly
+    the deque(maxlen=256) of one VecEnv stepping every id (dist.py)."""
+    from paper_2305_04180_b200 import VecEnv
+    from paper_2305_04180_b200.dist import merge_recent_returns, pooled_stats
+    maps = load_maps(4)
+    n, cfg, seed = 300, config(32, timeout_steps=9), 13
+    full = VecEnv(maps, n, _rg(), cfg)
+    full.reset_all(seed)
+    shards = [VecEnv(maps, 120, _rg(), cfg, env_id_offset=0),
+              VecEnv(maps, 180, _rg(), cfg, env_id_offset=120)]
+    for sh in shards:
+        sh.reset_all(seed)
+    for t in range(40):
+        a = random_actions(seed, np.arange(n), t)
+        full.step_batch(a)
+        shards[0].step_batch(a[:120])
+        shards[1].step_batch(a[120:])
+    want = full.recent_returns()
+    assert len(want) == 256
+    keys, vals = full.recent_returns_keyed()
+    assert vals.tolist() == want and np.all(np.diff(keys.astype(np.float64)) > 0)
+    got = merge_recent_returns([sh.recent_returns_keyed() for sh in shards])
+    assert got == want
+    assert pooled_stats(full)["recent_returns"] == want  # world size 1: no collective
+
+
 def test_auto_reset_reports_fresh_state_and_stores_terminal():  # test_vecenv.py:70-82
     from paper_2305_04180_b200 import VecEnv
     env = VecEnv([make_map(40)], 3, _rg(0.0), EnvConfig(timeout_steps=4))
