@@ -264,7 +264,6 @@ struct Chunk {
   uint32_t* gid;   // per slot: the env's stream lane (global env id)
   int32_t* list;   // slots in dispatch order (longest predicted scan first)
   int32_t* reg;    // slots in registration order
-  int32_t* hread;  // per slot: global slot whose step-count history predicts this scan, or -1
   int32_t* hwrite; // per slot: global slot whose history this scan refreshes, or -1
   uint32_t* qacc;  // per slot: march steps its rays took (shared atomics)
   int32_t* xslot;  // per env: post-reset slot, -1 if none
@@ -290,8 +289,7 @@ __device__ __forceinline__ Chunk chunk_smem(uint8_t* base, int cap, int slots, i
   c.gid = (uint32_t*)(c.stage + (size_t)slots * D);
   c.list = (int32_t*)(c.gid + slots);
   c.reg = c.list + slots;
-  c.hread = c.reg + slots;
-  c.hwrite = c.hread + slots;
+  c.hwrite = c.reg + slots;
   c.qacc = (uint32_t*)(c.hwrite + slots);
   c.xslot = (int32_t*)(c.qacc + slots);
   c.ctl = c.xslot + cap;
@@ -403,10 +401,9 @@ __device__ __forceinline__ int work_bucket(uint32_t steps) {
        : steps >= 7 ? 4 : steps >= 5 ? 5 : steps >= 3 ? 6 : 7;
 }
 
-// predicted bucket of one scan (called by the thread that registers it)
-__device__ __forceinline__ uint8_t scan_bucket(const EnvDev& d, int32_t hread) {
-  if (hread < 0) return 0;
-  return (uint8_t)work_bucket(d.qsum[hread] / (uint32_t)d.R);
+// predicted bucket of a scan from its lane's summed step count last step
+__device__ __forceinline__ uint8_t scan_bucket(const EnvDev& d, uint32_t qprev) {
+  return (uint8_t)work_bucket(qprev / (uint32_t)d.R);
 }
 
 // Refresh the lanes' step-count history from this chunk's scans (after a ray
@@ -587,9 +584,8 @@ __device__ __forceinline__ MapView bind_map(const EnvDev& d, int m, uint8_t* sme
 // Register a scan slot: origin, heading, noise stream position; queue it.
 __device__ __forceinline__ void add_slot(const EnvDev& d, const Chunk& c, int slot, double x,
                                          double y, double ch, double sh, double sig, uint32_t gid,
-                                         uint64_t nctr, int32_t hread, int32_t hwrite) {
-  c.sbucket[slot] = scan_bucket(d, hread);
-  c.hread[slot] = hread;
+                                         uint64_t nctr, uint8_t bucket, int32_t hwrite) {
+  c.sbucket[slot] = bucket;
   c.hwrite[slot] = hwrite;
   c.px[slot] = x; c.py[slot] = y; c.ch[slot] = ch; c.sh[slot] = sh; c.sig[slot] = sig;
   c.gid[slot] = gid;
@@ -638,7 +634,7 @@ __device__ __forceinline__ bool reset_env(const EnvDev& d, const MapView& mv, co
   for (int wi = 0; wi < ((delay + 15) >> 4); ++wi) d.hist[(int64_t)wi * d.n + s] = ~0ull;
   header_row(mc, x, y, bearing_error(x, y, th, mc.goal_x, mc.goal_y), c0, s0, 0.0, 0.0, vml, vma,
              c.stage + slot * d.D);
-  add_slot(d, c, slot, x, y, c0, s0, sig, gid, ctr, -1, (int32_t)s);
+  add_slot(d, c, slot, x, y, c0, s0, sig, gid, ctr, 0, (int32_t)s);  // no history: longest
   ctr += d.nb;
   return true;
 }
@@ -699,6 +695,7 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
     const double k = d.pk[s], dt = d.pdt[s], vml = d.pvl[s], vma = d.pva[s];
     const int32_t delay = d.delay[s];
     int32_t step = d.step[s];
+    const uint32_t qprev = d.qsum[s];  // loaded with the state: the scan's bucket needs it last
     // delay queue (core.py:176-182): matured = action issued `delay` steps ago
     uint32_t code = (uint32_t)av;
     if (delay > 0) {
@@ -759,7 +756,7 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
     }
     header_row(mc, x, y, alpha, d.c0[s], d.s0[s], vl, va, vml, vma, c.stage + e * d.D);
     // the post-step scan (core.py:203-206); cos/sin of h1 == of wrap(h1)
-    add_slot(d, c, e, x, y, cos1, sin1, d.psig[s], gid, ctr, (int32_t)s,
+    add_slot(d, c, e, x, y, cos1, sin1, d.psig[s], gid, ctr, scan_bucket(d, qprev),
              r.ended && d.auto_reset ? -1 : (int32_t)s);
     ctr += d.nb;
     d.x[s] = x; d.y[s] = y; d.h[s] = h; d.vl[s] = vl; d.va[s] = va;
