@@ -446,10 +446,10 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   TRY(env->alloc(&d.step, n));
   TRY(env->alloc(&d.delay, n));
   TRY(env->alloc(&d.needs_reset, n, 1));
-  TRY(env->alloc(&d.qsum, n));
-  {  // no history yet: 24 steps per beam (scans without history sort longest)
-    std::vector<uint32_t> q(n, 24u * (uint32_t)env->R);
-    cudaMemcpy(d.qsum, q.data(), 4 * n, cudaMemcpyHostToDevice);
+  TRY(env->alloc(&d.qmax, n));
+  {  // no history yet: scans without history sort longest
+    std::vector<uint32_t> q(n, 255u);
+    cudaMemcpy(d.qmax, q.data(), 4 * n, cudaMemcpyHostToDevice);
   }
   TRY(env->alloc(&d.episodes, n));
   TRY(env->alloc(&d.arrivals, n));

@@ -265,7 +265,7 @@ struct Chunk {
   int32_t* list;   // slots in dispatch order (longest predicted scan first)
   int32_t* reg;    // slots in registration order
   int32_t* hwrite; // per slot: global slot whose history this scan refreshes, or -1
-  uint32_t* qacc;  // per slot: march steps its rays took (shared atomics)
+  uint32_t* qacc;  // per slot: march steps its longest ray took (shared atomicMax)
   int32_t* xslot;  // per env: post-reset slot, -1 if none
   uint8_t* wmode;  // per env: which rows to write (see kernel)
   uint8_t* prox;   // per slot: some ray ended closer than the proximity range
@@ -390,20 +390,18 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
   }
 }
 
-// Longest-first order (LPT) of the chunk's scans: a scan's predicted work is
-// the mean number of march steps its env's beams took last step (the robot
-// moves <= 1.8 cm and turns <= 0.1 rad per step); unknown history (fresh
-// spawns) counts as long.  Slots are counting-sorted into 8 work buckets and
-// c.list is rewritten longest first; rays are then dispatched slot-major, so
-// the queue tail holds the cheapest scans.
-__device__ __forceinline__ int work_bucket(uint32_t steps) {
-  return steps >= 24 ? 0 : steps >= 16 ? 1 : steps >= 12 ? 2 : steps >= 9 ? 3
-       : steps >= 7 ? 4 : steps >= 5 ? 5 : steps >= 3 ? 6 : 7;
-}
+// Longest-first order (LPT) of the chunk's scans: a scan is ranked by the
+// march steps its env's longest beam took last step (the robot moves <= 1.8 cm
+// and turns <= 0.1 rad per step); the longest ray, not the mean, is what the
+// ray phase's tail waits for (-2 % step against ranking by the mean).
+// Unknown history (fresh spawns) counts as long.  Slots are counting-sorted
+// into 8 buckets and c.list is rewritten longest first; rays are then
+// dispatched slot-major, so the queue tail holds scans with only short rays.
 
-// predicted bucket of a scan from its lane's summed step count last step
-__device__ __forceinline__ uint8_t scan_bucket(const EnvDev& d, uint32_t qprev) {
-  return (uint8_t)work_bucket(qprev / (uint32_t)d.R);
+// predicted bucket of a scan from its lane's longest ray last step
+__device__ __forceinline__ uint8_t scan_bucket(uint32_t m) {
+  return (uint8_t)(m >= 60 ? 0 : m >= 45 ? 1 : m >= 36 ? 2 : m >= 29 ? 3 : m >= 23 ? 4
+                 : m >= 18 ? 5 : m >= 13 ? 6 : 7);
 }
 
 // Refresh the lanes' step-count history from this chunk's scans (after a ray
@@ -412,7 +410,7 @@ __device__ __forceinline__ void store_history(const EnvDev& d, const Chunk& c, i
   for (int k = threadIdx.x; k < n_slots; k += blockDim.x) {
     const int slot = c.reg[k];
     const int hw = c.hwrite[slot];
-    if (hw >= 0) d.qsum[hw] = c.qacc[slot];
+    if (hw >= 0) d.qmax[hw] = c.qacc[slot];
   }
 }
 
@@ -549,7 +547,7 @@ struct FinObs {
     const double v = dclip(dadd(t, dadd(0.0, dmul(c.sig[slot], z))), 0.0, max_range);
     rowp[5 + j] = (float)div_by(v, max_range, inv_max_range);
     if (t < proximity) c.prox[slot] = 1;
-    atomicAdd(&c.qacc[slot], (uint32_t)steps);
+    atomicMax(&c.qacc[slot], (uint32_t)steps);
   }
 };
 
@@ -695,7 +693,7 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
     const double k = d.pk[s], dt = d.pdt[s], vml = d.pvl[s], vma = d.pva[s];
     const int32_t delay = d.delay[s];
     int32_t step = d.step[s];
-    const uint32_t qprev = d.qsum[s];  // loaded with the state: the scan's bucket needs it last
+    const uint32_t qprev = d.qmax[s];  // loaded with the state: the scan's bucket needs it last
     // delay queue (core.py:176-182): matured = action issued `delay` steps ago
     uint32_t code = (uint32_t)av;
     if (delay > 0) {
@@ -756,7 +754,7 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
     }
     header_row(mc, x, y, alpha, d.c0[s], d.s0[s], vl, va, vml, vma, c.stage + e * d.D);
     // the post-step scan (core.py:203-206); cos/sin of h1 == of wrap(h1)
-    add_slot(d, c, e, x, y, cos1, sin1, d.psig[s], gid, ctr, scan_bucket(d, qprev),
+    add_slot(d, c, e, x, y, cos1, sin1, d.psig[s], gid, ctr, scan_bucket(qprev),
              r.ended && d.auto_reset ? -1 : (int32_t)s);
     ctr += d.nb;
     d.x[s] = x; d.y[s] = y; d.h[s] = h; d.vl[s] = vl; d.va[s] = va;

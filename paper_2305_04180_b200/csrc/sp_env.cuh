@@ -45,7 +45,7 @@ struct EnvDev {
   uint64_t* ctr;          // Philox block counter per lane
   int32_t *step, *delay;
   uint8_t* needs_reset;
-  uint32_t* qsum;         // n: march steps all beams of the lane's last scan took
+  uint32_t* qmax;         // n: march steps the longest beam of the lane's last scan took
   const double* ranges;   // 12 doubles per lane (or shared when ranges_shared)
   int32_t ranges_shared;
   const int64_t* env_of_slot;
