@@ -682,18 +682,21 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
                                           int64_t row, uint32_t gid, uint64_t& ctr, int cap,
                                           int slot_cap) {
   StepA r;
+  // the lane state is loaded before the action checks, so its DRAM round
+  // trip overlaps the row map -> action one
+  double x = d.x[s], y = d.y[s], h = d.h[s], vl = d.vl[s], va = d.va[s];
+  const double k = d.pk[s], dt = d.pdt[s], vml = d.pvl[s], vma = d.pva[s];
+  const int32_t delay = d.delay[s];
+  int32_t step = d.step[s];
+  const uint32_t qprev = d.qmax[s];  // the scan's bucket needs it last
+  const uint8_t nr = d.needs_reset[s];
   const int64_t av = a.actions[row];
   if (av < 0 || av >= d.n_actions) {
     set_error(d, SP_EACTION, row);
-  } else if (d.needs_reset[s]) {
+  } else if (nr) {
     set_error(d, SP_EEPISODE, row);
   } else {
     r.live = true;
-    double x = d.x[s], y = d.y[s], h = d.h[s], vl = d.vl[s], va = d.va[s];
-    const double k = d.pk[s], dt = d.pdt[s], vml = d.pvl[s], vma = d.pva[s];
-    const int32_t delay = d.delay[s];
-    int32_t step = d.step[s];
-    const uint32_t qprev = d.qmax[s];  // loaded with the state: the scan's bucket needs it last
     // delay queue (core.py:176-182): matured = action issued `delay` steps ago
     uint32_t code = (uint32_t)av;
     if (delay > 0) {
