@@ -124,6 +124,23 @@ __device__ __forceinline__ bool disc_hits(const MapView& mv, const EnvDev& d, do
   return false;
 }
 
+// ---------------------------------------------- debug phase timestamps ---
+// Built only with -DSP_TIMING (tools/debug): thread 0 of each CTA stamps
+// %clock64 (SM cycles) at phase boundaries of the first chunk.
+#ifdef SP_TIMING
+__device__ unsigned long long g_sp_ts[1024][12];
+__device__ __forceinline__ void sp_stamp(int k) {
+  if (threadIdx.x == 0 && blockIdx.x < 1024) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+    g_sp_ts[blockIdx.x][k] = t;
+  }
+}
+#define SP_STAMP(k) sp_stamp(k)
+#else
+#define SP_STAMP(k)
+#endif
+
 // ---------------------------------------------------------------- rays ---
 // Ray state in cell units: origin (x0, y0)/cell, direction (dx, dy)/cell and
 // cell/dx, cell/dy (so t = (face - x0) * idx comes out in cm), the step
@@ -350,7 +367,16 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
         int base = 0;
         if (lane == 0) base = atomicAdd(&c.ctl[0], n_idle);
         base = __shfl_sync(SP_FULL, base, 0);
-        if (base + n_idle >= total) drained = true;
+        if (base + n_idle >= total) {
+#ifdef SP_TIMING
+          if (base < total && lane == 0 && blockIdx.x < 1024) {  // the queue just drained
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+            g_sp_ts[blockIdx.x][10] = t;
+          }
+#endif
+          drained = true;
+        }
         const int my_a = base + __popc(ia & lt);
         const int my_b = base + na + __popc(ib & lt);
         if (fin_a && my_a < total) {
@@ -817,22 +843,6 @@ __device__ __forceinline__ void finish_env(const EnvDev& d, const StepArgs& a, c
   d.ret[s] = ret;
 }
 
-// ---------------------------------------------- debug phase timestamps ---
-// Built only with -DSP_TIMING (tools/debug): thread 0 of each CTA stamps
-// %clock64 (SM cycles) at phase boundaries of the first chunk.
-#ifdef SP_TIMING
-__device__ unsigned long long g_sp_ts[1024][12];
-__device__ __forceinline__ void sp_stamp(int k) {
-  if (threadIdx.x == 0 && blockIdx.x < 1024) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
-    g_sp_ts[blockIdx.x][k] = t;
-  }
-}
-#define SP_STAMP(k) sp_stamp(k)
-#else
-#define SP_STAMP(k)
-#endif
 
 // ------------------------------------------------------------ the kernel ---
 template <bool kSmem, bool kBordered>

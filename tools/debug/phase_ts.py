@@ -35,6 +35,9 @@ for n in (65536,):
     for i, nm in enumerate(names):
         print(f"   {nm:12s} median {np.median(d[:, i]):6.2f} us  max {d[:, i].max():6.2f} us")
     rays = d[:, 4]
+    drain = (ts[:, 10] - ts[:, 4]) / 1e3  # queue drained, relative to the ray phase start
+    print("   ray queue drained %.1f us into the ray phase (median); tail after it: median %.1f us, max %.1f us"
+          % (np.median(drain), np.median(rays - drain), (rays - drain).max()))
     print("   CTA envs: min %d max %d; CTAs spanning 2 maps: n/a; rays max/mean %.1f/%.1f us" % (nenv.min(), nenv.max(), rays.max(), rays.mean()))
     print("   per-map: map  ctas  envs/cta  rays_us(mean)  rays_us/env")
     for m in sorted(set(mapi.tolist())):
