@@ -130,7 +130,6 @@ struct SpEnv {
   int grid = 0, threads = 0;
   size_t smem = 0;
   int n_sm = 0, smem_optin = 0, smem_per_sm = 0;
-  bool bordered = false;
   int32_t* h_err = nullptr;  // pinned
   int64_t* h_scan = nullptr;  // pinned staging for scan offsets (n_maps + 1 + n_sm + 1)
   int64_t* d_scan = nullptr;
@@ -328,6 +327,9 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
     if (ranges[r].delay[0] < 0 || ranges[r].delay[1] > SP_MAX_DELAY ||
         ranges[r].delay[0] > ranges[r].delay[1])
       return fail(SP_EINVAL, "control delay range must lie in [0, 64]");
+  // GridMap's invariant (gridmap.py:90-95): the marcher relies on it (no step
+  // can leave the grid); the op-level seam sp_cast_rays takes any grid
+  if (!all_bordered(maps, n_maps)) return fail(SP_EMAP, "border cells must all be occupied");
 
   DevDeviceGuard guard(device);
   SpEnv* env = new SpEnv();
@@ -337,7 +339,6 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   env->D = 5 + cfg->n_beams;
   env->n_maps = n_maps;
   env->auto_reset = cfg->auto_reset != 0;
-  env->bordered = all_bordered(maps, n_maps);
   cudaDeviceProp prop;
   if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
     delete env;
@@ -505,14 +506,8 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   env->grid = plan.grid;
   env->threads = plan.threads;
   env->smem = plan.smem;
-  const void* kernels_[] = {(const void*)env_step_kernel<true, true>,
-                            (const void*)env_step_kernel<true, false>,
-                            (const void*)env_step_kernel<false, true>,
-                            (const void*)env_step_kernel<false, false>,
-                            (const void*)env_scan_kernel<true, true>,
-                            (const void*)env_scan_kernel<true, false>,
-                            (const void*)env_scan_kernel<false, true>,
-                            (const void*)env_scan_kernel<false, false>};
+  const void* kernels_[] = {(const void*)env_step_kernel<true>, (const void*)env_step_kernel<false>,
+                            (const void*)env_scan_kernel<true>, (const void*)env_scan_kernel<false>};
   cudaError_t e1 = cudaSuccess, e2 = cudaSuccess;
   for (const void* k : kernels_) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -537,15 +532,10 @@ int sp_env_destroy(SpEnv* env) {
 }
 
 static int launch_env(SpEnv* env, const StepArgs& a, cudaStream_t st) {
-  const bool sm = env->d.smem_maps, bd = env->bordered;
-  if (sm && bd)
-    env_step_kernel<true, true><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
-  else if (sm)
-    env_step_kernel<true, false><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
-  else if (bd)
-    env_step_kernel<false, true><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
+  if (env->d.smem_maps)
+    env_step_kernel<true><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
   else
-    env_step_kernel<false, false><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
+    env_step_kernel<false><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(SP_ECUDA, std::string("env_step_kernel: ") + cudaGetErrorString(e));
   return SP_OK;
@@ -869,14 +859,10 @@ int sp_env_scan(SpEnv* env, int64_t n, const int64_t* query_offsets, const doubl
   SP_CUDA(cudaMemcpyAsync(env->d_scan, env->h_scan, 8 * (nq + nc), cudaMemcpyHostToDevice, st));
   SP_CUDA(cudaEventRecord(env->scan_copied, st));
   ScanArgs q{n, env->d_scan + nq, env->d_scan, x, y, heading, ranges, hit_cell};
-  if (d.smem_maps && env->bordered)
-    env_scan_kernel<true, true><<<plan.grid, plan.threads, plan.smem, st>>>(d, q);
-  else if (d.smem_maps)
-    env_scan_kernel<true, false><<<plan.grid, plan.threads, plan.smem, st>>>(d, q);
-  else if (env->bordered)
-    env_scan_kernel<false, true><<<plan.grid, plan.threads, plan.smem, st>>>(d, q);
+  if (d.smem_maps)
+    env_scan_kernel<true><<<plan.grid, plan.threads, plan.smem, st>>>(d, q);
   else
-    env_scan_kernel<false, false><<<plan.grid, plan.threads, plan.smem, st>>>(d, q);
+    env_scan_kernel<false><<<plan.grid, plan.threads, plan.smem, st>>>(d, q);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(SP_ECUDA, std::string("env_scan_kernel: ") + cudaGetErrorString(e));
   return SP_OK;

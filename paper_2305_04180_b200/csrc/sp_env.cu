@@ -182,8 +182,8 @@ __device__ __forceinline__ int floor_i(double v) {  // floor(v), |v| < 2^31
 // exit point.  Returns true when a live ray finished.  r.t then holds the
 // exit parameter of its last free cell: the range once clipped to max_range
 // (ray_range), and ray_hit() recovers the occupied cell it stopped in.
-// kBordered: every map has an occupied border, so no step can leave the grid.
-template <bool kBordered>
+// Every map has an occupied border (GridMap's invariant, checked by
+// sp_env_create), so no step can leave the grid and there are no bounds tests.
 __device__ __forceinline__ bool ray_step(Ray& r, const MapView& mv, const EnvDev& d) {
   const int code = mv.scode(r.ix, r.iy);  // < 0: mixed block
   const bool cellwise = code < 0;
@@ -207,8 +207,7 @@ __device__ __forceinline__ bool ray_step(Ray& r, const MapView& mv, const EnvDev
   const int nx = xs ? face_x - fx + r.sx : cc;  // far cell + sx
   const int ny = xs ? cc : face_y - fy + r.sy;
   const bool over = t > d.max_range;  // :97-99
-  const bool out = !kBordered && ((unsigned)nx >= (unsigned)d.W || (unsigned)ny >= (unsigned)d.H);
-  const bool finished = occupied || over || out;
+  const bool finished = occupied || over;
   if (!occupied) {
     r.t = t;
     if (!finished) {
@@ -221,8 +220,7 @@ __device__ __forceinline__ bool ray_step(Ray& r, const MapView& mv, const EnvDev
 }
 
 // A parked ray: a finished fixed point for the lanes of a ray slot with no
-// ray (on bordered maps cell (0, 0) is occupied; otherwise the ray drifts out
-// of the grid or past max_range and stops there).
+// ray (cell (0, 0) is a border cell, occupied).
 __device__ __forceinline__ void ray_park(Ray& r) {
   r.ix = r.iy = 0;
   r.sx = r.sy = 1;
@@ -333,7 +331,7 @@ __device__ __forceinline__ int div_r(int q, const EnvDev& d) {
 // other's.  A warp refills only when at least d.refill_min of its 64 ray
 // slots are idle (or the queue is drained); finished rays are retired in the
 // same branch, so per-ray setup/finish code runs at high SIMT occupancy.
-template <bool kBordered, bool kHit, class Fin>
+template <bool kHit, class Fin>
 __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, const Chunk& c,
                                           const double2* beam, int n_env, const Fin& fin) {
   const int R = d.R;
@@ -410,8 +408,8 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
     // stays put in the second
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-      fin_a = ray_step<kBordered>(ra, mv, d);
-      fin_b = ray_step<kBordered>(rb, mv, d);
+      fin_a = ray_step(ra, mv, d);
+      fin_b = ray_step(rb, mv, d);
     }
   }
 }
@@ -845,7 +843,7 @@ __device__ __forceinline__ void finish_env(const EnvDev& d, const StepArgs& a, c
 
 
 // ------------------------------------------------------------ the kernel ---
-template <bool kSmem, bool kBordered>
+template <bool kSmem>
 __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     env_step_kernel(const __grid_constant__ EnvDev d, const __grid_constant__ StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -949,7 +947,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     noise_phase(d, c, n_slots, kpre, cta_grp());
     __syncthreads();
     SP_STAMP(4);
-    ray_phase<kBordered, false>(mv, d, c, beam, n_slots, fin);
+    ray_phase<false>(mv, d, c, beam, n_slots, fin);
     __syncthreads();
     SP_STAMP(5);
     store_history(d, c, n_slots);
@@ -981,7 +979,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       order_slots(c, n2, cta_grp());
       noise_phase(d, c, n2, 0, cta_grp());
       __syncthreads();
-      ray_phase<kBordered, false>(mv, d, c, beam, n2, fin);
+      ray_phase<false>(mv, d, c, beam, n2, fin);
       __syncthreads();
       store_history(d, c, n2);
       write_rows(d, a, c, s0, n, cta_grp());
@@ -1012,7 +1010,7 @@ struct FinScan {
 #ifndef SP_SCAN_THREADS
 #define SP_SCAN_THREADS SP_CTA_THREADS
 #endif
-template <bool kSmem, bool kBordered>
+template <bool kSmem>
 __global__ void __launch_bounds__(SP_SCAN_THREADS, SP_CTAS_PER_SM)
     env_scan_kernel(const __grid_constant__ EnvDev d, const __grid_constant__ ScanArgs q) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -1052,7 +1050,7 @@ __global__ void __launch_bounds__(SP_SCAN_THREADS, SP_CTAS_PER_SM)
     }
     __syncthreads();
     const FinScan fin{q.ranges, q.hit_cell, s0, d.R};
-    ray_phase<kBordered, true>(mv, d, c, beam, n, fin);
+    ray_phase<true>(mv, d, c, beam, n, fin);
     s0 += n;
   }
 }

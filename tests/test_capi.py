@@ -126,3 +126,10 @@ def test_env_create_validates_before_touching_the_device():
     bad[0].delay[0], bad[0].delay[1] = 0, 65
     assert create(cfg(), [desc()], ranges=bad) == _lib.SP_EINVAL
     assert b"delay" in lib.sp_last_error()
+    # GridMap's border invariant (gridmap.py:90-95), which the marcher relies on
+    holed = np.ones((20, 20), np.uint8)
+    holed[0, 7] = 0
+    d = desc()
+    d.occupancy = holed.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
+    assert create(cfg(), [d]) == _lib.SP_EMAP
+    assert b"border" in lib.sp_last_error()

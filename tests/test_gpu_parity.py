@@ -144,6 +144,19 @@ def test_fast_marcher_hit_cells(n_beams, max_range):
     assert_close(got, want, rtol=1e-9, atol=1e-9, what="ranges")
 
 
+def test_unbordered_maps_are_rejected():
+    """A map whose border is not fully occupied (GridMap validates this,
+    gridmap.py:90-95; here the border is cleared after construction, as a raw
+    map could arrive) raises MapError: the marcher has no grid-exit tests.
+    The op-level seam (sp_cast_rays) takes any grid, test_gpu_kernels.py."""
+    import copy
+    from paper_2305_04180_b200.sim import MapError
+    maps = [copy.deepcopy(m) for m in load_maps(2)]
+    maps[1].occupancy[0, 5] = False
+    with pytest.raises(MapError):
+        _vec(maps, 4, ranges(0.0), config(32))
+
+
 def _vs_oracle_run(maps, n, div, steps, seed, n_beams=32):
     from oracle.oracle import OracleVecEnv
     cfg = config(n_beams)

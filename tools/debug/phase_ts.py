@@ -9,7 +9,7 @@ from paper_2305_04180_b200 import VecEnv, _lib
 from paper_2305_04180_b200.vecenv import StepBatch
 lib = ctypes.CDLL(_lib.LIB_PATH)
 names = ["prologue", "bind_map", "phaseA", "order+noise", "rays", "phaseC", "rows"]
-for n in (65536,):
+for n in (int(os.environ.get("N", "65536")),):
     env = VecEnv(load_maps(16), n, ranges(0.3), config(32), check_actions=False)
     env.reset_all(0)
     dev = env.device; D = env.state_dim

@@ -3,7 +3,7 @@ kernel that contains `need` table loads (LDS.S8 / LDS.U8).  Usage:
 python tools/debug/sass_loop.py [lib.so] [kernel-substring] [need]"""
 import re, subprocess, sys
 lib = sys.argv[1] if len(sys.argv) > 1 else "paper_2305_04180_b200/_lib/libsparrow.so"
-kern = sys.argv[2] if len(sys.argv) > 2 else "env_step_kernelILb1ELb1"
+kern = sys.argv[2] if len(sys.argv) > 2 else "env_step_kernelILb1E"
 need = int(sys.argv[3]) if len(sys.argv) > 3 else 4
 out = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
 body, cur = [], None
