@@ -173,8 +173,8 @@ def hybrid_box(occ, levels=LEVELS16):
     return box
 
 
-def cell_box(occ):
-    r = np.clip(chessboard(occ) - 1, 0, 255)
+def cell_box(occ, cap=255):
+    r = np.clip(chessboard(occ) - 1, 0, cap)
 
     def box(ix, iy, sx, sy):
         rr = r[iy, ix]
@@ -222,7 +222,8 @@ def main():
         for name, mk in (("block", block_box), ("quad", quad_box), ("quad16", lambda o: quad_box(o, 16)),
                          ("quadlog", lambda o: quad_box(o, 127, LEVELS16)),
                          ("hybrid", hybrid_box),
-                         ("cell", cell_box)):
+                         ("cell", cell_box), ("cell14", lambda o: cell_box(o, 14)),
+                         ("cell6", lambda o: cell_box(o, 6))):
             st = march(occ, *rays, 300.0, mk(occ))
             tot.setdefault(name, []).append(st)
     for name, v in tot.items():
