@@ -9,21 +9,24 @@
 //   that lies inside one map whenever the map count allows, so a CTA stages
 //   one map once per launch.
 // * Per map, two tables live in shared memory, staged by one TMA bulk copy
-//   (cp.async.bulk + mbarrier): a 2x2-block table (u8: 0x80 | occupancy mask
-//   of the block's four cells when any is occupied, else the radius r of the
-//   all-free (2r+1)^2-block box around it) that the march reads once per
-//   step, and a 1-bit occupancy bitmap (H x ceil(W/32) u32) for the exact
-//   disc-collision test.  366 x 366 cells -> 33.5 KB + 17.6 KB.
+//   (cp.async.bulk + mbarrier): a 2x2-block table (signed byte: 0x80 | the
+//   occupancy mask of the block's cells, bit (ix + 2 iy) & 3, when any is
+//   occupied, else the side k = 2r + 1 of the all-free k x k-block box
+//   around it) that the march reads once per step, and a 1-bit occupancy
+//   bitmap (H x ceil(W/32) u32) for the exact disc-collision test.
+//   366 x 366 cells -> 33.5 KB + 17.6 KB.  Every map has an occupied border.
 // * A CTA walks its range in chunks of up to `chunk_cap` envs with CTA-wide
 //   phases separated by __syncthreads:
 //     A  thread-per-env physics, collision, events, shaped-reward partial,
-//        obs header and LiDAR noise (fp64 in the reference's rounding order);
-//     B  one CTA-wide LiDAR ray queue over chunk x R rays: warps take as many
-//        rays as they have idle lanes (one shared atomic), so ray-length
-//        divergence only idles lanes at the very end of the chunk;
-//     C  thread-per-env reward, outputs, VecEnv statistics; coalesced rows;
-//     D  auto-reset of the finished envs (resample, spawn rejection) and a
-//        fresh scan through the same ray queue, then the post-reset rows.
+//        obs header (fp64 in the reference's rounding order); fused
+//        auto-reset of finished envs (resample, spawn rejection) with their
+//        fresh scan in an extra slot; collisions / arrivals finish here;
+//        threads without an env pre-generate the LiDAR noise;
+//     B  one CTA-wide LiDAR ray queue over all scans of the chunk, longest
+//        predicted scan first: warps take as many rays as they have idle
+//        slots (one shared atomic), two rays per lane;
+//     C  thread-per-env reward of running / timed-out envs, outputs, VecEnv
+//        statistics; then coalesced rows (post-step and post-reset).
 // * The march visits the same cells as the reference DDA (_cy.pyx:89-105) but
 //   jumps over free boxes in one step: at cell (ix,iy) with free box B, the
 //   ray leaves B through the face with the smaller exit parameter (ties go to
