@@ -228,7 +228,8 @@ static int extra_slots(int cap) { return std::max(32, cap / 8); }
 static size_t chunk_bytes(int cap, int D, int R) {
   const size_t slots = (size_t)cap + extra_slots(cap);
   (void)R;
-  return slots * (74 + 4 * (size_t)D) + 30 * (size_t)cap + 96;
+  (void)D;
+  return slots * 90 + 30 * (size_t)cap + 96;
 }
 
 static Plan plan_launch(SpEnv* env, const std::vector<int64_t>& off, bool staging = true) {

@@ -290,7 +290,8 @@ struct Chunk {
   uint8_t* sbucket;  // per slot: predicted work bucket (0 = longest)
   int* ctl;        // [0] ray-queue head [1] slots listed [2] extra slots used [3] overflow
                    // [4..11] bucket counts, [12..19] bucket offsets
-  float* stage;    // slots x D staging rows
+  float** out0;    // per slot: the output row its scan fills (noise z parks there first)
+  float** out1;    // per slot: a second row that receives the same values, or null
 };
 
 __device__ __forceinline__ Chunk chunk_smem(uint8_t* base, int cap, int slots, int D, int R) {
@@ -303,8 +304,10 @@ __device__ __forceinline__ Chunk chunk_smem(uint8_t* base, int cap, int slots, i
   c.nctr = (uint64_t*)(c.sig + slots);
   c.retp = (double*)(c.nctr + slots);
   c.part = c.retp + cap;
-  c.stage = (float*)(c.part + cap);
-  c.gid = (uint32_t*)(c.stage + (size_t)slots * D);
+  c.out0 = (float**)(c.part + cap);
+  c.out1 = c.out0 + slots;
+  c.gid = (uint32_t*)(c.out1 + slots);
+  (void)D;
   c.list = (int32_t*)(c.gid + slots);
   c.reg = c.list + slots;
   c.hwrite = c.reg + slots;
@@ -488,7 +491,7 @@ __device__ __forceinline__ void noise_block(const EnvDev& d, const Chunk& c, int
   const Block4 blk = stream_block(d.seed, c.gid[slot], 0u, c.nctr[slot] + (uint64_t)b);
   float z[4];
   draw_normals4(blk, z);
-  float* row = c.stage + slot * d.D + 5 + 4 * b;
+  float* row = c.out0[slot] + 5 + 4 * b;
 #pragma unroll
   for (int u = 0; u < 4; ++u)
     if (4 * b + u < d.R) row[u] = z[u];
@@ -552,13 +555,20 @@ __device__ __forceinline__ double div_by(double v, double m, double inv_m) {
 // core.py:243-258 columns 0..4 (LiDAR columns come from the ray phase)
 __device__ __forceinline__ void header_row(const MapConst& mc, double x, double y, double alpha,
                                            double c0, double s0, double vl, double va, double vml,
-                                           double vma, float* row) {
+                                           double vma, float* row, float* row1) {
   const double rx = dsub(mc.goal_x, x), ry = dsub(mc.goal_y, y);
-  row[0] = (float)div_by(dadd(dmul(c0, rx), dmul(s0, ry)), mc.plan_dist, mc.inv_plan);
-  row[1] = (float)div_by(dadd(dmul(-s0, rx), dmul(c0, ry)), mc.plan_dist, mc.inv_plan);
-  row[2] = (float)div_by(alpha, SP_PI, SP_INV_PI);
-  row[3] = (float)ddiv(vl, vml);
-  row[4] = (float)ddiv(va, vma);
+  float h[5];
+  h[0] = (float)div_by(dadd(dmul(c0, rx), dmul(s0, ry)), mc.plan_dist, mc.inv_plan);
+  h[1] = (float)div_by(dadd(dmul(-s0, rx), dmul(c0, ry)), mc.plan_dist, mc.inv_plan);
+  h[2] = (float)div_by(alpha, SP_PI, SP_INV_PI);
+  h[3] = (float)ddiv(vl, vml);
+  h[4] = (float)ddiv(va, vma);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) row[k] = h[k];
+  if (row1) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) row1[k] = h[k];
+  }
 }
 
 // Finish functor of the ray phase: noisy normalized obs into the staging row
@@ -569,10 +579,12 @@ struct FinObs {
   int D;
   double max_range, inv_max_range, proximity;
   __device__ __forceinline__ void operator()(int slot, int j, double t, int, int steps) const {
-    float* rowp = c.stage + slot * D;
+    float* rowp = c.out0[slot];
     const double z = (double)rowp[5 + j];
     const double v = dclip(dadd(t, dadd(0.0, dmul(c.sig[slot], z))), 0.0, max_range);
-    rowp[5 + j] = (float)div_by(v, max_range, inv_max_range);
+    const float o = (float)div_by(v, max_range, inv_max_range);
+    rowp[5 + j] = o;
+    if (float* r1 = c.out1[slot]) r1[5 + j] = o;
     if (t < proximity) c.prox[slot] = 1;
     atomicMax(&c.qacc[slot], (uint32_t)steps);
   }
@@ -609,8 +621,11 @@ __device__ __forceinline__ MapView bind_map(const EnvDev& d, int m, uint8_t* sme
 // Register a scan slot: origin, heading, noise stream position; queue it.
 __device__ __forceinline__ void add_slot(const EnvDev& d, const Chunk& c, int slot, double x,
                                          double y, double ch, double sh, double sig, uint32_t gid,
-                                         uint64_t nctr, uint8_t bucket, int32_t hwrite) {
+                                         uint64_t nctr, uint8_t bucket, int32_t hwrite, float* o0,
+                                         float* o1) {
   c.sbucket[slot] = bucket;
+  c.out0[slot] = o0;
+  c.out1[slot] = o1;
   c.hwrite[slot] = hwrite;
   c.px[slot] = x; c.py[slot] = y; c.ch[slot] = ch; c.sh[slot] = sh; c.sig[slot] = sig;
   c.gid[slot] = gid;
@@ -625,7 +640,7 @@ __device__ __forceinline__ void add_slot(const EnvDev& d, const Chunk& c, int sl
 // noise blocks follow the reset draws, core.py:159-160).  false = no spawn.
 __device__ __forceinline__ bool reset_env(const EnvDev& d, const MapView& mv, const MapConst& mc,
                                           int64_t s, uint32_t gid, uint64_t& ctr, const Chunk& c,
-                                          int slot) {
+                                          int slot, float* orow) {
   const double* rg = d.ranges + (d.ranges_shared ? 0 : 12 * s);
   // DiversityRanges.sample (params.py:112-121): U U I U U U
   const double k = draw_uniform(stream_block(d.seed, gid, 0u, ctr++), rg[0], rg[1]);
@@ -658,8 +673,8 @@ __device__ __forceinline__ bool reset_env(const EnvDev& d, const MapView& mv, co
   d.needs_reset[s] = 0;
   for (int wi = 0; wi < ((delay + 15) >> 4); ++wi) d.hist[(int64_t)wi * d.n + s] = ~0ull;
   header_row(mc, x, y, bearing_error(x, y, th, mc.goal_x, mc.goal_y), c0, s0, 0.0, 0.0, vml, vma,
-             c.stage + slot * d.D);
-  add_slot(d, c, slot, x, y, c0, s0, sig, gid, ctr, 0, (int32_t)s);  // no history: longest
+             orow, nullptr);
+  add_slot(d, c, slot, x, y, c0, s0, sig, gid, ctr, 0, (int32_t)s, orow, nullptr);  // no history
   ctr += d.nb;
   return true;
 }
@@ -672,25 +687,6 @@ enum : uint8_t {
   W_RESET_OV = 3,  // stage[e] -> store_states; states after the overflow pass
   W_STATE = 4      // stage[e] -> states only (reset_all, overflow pass)
 };
-
-// Coalesced row writes: the chunk's rows are walked as one flat array of
-// n x D floats so every lane stores (full SIMT), consecutive lanes hitting
-// consecutive addresses of the same output row.
-__device__ __forceinline__ void write_rows(const EnvDev& d, const StepArgs& a, const Chunk& c,
-                                           int64_t s0, int n, const Grp& g) {
-  const int D = d.D;
-  const int total = n * D;
-  for (int f = g.tid; f < total; f += g.n) {
-    const int e = (int)(((uint64_t)(uint32_t)f * d.d_magic) >> 40);  // f / D
-    const int k = f - e * D;
-    const uint8_t w = c.wmode[e];
-    if (w == W_NONE) continue;
-    const int64_t o = (int64_t)c.rowi[e] * D + k;
-    const float own = c.stage[e * D + k];
-    if (w != W_STATE) a.store_states[o] = own;
-    if (w != W_RESET_OV) a.states[o] = w == W_RESET_X ? c.stage[c.xslot[e] * D + k] : own;
-  }
-}
 
 // Phase A of one env in MODE_STEP (core.py:165-206 + vecenv.py:96-114): delay
 // queue, kinematics, collision, events, the reward without its proximity term,
@@ -782,10 +778,14 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
       r.partial = dadd(dadd(dadd(dmul(0.3, r_d1), dmul(0.1, r_d2)), dmul(0.3, r_v)),
                      dmul(0.3, r_a));
     }
-    header_row(mc, x, y, alpha, d.c0[s], d.s0[s], vl, va, vml, vma, c.stage + e * d.D);
+    // rows: the post-step obs goes to store_states, and to states too unless
+    // the episode ended and resets (then states gets the fresh scan)
+    float* o_store = a.store_states + row * d.D;
+    float* o_state = r.ended && d.auto_reset ? nullptr : a.states + row * d.D;
+    header_row(mc, x, y, alpha, d.c0[s], d.s0[s], vl, va, vml, vma, o_store, o_state);
     // the post-step scan (core.py:203-206); cos/sin of h1 == of wrap(h1)
     add_slot(d, c, e, x, y, cos1, sin1, d.psig[s], gid, ctr, scan_bucket(qprev),
-             r.ended && d.auto_reset ? -1 : (int32_t)s);
+             r.ended && d.auto_reset ? -1 : (int32_t)s, o_store, o_state);
     ctr += d.nb;
     d.x[s] = x; d.y[s] = y; d.h[s] = h; d.vl[s] = vl; d.va[s] = va;
     d.step[s] = step;
@@ -795,7 +795,7 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
       const int k2 = atomicAdd(&c.ctl[2], 1);
       if (k2 < slot_cap - cap) {
         const int xs = cap + k2;
-        if (reset_env(d, mv, mc, s, gid, ctr, c, xs)) {
+        if (reset_env(d, mv, mc, s, gid, ctr, c, xs, a.states + row * d.D)) {
           c.xslot[e] = xs;
           c.wmode[e] = W_RESET_X;
         } else {
@@ -903,6 +903,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     if (act && e < kpre) {  // the post-step scan's noise stream (add_slot writes the same)
       c.nctr[e] = ctr;
       c.gid[e] = gid;
+      c.out0[e] = a.store_states + row * d.D;  // z parks in the store_states row
     }
     __syncthreads();
     if (kpre > 0 && !act) prenoise(d, c, kpre, n);
@@ -916,7 +917,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     if (a.mode != MODE_STEP) {
       const bool want = a.mode == MODE_RESET_ALL || (act && a.reset_mask[row] != 0);
       if (act && want) {
-        if (reset_env(d, mv, mc, s, gid, ctr, c, e)) {
+        if (reset_env(d, mv, mc, s, gid, ctr, c, e, a.states + row * d.D)) {
           c.wmode[e] = W_STATE;
           if (a.mode == MODE_RESET_ALL) {
             d.ret[s] = 0.0;
@@ -958,7 +959,6 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     if (act && c.evs[e] >= 0)
       finish_env(d, a, c, e, s, c.rowi[e], c.evs[e], c.part[e], c.send[e], c.retp[e]);
     SP_STAMP(6);
-    write_rows(d, a, c, s0, n, cta_grp());
     // ---- overflow pass: resets that did not fit the extra slots (rare) -----
     if (a.mode == MODE_STEP && c.ctl[3] > 0) {
       __syncthreads();
@@ -967,7 +967,8 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       if (act && c.wmode[e] == W_RESET_OV) {
         uint64_t ctr2 = d.ctr[s];
         const int64_t row2 = c.rowi[e];
-        if (reset_env(d, mv, mc, s, (uint32_t)(d.env_id_offset + row2), ctr2, c, e)) {
+        if (reset_env(d, mv, mc, s, (uint32_t)(d.env_id_offset + row2), ctr2, c, e,
+                      a.states + row2 * d.D)) {
           c.wmode[e] = W_STATE;
         } else {
           set_error(d, SP_EMAP, row2);
@@ -985,7 +986,6 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       ray_phase<false>(mv, d, c, beam, n2, fin);
       __syncthreads();
       store_history(d, c, n2);
-      write_rows(d, a, c, s0, n, cta_grp());
     }
     SP_STAMP(7);
     s0 += n;
