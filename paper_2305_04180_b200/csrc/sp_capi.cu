@@ -102,6 +102,42 @@ void build_block_table(const uint8_t* occ, int H, int W, int Hb, int Wb, uint8_t
     out[i] = mask[i] ? (uint8_t)(0x80u | mask[i]) : (uint8_t)(2 * std::min(dist[i] - 1, 63) + 1);
 }
 
+// Per-cell free-box table (the march's table): an occupied cell stores 0x80
+// (negative as a signed byte); a free cell stores r = (chessboard distance to
+// the nearest occupied or out-of-grid cell) - 1, clamped to 127: the
+// (2r+1) x (2r+1) cells centred on it are all free.  Exact two-pass
+// chessboard distance transform.
+void build_cell_table(const uint8_t* occ, int H, int W, uint8_t* out) {
+  std::vector<int> dist((size_t)H * W);
+  for (int y = 0; y < H; ++y)
+    for (int x = 0; x < W; ++x) {
+      const int border = std::min(std::min(x + 1, y + 1), std::min(W - x, H - y));
+      dist[(size_t)y * W + x] = occ[(size_t)y * W + x] ? 0 : border;
+    }
+  for (int y = 0; y < H; ++y)
+    for (int x = 0; x < W; ++x) {
+      int& d = dist[(size_t)y * W + x];
+      if (x > 0) d = std::min(d, dist[(size_t)y * W + x - 1] + 1);
+      if (y > 0) {
+        d = std::min(d, dist[(size_t)(y - 1) * W + x] + 1);
+        if (x > 0) d = std::min(d, dist[(size_t)(y - 1) * W + x - 1] + 1);
+        if (x + 1 < W) d = std::min(d, dist[(size_t)(y - 1) * W + x + 1] + 1);
+      }
+    }
+  for (int y = H - 1; y >= 0; --y)
+    for (int x = W - 1; x >= 0; --x) {
+      int& d = dist[(size_t)y * W + x];
+      if (x + 1 < W) d = std::min(d, dist[(size_t)y * W + x + 1] + 1);
+      if (y + 1 < H) {
+        d = std::min(d, dist[(size_t)(y + 1) * W + x] + 1);
+        if (x + 1 < W) d = std::min(d, dist[(size_t)(y + 1) * W + x + 1] + 1);
+        if (x > 0) d = std::min(d, dist[(size_t)(y + 1) * W + x - 1] + 1);
+      }
+    }
+  for (size_t i = 0; i < dist.size(); ++i)
+    out[i] = dist[i] == 0 ? (uint8_t)0x80u : (uint8_t)std::min(dist[i] - 1, 127);
+}
+
 // every map's border row/column fully occupied (GridMap's invariant,
 // gridmap.py:90-95): no march step can then leave the grid
 bool all_bordered(const SpMapDesc* maps, int n_maps) {
@@ -355,8 +391,8 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   d.D = env->D;
   d.H = H;
   d.W = W;
-  d.Hb = (H + 1) / 2;
-  d.Wb = (W + 1) / 2;
+  d.Hb = H;  // the march table is per cell (build_cell_table)
+  d.Wb = W;
   d.WW = (W + 31) / 32;
   d.n_maps = n_maps;
   d.cell = cell;
@@ -370,7 +406,7 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   d.n_actions = cfg->n_actions;
   {
     const int K = (int)std::ceil(cfg->robot_radius_cm / cell);
-    d.need_k = 2 * ((K + 1) / 2) + 1;
+    d.need_k = K;  // a cell box of radius >= K covers the disc's cell bbox
   }
   for (int c = 0; c <= SP_MAX_ACTIONS; ++c) {
     d.action_v[c] = c < cfg->n_actions ? cfg->action_table[2 * c] : 0.0;
@@ -406,7 +442,7 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   std::vector<MapConst> mconst(n_maps);
   for (int m = 0; m < n_maps; ++m) {
     uint8_t* base = host_maps.data() + (size_t)m * d.map_bytes;
-    build_block_table(maps[m].occupancy, H, W, d.Hb, d.Wb, base);
+    build_cell_table(maps[m].occupancy, H, W, base);
     uint32_t* bits = (uint32_t*)(base + d.blk_bytes);
     for (int iy = 0; iy < H; ++iy)
       for (int ix = 0; ix < W; ++ix)

@@ -76,11 +76,11 @@ struct MapView {
   const uint32_t* bits;
   int W, H, Wb, WW;
   __device__ __forceinline__ uint32_t code(int ix, int iy) const {
-    return blk[(iy >> 1) * Wb + (ix >> 1)];
+    return blk[iy * Wb + ix];
   }
   // the same byte sign-extended: < 0 for a mixed block, else the box side
   __device__ __forceinline__ int scode(int ix, int iy) const {
-    return ((const int8_t*)blk)[(iy >> 1) * Wb + (ix >> 1)];
+    return ((const int8_t*)blk)[iy * Wb + ix];
   }
   __device__ __forceinline__ uint32_t word(int ix, int iy) const {
     return bits[iy * WW + (ix >> 5)];
@@ -95,7 +95,7 @@ __device__ __forceinline__ bool disc_hits(const MapView& mv, const EnvDev& d, do
     return true;  // :124-126
   const int cx = (int)floor(x * d.inv_cell), cy = (int)floor(y * d.inv_cell);
   if (cx >= 0 && cx < d.W && cy >= 0 && cy < d.H) {
-    const uint32_t code = mv.code(cx, cy);  // free box of side code covers the bbox?
+    const uint32_t code = mv.code(cx, cy);  // free box of radius code covers the bbox?
     if ((code & 0x80u) == 0u && code >= (uint32_t)d.need_k) return false;
   }
   int ix0 = (int)floor(ddiv(dsub(x, r), cell)); if (ix0 < 0) ix0 = 0;  // :128-135
@@ -188,15 +188,13 @@ __device__ __forceinline__ int floor_i(double v) {  // floor(v), |v| < 2^31
 // Every map has an occupied border (GridMap's invariant, checked by
 // sp_env_create), so no step can leave the grid and there are no bounds tests.
 __device__ __forceinline__ bool ray_step(Ray& r, const MapView& mv, const EnvDev& d) {
-  const int code = mv.scode(r.ix, r.iy);  // < 0: mixed block
-  const bool cellwise = code < 0;
-  const bool occupied = cellwise && ((code >> ((r.ix + (r.iy << 1)) & 3)) & 1);
-  // last cell of the free region on each axis: the cell itself, or the box's
-  // far cell (ix | 1) + sx * (2r + 1) - fx, written as a face index below
-  const int k = (int)code;  // box side 2r + 1 in blocks (unused when cellwise)
+  const int code = mv.scode(r.ix, r.iy);  // < 0: occupied, else the box radius
+  const bool occupied = code < 0;
+  // the far cell of the free box on each axis is ix + sx * r (r = 0: the cell
+  // itself, a plain DDA step), written as a face index below
   const int fx = max(r.sx, 0), fy = max(r.sy, 0);  // 1 when moving +
-  const int face_x = cellwise ? r.ix + fx : (r.ix | 1) + r.sx * k;
-  const int face_y = cellwise ? r.iy + fy : (r.iy | 1) + r.sy * k;
+  const int face_x = r.ix + fx + r.sx * code;
+  const int face_y = r.iy + fy + r.sy * code;
   const double tx = ((double)face_x - r.x0) * r.idx;
   const double ty = ((double)face_y - r.y0) * r.idy;
   const bool xs = tx <= ty;
@@ -244,7 +242,7 @@ __device__ __forceinline__ double ray_range(const Ray& r, const EnvDev& d) {
 __device__ __forceinline__ int ray_hit(const Ray& r, const MapView& mv, const EnvDev& d) {
   if ((unsigned)r.ix >= (unsigned)d.W || (unsigned)r.iy >= (unsigned)d.H) return -1;
   const uint32_t code = mv.code(r.ix, r.iy);
-  const bool occ = code >= 0x80u && ((code >> ((r.ix + (r.iy << 1)) & 3)) & 1u);
+  const bool occ = code >= 0x80u;
   return occ ? r.iy * d.W + r.ix : -1;
 }
 
