@@ -54,54 +54,6 @@ struct DevDeviceGuard {
   }
 };
 
-// 2x2-block table: a block holding an occupied (or out-of-grid) cell stores
-// 0x80 | mask, where cell (ix, iy) = (2bx+dx, 2by+dy) is bit (ix + 2 iy) & 3
-// = dx + 2 ((bx + dy) & 1) (the march tests it with one shift-add); a free block
-// stores k = 2r + 1, r = (chessboard distance to the nearest such block) - 1
-// clamped to 63: the k x k blocks centred on it are all free (the march uses
-// k as is: the box's far cell is (ix | 1) + sx * k).
-void build_block_table(const uint8_t* occ, int H, int W, int Hb, int Wb, uint8_t* out) {
-  const int INF = 1 << 29;
-  std::vector<int> dist((size_t)Hb * Wb);
-  std::vector<uint8_t> mask((size_t)Hb * Wb, 0);
-  for (int by = 0; by < Hb; ++by)
-    for (int bx = 0; bx < Wb; ++bx) {
-      uint8_t mk = 0;
-      for (int dy = 0; dy < 2; ++dy)
-        for (int dx = 0; dx < 2; ++dx) {
-          const int iy = 2 * by + dy, ix = 2 * bx + dx;
-          if (iy >= H || ix >= W || occ[(size_t)iy * W + ix]) mk |= (uint8_t)(1u << ((ix + 2 * iy) & 3));
-        }
-      mask[(size_t)by * Wb + bx] = mk;
-      // outside the block grid counts as blocked: distance to the border
-      const int border = std::min(std::min(bx + 1, by + 1), std::min(Wb - bx, Hb - by));
-      dist[(size_t)by * Wb + bx] = mk ? 0 : std::min(border, INF);
-    }
-  // two-pass chessboard distance transform (exact for the L-inf metric)
-  for (int by = 0; by < Hb; ++by)
-    for (int bx = 0; bx < Wb; ++bx) {
-      int& d = dist[(size_t)by * Wb + bx];
-      if (bx > 0) d = std::min(d, dist[(size_t)by * Wb + bx - 1] + 1);
-      if (by > 0) {
-        d = std::min(d, dist[(size_t)(by - 1) * Wb + bx] + 1);
-        if (bx > 0) d = std::min(d, dist[(size_t)(by - 1) * Wb + bx - 1] + 1);
-        if (bx + 1 < Wb) d = std::min(d, dist[(size_t)(by - 1) * Wb + bx + 1] + 1);
-      }
-    }
-  for (int by = Hb - 1; by >= 0; --by)
-    for (int bx = Wb - 1; bx >= 0; --bx) {
-      int& d = dist[(size_t)by * Wb + bx];
-      if (bx + 1 < Wb) d = std::min(d, dist[(size_t)by * Wb + bx + 1] + 1);
-      if (by + 1 < Hb) {
-        d = std::min(d, dist[(size_t)(by + 1) * Wb + bx] + 1);
-        if (bx + 1 < Wb) d = std::min(d, dist[(size_t)(by + 1) * Wb + bx + 1] + 1);
-        if (bx > 0) d = std::min(d, dist[(size_t)(by + 1) * Wb + bx - 1] + 1);
-      }
-    }
-  for (size_t i = 0; i < dist.size(); ++i)
-    out[i] = mask[i] ? (uint8_t)(0x80u | mask[i]) : (uint8_t)(2 * std::min(dist[i] - 1, 63) + 1);
-}
-
 // Per-cell free-box table (the march's table): an occupied cell stores 0x80
 // (negative as a signed byte); a free cell stores r = (chessboard distance to
 // the nearest occupied or out-of-grid cell) - 1, clamped to 127: the

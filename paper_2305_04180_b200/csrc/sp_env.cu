@@ -9,12 +9,14 @@
 //   that lies inside one map whenever the map count allows, so a CTA stages
 //   one map once per launch.
 // * Per map, two tables live in shared memory, staged by one TMA bulk copy
-//   (cp.async.bulk + mbarrier): a 2x2-block table (signed byte: 0x80 | the
-//   occupancy mask of the block's cells, bit (ix + 2 iy) & 3, when any is
-//   occupied, else the side k = 2r + 1 of the all-free k x k-block box
-//   around it) that the march reads once per step, and a 1-bit occupancy
+//   (cp.async.bulk + mbarrier): a per-cell table (signed byte: 0x80 for an
+//   occupied cell, else the radius r of the all-free (2r+1)^2-cell box
+//   centred on it) that the march reads once per step, and a 1-bit occupancy
 //   bitmap (H x ceil(W/32) u32) for the exact disc-collision test.
-//   366 x 366 cells -> 33.5 KB + 17.6 KB.  Every map has an occupied border.
+//   366 x 366 cells -> 131 KB + 17.6 KB.  Every map has an occupied border.
+// * Scans write straight into the output rows (the noise z parks in the row
+//   until the ray retires), so a chunk needs no staging rows: 86 B of shared
+//   memory per scan slot, which is what leaves room for the per-cell table.
 // * A CTA walks its range in chunks of up to `chunk_cap` envs with CTA-wide
 //   phases separated by __syncthreads:
 //     A  thread-per-env physics, collision, events, shaped-reward partial,
@@ -26,7 +28,7 @@
 //        predicted scan first: warps take as many rays as they have idle
 //        slots (one shared atomic), two rays per lane;
 //     C  thread-per-env reward of running / timed-out envs, outputs, VecEnv
-//        statistics; then coalesced rows (post-step and post-reset).
+//        statistics.
 // * The march visits the same cells as the reference DDA (_cy.pyx:89-105) but
 //   jumps over free boxes in one step: at cell (ix,iy) with free box B, the
 //   ray leaves B through the face with the smaller exit parameter (ties go to
@@ -78,7 +80,7 @@ struct MapView {
   __device__ __forceinline__ uint32_t code(int ix, int iy) const {
     return blk[iy * Wb + ix];
   }
-  // the same byte sign-extended: < 0 for a mixed block, else the box side
+  // the same byte sign-extended: < 0 for an occupied cell, else the box radius
   __device__ __forceinline__ int scode(int ix, int iy) const {
     return ((const int8_t*)blk)[iy * Wb + ix];
   }
@@ -87,7 +89,7 @@ struct MapView {
   }
 };
 
-// disc_collides for one disc (_cy.pyx:109-158), exact fp64 test; the block
+// disc_collides for one disc (_cy.pyx:109-158), exact fp64 test; the cell
 // table proves most discs free with one lookup.
 __device__ __forceinline__ bool disc_hits(const MapView& mv, const EnvDev& d, double x, double y) {
   const double r = d.radius, cell = d.cell;
@@ -177,12 +179,13 @@ __device__ __forceinline__ int floor_i(double v) {  // floor(v), |v| < 2^31
 // One march step, branch-free: every lane of the warp executes it.  A
 // finished ray is a fixed point (it stays in its occupied cell, or re-derives
 // the same over-range exit without moving), so idle and finished rays can keep
-// stepping without a liveness test.  The block byte is either 0x80 | the occupancy mask of
-// the block's 2x2 cells (then the step is one cell, as _cy.pyx:89-96), or the
-// side k = 2r+1 of the free k x k-block box around it (then the ray leaves the
-// whole box).  Either way the ray exits through the face with the smaller
-// parameter (ties to x, as tmx <= tmy does) into the cell containing the
-// exit point.  Returns true when a live ray finished.  r.t then holds the
+// stepping without a liveness test.  The cell byte is negative for an
+// occupied cell (the ray stops there), else the radius r of the free
+// (2r+1)^2-cell box centred on the cell: r = 0 is one DDA cell step
+// (_cy.pyx:89-96), larger r lets the ray leave the whole box.  Either way it
+// exits through the face with the smaller parameter (ties to x, as tmx <= tmy
+// does) into the cell containing the exit point.  Returns true when the ray
+// has finished (idempotent once it has).  r.t then holds the
 // exit parameter of its last free cell: the range once clipped to max_range
 // (ray_range), and ray_hit() recovers the occupied cell it stopped in.
 // Every map has an occupied border (GridMap's invariant, checked by
@@ -483,8 +486,8 @@ __device__ __forceinline__ void set_error(const EnvDev& d, int code, int64_t row
 
 // LiDAR noise (core.py:237-241): every listed slot needs R standard normals
 // from blocks nctr[slot] .. nctr[slot]+nb-1 of its stream.  One work item per
-// Philox block, spread over the whole CTA; z is staged in the obs row.
-// z ~ N(0,1) of one noise block (4 beams) of `slot` into its staging row
+// Philox block, spread over the whole CTA; z parks in the slot's output row.
+// z ~ N(0,1) of one noise block (4 beams) of `slot` into its output row
 __device__ __forceinline__ void noise_block(const EnvDev& d, const Chunk& c, int slot, int b) {
   const Block4 blk = stream_block(d.seed, c.gid[slot], 0u, c.nctr[slot] + (uint64_t)b);
   float z[4];

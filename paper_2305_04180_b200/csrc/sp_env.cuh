@@ -25,12 +25,12 @@ struct MapConst {
 struct EnvDev {
   int64_t n;              // lanes (slots)
   int32_t R, D;           // beams, obs dim = 5 + R
-  int32_t H, W, Hb, Wb, WW;  // grid, 2x2-block grid, 32-bit words per bitmap row
+  int32_t H, W, Hb, Wb, WW;  // grid, march-table grid (= grid: per cell), 32-bit words per bitmap row
   int32_t n_maps;
   double cell, inv_cell, max_range, radius, proximity;
   int32_t timeout, spawn_attempts, auto_reset, n_actions;
-  int32_t need_k;         // block-box side 2r+1 that proves "no disc collision"
-  uint32_t blk_bytes;     // per-map block table bytes (16-byte padded)
+  int32_t need_k;         // cell-box radius that proves "no disc collision" (ceil(radius / cell))
+  uint32_t blk_bytes;     // per-map march (cell) table bytes (16-byte padded)
   uint32_t bits_bytes;    // per-map bitmap bytes
   uint32_t map_bytes;     // blk_bytes + bits_bytes
   double action_v[SP_MAX_ACTIONS + 1], action_w[SP_MAX_ACTIONS + 1];  // code 15 = (0, 0)
