@@ -350,6 +350,7 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
   bool busy_a = false, busy_b = false, fin_a = true, fin_b = true;
   bool drained = total == 0;
   int ea = 0, ja = 0, eb = 0, jb = 0;
+  float za = 0.0f, zb = 0.0f;  // the slots' prefetched noise (Fin::pre)
   Ray ra, rb;
   ray_park(ra);
   ray_park(rb);
@@ -359,11 +360,11 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
     const int na = __popc(ia), n_idle = na + __popc(ib);
     if (n_idle >= d.refill_min || drained) {
       if (busy_a && fin_a) {  // steps taken = moves + the finishing step
-        fin(ea, ja, ray_range(ra, d), kHit ? ray_hit(ra, mv, d) : -1, ra.n + 1);
+        fin(ea, ja, ray_range(ra, d), kHit ? ray_hit(ra, mv, d) : -1, ra.n + 1, za);
         busy_a = false;
       }
       if (busy_b && fin_b) {
-        fin(eb, jb, ray_range(rb, d), kHit ? ray_hit(rb, mv, d) : -1, rb.n + 1);
+        fin(eb, jb, ray_range(rb, d), kHit ? ray_hit(rb, mv, d) : -1, rb.n + 1, zb);
         busy_b = false;
       }
       if (drained) {
@@ -388,8 +389,9 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
           const int g = div_r(my_a, d);
           ea = c.list[g];
           ja = my_a - g * R;
+          za = fin.pre(ea, ja);
           if (ray_setup(ra, c.px[ea], c.py[ea], c.ch[ea], c.sh[ea], beam[ja], d)) {
-            fin(ea, ja, 0.0, -1, 1);  // origin outside the grid: range 0 (_cy.pyx:37-39)
+            fin(ea, ja, 0.0, -1, 1, za);  // origin outside the grid: range 0 (_cy.pyx:37-39)
             ray_park(ra);
           } else {
             busy_a = true;
@@ -400,8 +402,9 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
           const int g = div_r(my_b, d);
           eb = c.list[g];
           jb = my_b - g * R;
+          zb = fin.pre(eb, jb);
           if (ray_setup(rb, c.px[eb], c.py[eb], c.ch[eb], c.sh[eb], beam[jb], d)) {
-            fin(eb, jb, 0.0, -1, 1);
+            fin(eb, jb, 0.0, -1, 1, zb);
             ray_park(rb);
           } else {
             busy_b = true;
@@ -579,9 +582,13 @@ struct FinObs {
   Chunk c;
   int D;
   double max_range, inv_max_range, proximity;
-  __device__ __forceinline__ void operator()(int slot, int j, double t, int, int steps) const {
+  // z of beam j, parked in the output row by the noise pass: loaded when the
+  // ray is dispatched so the L2 round trip overlaps its march
+  __device__ __forceinline__ float pre(int slot, int j) const { return c.out0[slot][5 + j]; }
+  __device__ __forceinline__ void operator()(int slot, int j, double t, int, int steps,
+                                             float zpre) const {
     float* rowp = c.out0[slot];
-    const double z = (double)rowp[5 + j];
+    const double z = (double)zpre;
     const double v = dclip(dadd(t, dadd(0.0, dmul(c.sig[slot], z))), 0.0, max_range);
     const float o = (float)div_by(v, max_range, inv_max_range);
     rowp[5 + j] = o;
@@ -1004,7 +1011,8 @@ struct FinScan {
   int32_t* hit_cell;
   int64_t s0;
   int R;
-  __device__ __forceinline__ void operator()(int e, int j, double t, int hit, int) const {
+  __device__ __forceinline__ float pre(int, int) const { return 0.0f; }
+  __device__ __forceinline__ void operator()(int e, int j, double t, int hit, int, float) const {
     const int64_t o = (s0 + e) * R + j;
     ranges[o] = t;
     if (hit_cell) hit_cell[o] = hit;
