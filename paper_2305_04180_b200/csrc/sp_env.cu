@@ -601,7 +601,7 @@ struct FinObs {
 // Load map m's tables (TMA bulk copy into shared memory) -- or point at HBM.
 template <bool kSmem>
 __device__ __forceinline__ MapView bind_map(const EnvDev& d, int m, uint8_t* smem_maps,
-                                            uint64_t* bar, uint32_t& phase) {
+                                            uint64_t* bar, uint32_t& phase, bool wait = true) {
   const uint8_t* src = d.maps + (size_t)m * d.map_bytes;
   MapView mv;
   mv.W = d.W;
@@ -615,7 +615,7 @@ __device__ __forceinline__ MapView bind_map(const EnvDev& d, int m, uint8_t* sme
       mbar_expect_tx(bar, d.map_bytes);
       tma_bulk_g2s(smem_maps, src, d.map_bytes, bar);
     }
-    mbar_wait(bar, phase);
+    if (wait) mbar_wait(bar, phase);
     phase ^= 1u;
     mv.blk = smem_maps;
     mv.bits = (const uint32_t*)(smem_maps + d.blk_bytes);
@@ -711,7 +711,7 @@ struct StepA {
 __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, const MapView& mv,
                                           const MapConst& mc, const Chunk& c, int e, int64_t s,
                                           int64_t row, uint32_t gid, uint64_t& ctr, int cap,
-                                          int slot_cap) {
+                                          int slot_cap, uint64_t* mbar, int mpar) {
   StepA r;
   // the lane state is loaded before the action checks, so its DRAM round
   // trip overlaps the row map -> action one
@@ -766,6 +766,7 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
     y = dadd(y, ddy);
     h = wrap_angle(h1);
     // events (core.py:189-201)
+    if (mpar >= 0) mbar_wait(mbar, (uint32_t)mpar);  // the map tables (staged during the loads above)
     const bool coll = disc_hits(mv, d, x, y);
     const double gdx = dsub(mc.goal_x, x), gdy = dsub(mc.goal_y, y);
     const double d1 = __dsqrt_rn(dadd(dmul(gdx, gdx), dmul(gdy, gdy)));
@@ -872,6 +873,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
   const int D = d.D;
   const FinObs fin{c, D, d.max_range, d.inv_max_range, d.proximity};
   int m = 0, cur_map = -1;
+  int map_par = -1;  // parity of a map load not yet waited for, or -1
   // shared-memory tables always sit at the start of smem: seeding the view with
   // that address lets the march fold the table base into its LDS offsets
   MapView mv{};
@@ -882,7 +884,10 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
   for (int64_t s0 = sb; s0 < se;) {
     while (d.map_off[m + 1] <= s0) ++m;
     if (m != cur_map) {
-      mv = bind_map<kSmem>(d, m, smem, bar, phase);
+      // the TMA lands while phase A loads its lanes; step_env waits right
+      // before its first table read
+      map_par = kSmem ? (int)phase : -1;
+      mv = bind_map<kSmem>(d, m, smem, bar, phase, false);
       cur_map = m;
       SP_STAMP(2);
 #ifdef SP_TIMING
@@ -924,6 +929,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     }
     if (a.mode != MODE_STEP) {
       const bool want = a.mode == MODE_RESET_ALL || (act && a.reset_mask[row] != 0);
+      if (map_par >= 0) mbar_wait(bar, (uint32_t)map_par);
       if (act && want) {
         if (reset_env(d, mv, mc, s, gid, ctr, c, e, a.states + row * d.D)) {
           c.wmode[e] = W_STATE;
@@ -938,7 +944,8 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       }
     } else if (act) {
       const double ret_prev = d.ret[s];  // issued early: only the outputs wait on it
-      const StepA r = step_env(d, a, mv, mc, c, e, s, row, gid, ctr, d.chunk_cap, d.slot_cap);
+      const StepA r = step_env(d, a, mv, mc, c, e, s, row, gid, ctr, d.chunk_cap, d.slot_cap, bar,
+                               map_par);
       d.ctr[s] = ctr;
       if (r.live) {
         if (r.ev == 1 || r.ev == 2) {  // terminal reward: no scan needed
@@ -950,6 +957,10 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
           c.retp[e] = ret_prev;
         }
       }
+    }
+    if (map_par >= 0) {  // threads without an env have not waited for the tables yet
+      mbar_wait(bar, (uint32_t)map_par);
+      map_par = -1;
     }
     __syncthreads();
     SP_STAMP(3);
