@@ -99,9 +99,23 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
                   int64_t env_id_offset, int device, SpEnv** out);
 int sp_env_destroy(SpEnv* env);
 int sp_env_reset_all(SpEnv* env, uint64_t seed, float* states /* dev (N, 5+R) */, void* stream);
+/* states and store_states must not overlap (with auto-reset an env's two scans
+ * park their LiDAR noise in different rows): SP_EINVAL otherwise. */
 int sp_env_step(SpEnv* env, const int64_t* actions /* dev (N) */, float* states,
                 float* store_states, double* rewards, uint8_t* dones, uint8_t* truncated,
                 int8_t* events, void* stream);
+/* Recording (parity / inspection; off by default, costs nothing when off):
+ * every following reset_all / step / reset_lanes also writes, per caller row
+ * and beam (dev int32/f64 [N][R], row-major, NULL = not recorded),
+ *   hit_store  the occupied cell iy*W+ix each ray of the post-step scan (the
+ *              store_states rows) stopped in, -1 at max range / grid exit;
+ *   hit_state  the same for the scan behind the returned states rows (the
+ *              fresh-spawn scan of an env that reset, else the post-step one);
+ *   scan_state that scan's noisy clipped range in cm: SimBatch.last_scan
+ *              (sim/core.py:97, 237-241).
+ * The bit-exact hit-cell parity tests read these against the oracle's DDA. */
+int sp_env_set_recording(SpEnv* env, int32_t* hit_store, int32_t* hit_state,
+                         double* scan_state);
 /* Host-buffer step: the reference's numpy step_batch contract (vecenv.py:94-116)
  * for callers holding host memory.  h_actions: N int64; h_out: one contiguous
  * block of sp_env_host_out_bytes(env) bytes laid out as
@@ -140,6 +154,12 @@ int sp_env_read_state(SpEnv* env, int field, double* host_out, void* stream);
 /* overwrite one pose field (ids 0-6 above, 17 start_cos, 18 start_sin) from a
  * host array (external order) -- the reference tests' place() (test_env.py:37-42) */
 int sp_env_write_state(SpEnv* env, int field, const double* host_in, void* stream);
+/* The delay FIFO of every lane (SimBatch._pending, sim/core.py:106, 156,
+ * 176-182) as host u64 [N][4] in caller row order: a shift register of 4-bit
+ * action codes, nibble q of the 256-bit word = the action issued q steps ago
+ * (q = 0 newest), code 15 = the (0, 0) filler a reset queues; the lane's
+ * control delay d says how many of the nibbles are pending (q < d). */
+int sp_env_read_fifo(SpEnv* env, uint64_t* host_out, void* stream);
 /* SimBatch.reset_lane (core.py:114-161) for the lanes with mask[i] != 0 (device,
  * external order), continuing each lane's stream; writes their rows of states. */
 int sp_env_reset_lanes(SpEnv* env, const uint8_t* mask, float* states, void* stream);

@@ -70,6 +70,7 @@ def load_lib():
                                      c_dp, c_i64p]
     lib.or_env_reset_stats.argtypes = [ctypes.c_void_p]
     lib.or_env_err_lane.argtypes = [ctypes.c_void_p]
+    lib.or_env_get_cells.argtypes = [ctypes.c_void_p, c_i64p, c_i64p, c_dp]
     lib.or_cast_rays.argtypes = [c_u8p, c_dp, ctypes.c_int64, ctypes.c_int64, c_i64p, c_dp, c_dp,
                                  c_dp, c_dp, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
                                  c_dp, c_i64p]
@@ -280,6 +281,65 @@ class OracleVecEnv:
 
     def reset_stats(self):
         self._lib.or_env_reset_stats(self._h)
+
+    def cells(self) -> dict:
+        """Hit cells (iy*W+ix, -1 none) of the last step's post-step scans
+        (``store``) and of the scans behind the current states rows
+        (``state``), plus ``last_scan`` (cm, ``core.py:97``); (N, R) each."""
+        k = (self.n, self.n_beams)
+        store = np.empty(k, dtype=np.int64)
+        last = np.empty(k, dtype=np.int64)
+        ls = np.empty(k, dtype=np.float64)
+        self._lib.or_env_get_cells(self._h, _p(store, c_i64p), _p(last, c_i64p), _p(ls, c_dp))
+        return {"store": store, "state": last, "last_scan": ls}
+
+
+class ShardedOracle:
+    """``OracleVecEnv`` over ``shards`` contiguous env-id ranges stepped on
+    host threads (the C calls release the GIL).  Lanes are independent and
+    keyed by global env id, so this is exactly the
+    single-process oracle, at host-core speed for BASELINE-size parity runs."""
+
+    def __init__(self, maps, n_copies, ranges, config, env_id_offset=0, shards=None):
+        from concurrent.futures import ThreadPoolExecutor
+        n = int(n_copies)
+        shards = max(1, min(int(shards or os.cpu_count() or 1), n))
+        cuts = [n * k // shards for k in range(shards + 1)]
+        self.cuts = cuts
+        self.n = n
+        self.parts = [OracleVecEnv(maps, cuts[k + 1] - cuts[k], ranges, config,
+                                   env_id_offset=env_id_offset + cuts[k])
+                      for k in range(shards)]
+        self._pool = ThreadPoolExecutor(shards)
+
+    def _map(self, fn):
+        return list(self._pool.map(fn, range(len(self.parts))))
+
+    def reset_all(self, seed):
+        return np.concatenate(self._map(lambda k: self.parts[k].reset_all(seed)))
+
+    def step_batch(self, actions) -> OracleStep:
+        a = np.ascontiguousarray(actions, dtype=np.int64)
+        outs = self._map(lambda k: self.parts[k].step_batch(a[self.cuts[k]:self.cuts[k + 1]]))
+        return OracleStep(*(np.concatenate([o[f] for o in outs]) for f in range(6)))
+
+    def pose(self) -> dict:
+        ps = self._map(lambda k: self.parts[k].pose())
+        return {f: np.concatenate([p[f] for p in ps]) for f in ps[0]}
+
+    def cells(self) -> dict:
+        cs = self._map(lambda k: self.parts[k].cells())
+        return {f: np.concatenate([c[f] for c in cs]) for f in cs[0]}
+
+    def stats(self) -> dict:
+        """Per-copy counters (the recent-returns deque is per shard: not merged)."""
+        ss = self._map(lambda k: self.parts[k].stats())
+        return {f: np.concatenate([s[f] for s in ss])
+                for f in ("episodes", "arrivals", "return_sum", "first_event", "first_return",
+                          "first_steps")}
+
+    def close(self):
+        self._pool.shutdown()
 
 
 # -- replay ----------------------------------------------------------------------

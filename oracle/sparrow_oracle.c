@@ -306,6 +306,9 @@ typedef struct {
   int64_t recent_count; /* total appended */
   /* scratch */
   double *scan_raw, *scan_min;
+  /* hit cells (or_cast_one's hit_cell) of the scan behind the current states
+   * row (cells_last) and of the last step's post-step scan (cells_store) */
+  int64_t *cells_last, *cells_store;
   int err_lane;
 } OrEnv;
 
@@ -341,6 +344,7 @@ OrEnv* or_env_create(int32_t n_beams, double max_range, double robot_radius, dou
   A(ep_return, double, n); A(episodes, int64_t, n); A(arrivals, int64_t, n);
   A(return_sum, double, n); A(first_event, int8_t, n); A(first_return, double, n);
   A(first_steps, int64_t, n); A(scan_raw, double, n * n_beams); A(scan_min, double, n);
+  A(cells_last, int64_t, n * n_beams); A(cells_store, int64_t, n * n_beams);
 #undef A
   for (int64_t i = 0; i < n; ++i) { e->needs_reset[i] = 1; e->first_event[i] = -1; }
   return e;
@@ -352,7 +356,7 @@ void or_env_destroy(OrEnv* e) {
                   e->start_sin, e->pk, e->pdt, e->pvl, e->pva, e->psig, e->pdelay, e->step_count,
                   e->needs_reset, e->last_scan, e->qv, e->qhead, e->qlen, e->rng, e->ep_return,
                   e->episodes, e->arrivals, e->return_sum, e->first_event, e->first_return,
-                  e->first_steps, e->scan_raw, e->scan_min};
+                  e->first_steps, e->scan_raw, e->scan_min, e->cells_last, e->cells_store};
   for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i) free(ptrs[i]);
   free(e);
 }
@@ -400,7 +404,7 @@ static void or_scan_lane(OrEnv* e, int64_t i) {
   for (int j = 0; j < R; ++j) {
     double ang = e->heading[i] + e->offsets[j]; /* core.py:224 */
     raw[j] = or_cast_one(occ, edt, e->H, e->W, e->x[i], e->y[i], cos(ang), sin(ang), e->cell,
-                         e->max_range, NULL, NULL);
+                         e->max_range, e->cells_last + i * R + j, NULL);
     if (raw[j] < mn) mn = raw[j];
   }
   e->scan_min[i] = mn; /* core.py:205 */
@@ -532,6 +536,7 @@ int or_env_step(OrEnv* e, const int64_t* actions, float* states, float* store_st
     int8_t ev = coll ? 1 : (arrived ? 2 : (timed_out ? 3 : 0));
     /* scan + noise (core.py:203-206) */
     or_scan_lane(e, i);
+    memcpy(e->cells_store + i * R, e->cells_last + i * R, sizeof(int64_t) * (size_t)R);
     /* reward, reward.py:55-83 */
     double alpha = or_bearing(e->x[i], e->y[i], e->heading[i], e->goal_x[m], e->goal_y[m]);
     double d2 = or_cross_track(e->x[i], e->y[i], e->start_x[i], e->start_y[i], e->goal_x[m],
@@ -607,3 +612,12 @@ void or_env_reset_stats(OrEnv* e) {
 }
 
 int or_env_err_lane(const OrEnv* e) { return e->err_lane; }
+
+/* hit cells of the last step's post-step scans and of the scans behind the
+ * current states rows, plus last_scan (core.py:97), n * n_beams each */
+void or_env_get_cells(const OrEnv* e, int64_t* store, int64_t* last, double* last_scan) {
+  const size_t k = (size_t)e->n * (size_t)e->n_beams;
+  if (store) memcpy(store, e->cells_store, sizeof(int64_t) * k);
+  if (last) memcpy(last, e->cells_last, sizeof(int64_t) * k);
+  if (last_scan) memcpy(last_scan, e->last_scan, sizeof(double) * k);
+}

@@ -1,9 +1,9 @@
 // sp_capi.cu -- extern "C" implementation of include/sparrow.h.
 //
-// Host responsibilities: map preprocessing (bit-packing, 2x2-block free-box
-// table by an exact chessboard distance transform), map-major slot ordering,
-// device SoA allocation, launch geometry (one CTA per SM, shared memory =
-// one map's tables + per-warp scratch), error codes.
+// Host responsibilities: map preprocessing (bit-packing, the per-cell
+// free-box table by an exact chessboard distance transform), map-major slot
+// ordering, device SoA allocation, launch geometry (one CTA per SM, shared
+// memory = one map's tables + the chunk scratch), error codes.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -123,6 +123,10 @@ struct SpEnv {
   int64_t* d_scan = nullptr;
   cudaEvent_t scan_copied = nullptr;
   uint8_t* d_host_stage = nullptr;  // sp_env_step_host: actions | output block (device)
+  // sp_env_set_recording: hit cells / noisy ranges of every launch (null = off)
+  int32_t* rec_hit_store = nullptr;
+  int32_t* rec_hit_state = nullptr;
+  double* rec_scan_state = nullptr;
   std::mutex mu;
 
   template <class T>
@@ -358,7 +362,13 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   d.n_actions = cfg->n_actions;
   {
     const int K = (int)std::ceil(cfg->robot_radius_cm / cell);
-    d.need_k = K;  // a cell box of radius >= K covers the disc's cell bbox
+    // a cell box of radius >= K around the disc's centre cell covers its cell
+    // bbox.  disc_hits finds the centre cell as floor(x * inv_cell): exact
+    // when the cell size is a power of two, else it may land one cell off
+    // next to a cell edge, which one more ring of free cells absorbs
+    int e2 = 0;
+    const bool pow2 = std::frexp(cell, &e2) == 0.5;
+    d.need_k = K + (pow2 ? 0 : 1);
   }
   for (int c = 0; c <= SP_MAX_ACTIONS; ++c) {
     d.action_v[c] = c < cfg->n_actions ? cfg->action_table[2 * c] : 0.0;
@@ -495,7 +505,10 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   env->grid = plan.grid;
   env->threads = plan.threads;
   env->smem = plan.smem;
-  const void* kernels_[] = {(const void*)env_step_kernel<true>, (const void*)env_step_kernel<false>,
+  const void* kernels_[] = {(const void*)env_step_kernel<true, false>,
+                            (const void*)env_step_kernel<false, false>,
+                            (const void*)env_step_kernel<true, true>,
+                            (const void*)env_step_kernel<false, true>,
                             (const void*)env_scan_kernel<true>, (const void*)env_scan_kernel<false>};
   cudaError_t e1 = cudaSuccess, e2 = cudaSuccess;
   for (const void* k : kernels_) {
@@ -520,13 +533,34 @@ int sp_env_destroy(SpEnv* env) {
   return SP_OK;
 }
 
-static int launch_env(SpEnv* env, const StepArgs& a, cudaStream_t st) {
-  if (env->d.smem_maps)
-    env_step_kernel<true><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
-  else
-    env_step_kernel<false><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
+static int launch_env(SpEnv* env, StepArgs a, cudaStream_t st) {
+  a.hit_store = env->rec_hit_store;
+  a.hit_state = env->rec_hit_state;
+  a.scan_state = env->rec_scan_state;
+  const bool rec = a.hit_store || a.hit_state || a.scan_state;
+  if (env->d.smem_maps) {
+    if (rec)
+      env_step_kernel<true, true><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
+    else
+      env_step_kernel<true, false><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
+  } else {
+    if (rec)
+      env_step_kernel<false, true><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
+    else
+      env_step_kernel<false, false><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(SP_ECUDA, std::string("env_step_kernel: ") + cudaGetErrorString(e));
+  return SP_OK;
+}
+
+int sp_env_set_recording(SpEnv* env, int32_t* hit_store, int32_t* hit_state,
+                         double* scan_state) {
+  if (!env) return fail(SP_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(env->mu);
+  env->rec_hit_store = hit_store;
+  env->rec_hit_state = hit_state;
+  env->rec_scan_state = scan_state;
   return SP_OK;
 }
 
@@ -536,7 +570,9 @@ int sp_env_reset_all(SpEnv* env, uint64_t seed, float* states, void* stream) {
   std::lock_guard<std::mutex> lk(env->mu);
   cudaStream_t st = (cudaStream_t)stream;
   env->d.seed = seed;
-  env->step_index = 0;
+  // step_index keeps increasing across reset_all: the recent-returns ring is
+  // keyed (step_index << 32 | row), and the reference's deque keeps appending
+  // in time order across resets (vecenv.py:79, 109)
   SP_CUDA(cudaMemsetAsync(env->d.ctr, 0, sizeof(uint64_t) * env->n, st));
   SP_CUDA(cudaMemsetAsync(env->d.err, 0, 16, st));
   StepArgs a{};
@@ -545,13 +581,30 @@ int sp_env_reset_all(SpEnv* env, uint64_t seed, float* states, void* stream) {
   return launch_env(env, a, st);
 }
 
+static int step_locked(SpEnv* env, const int64_t* actions, float* states, float* store_states,
+                       double* rewards, uint8_t* dones, uint8_t* truncated, int8_t* events,
+                       cudaStream_t stream);
+
 int sp_env_step(SpEnv* env, const int64_t* actions, float* states, float* store_states,
                 double* rewards, uint8_t* dones, uint8_t* truncated, int8_t* events,
                 void* stream) {
   if (!env || !actions || !states || !store_states || !rewards || !dones || !truncated || !events)
     return fail(SP_EINVAL, "null argument");
+  {
+    const uintptr_t rb = (uintptr_t)env->n * (uintptr_t)env->D * sizeof(float);
+    const uintptr_t s0 = (uintptr_t)states, s1 = (uintptr_t)store_states;
+    if (s0 < s1 + rb && s1 < s0 + rb)
+      return fail(SP_EINVAL, "states and store_states must not overlap");
+  }
   DevDeviceGuard guard(env->device);
   std::lock_guard<std::mutex> lk(env->mu);
+  return step_locked(env, actions, states, store_states, rewards, dones, truncated, events,
+                     (cudaStream_t)stream);
+}
+
+static int step_locked(SpEnv* env, const int64_t* actions, float* states, float* store_states,
+                       double* rewards, uint8_t* dones, uint8_t* truncated, int8_t* events,
+                       cudaStream_t stream) {
   StepArgs a{};
   a.mode = MODE_STEP;
   a.step_index = ++env->step_index;
@@ -562,7 +615,7 @@ int sp_env_step(SpEnv* env, const int64_t* actions, float* states, float* store_
   a.dones = dones;
   a.truncated = truncated;
   a.events = events;
-  return launch_env(env, a, (cudaStream_t)stream);
+  return launch_env(env, a, stream);
 }
 
 int64_t sp_env_host_out_bytes(SpEnv* env) {
@@ -573,6 +626,7 @@ int64_t sp_env_host_out_bytes(SpEnv* env) {
 int sp_env_step_host(SpEnv* env, const int64_t* h_actions, void* h_out, void* stream) {
   if (!env || !h_actions || !h_out) return fail(SP_EINVAL, "null argument");
   DevDeviceGuard guard(env->device);
+  std::lock_guard<std::mutex> lk(env->mu);  // one staging block per handle
   const int64_t n = env->n, D = env->D, out_bytes = sp_env_host_out_bytes(env);
   if (!env->d_host_stage) {
     uint8_t* p = nullptr;
@@ -588,8 +642,8 @@ int sp_env_step_host(SpEnv* env, const int64_t* h_actions, void* h_out, void* st
   float* states = (float*)(o + 8 * n);
   float* store = states + n * D;
   uint8_t* dones = (uint8_t*)(store + n * D);
-  const int rc = sp_env_step(env, (const int64_t*)dev_act, states, store, rewards, dones,
-                             dones + n, (int8_t*)(dones + 2 * n), stream);
+  const int rc = step_locked(env, (const int64_t*)dev_act, states, store, rewards, dones,
+                             dones + n, (int8_t*)(dones + 2 * n), st);
   if (rc != SP_OK) return rc;
   SP_CUDA(cudaMemcpyAsync(h_out, o, out_bytes, cudaMemcpyDeviceToHost, st));
   SP_CUDA(cudaStreamSynchronize(st));
@@ -769,6 +823,21 @@ int sp_env_read_state(SpEnv* env, int field, double* host_out, void* stream) {
   return SP_OK;
 }
 
+int sp_env_read_fifo(SpEnv* env, uint64_t* host_out, void* stream) {
+  if (!env || !host_out) return fail(SP_EINVAL, "null argument");
+  DevDeviceGuard guard(env->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = env->n;
+  std::vector<uint64_t> h((size_t)(4 * n));
+  SP_CUDA(cudaMemcpyAsync(h.data(), env->d.hist, 8 * 4 * (size_t)n, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t s = env->slot_of_env[i];
+    for (int w = 0; w < 4; ++w) host_out[4 * i + w] = h[(size_t)(w * n + s)];
+  }
+  return SP_OK;
+}
+
 int sp_env_write_state(SpEnv* env, int field, const double* host_in, void* stream) {
   if (!env || !host_in) return fail(SP_EINVAL, "null argument");
   DevDeviceGuard guard(env->device);
@@ -933,9 +1002,13 @@ int sp_rb_append(SpReplay* rb, const float* states, const int64_t* actions, cons
   if (!states || !actions || !rewards || !next_states || !dones) return fail(SP_EINVAL, "null argument");
   DevDeviceGuard guard(rb->device);
   std::lock_guard<std::mutex> lk(rb->mu);
-  const int64_t flat = n * rb->dim;
+  const int64_t vecs = (2 * n * rb->dim + 3) / 4;  // float4 chunks of s and s2
   const int64_t new_size = std::min(rb->size + n, rb->cap);
-  rb_append_kernel<<<grid_for(flat, 256), 256, 0, (cudaStream_t)stream>>>(
+  // ~4 vectors per thread (the loop keeps four loads in flight), at least
+  // one thread per row for the small columns, at most 8 CTAs per SM
+  const int64_t thr = std::max<int64_t>(n, (vecs + 3) / 4);
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((thr + 255) / 256, 148 * 8));
+  rb_append_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
       rb->s, rb->a, rb->r, rb->s2, rb->dn, rb->cap, rb->dim, rb->cursor, states, actions, rewards,
       reward_is_f64, next_states, dones, n, rb->d_size, new_size);
   SP_CUDA(cudaGetLastError());

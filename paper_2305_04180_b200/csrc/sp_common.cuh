@@ -65,14 +65,21 @@ __device__ __forceinline__ int64_t draw_integer(const Block4& b, int64_t lo, int
   return lo + (int64_t)__umul64hi(word64(b), (uint64_t)(hi - lo));
 }
 
-// Four standard normals per block (Box-Muller on (x0,x1), (x2,x3)).  fp32 is
-// enough here: the noise never feeds a branch, and the stated parity
-// tolerance on noisy ranges is 1e-5 relative (z error ~1e-7 relative).
+// -2 ln(u1), u1 = (x + 1) / 2^32 in (0, 1], to fp32 relative precision: for
+// u1 >= 1/2 through log1p of the exact integer complement (a plain fp32 u1
+// would keep only 24 of the 32 bits and lose r = sqrt(-2 ln u1) near u1 = 1).
+__device__ __forceinline__ float neg2log_u1(uint32_t x) {
+  if (x >= 0x80000000u) return -2.0f * log1pf(-(float)(0xFFFFFFFFu - x) * 0x1.0p-32f);
+  return -2.0f * logf(((float)x + 1.0f) * 0x1.0p-32f);
+}
+
+// Four standard normals per block (Box-Muller on (x0,x1), (x2,x3)), the RNG
+// contract's mapping (oracle or_normals) evaluated in fp32: z is within
+// ~5e-7 absolute of the fp64 value (|z| <= 6.7), i.e. a noisy range within
+// sigma * 5e-7 cm.  The noise never feeds a branch.
 __device__ __forceinline__ void draw_normals4(const Block4& b, float z[4]) {
-  float u1a = ((float)b.x0 + 1.0f) * 0x1.0p-32f;
-  float u1b = ((float)b.x2 + 1.0f) * 0x1.0p-32f;
-  float ra = sqrtf(-2.0f * logf(u1a));
-  float rb = sqrtf(-2.0f * logf(u1b));
+  float ra = sqrtf(neg2log_u1(b.x0));
+  float rb = sqrtf(neg2log_u1(b.x2));
   float sa, ca, sb, cb;
   sincospif(2.0f * ((float)b.x1 * 0x1.0p-32f), &sa, &ca);
   sincospif(2.0f * ((float)b.x3 * 0x1.0p-32f), &sb, &cb);

@@ -578,23 +578,45 @@ __device__ __forceinline__ void header_row(const MapConst& mc, double x, double 
 // Finish functor of the ray phase: noisy normalized obs into the staging row
 // (core.py:237-241, 257) and the proximity flag (reward.py:70: scan_min < 30
 // is "some ray < 30", core.py:205).
+// kRec (recording builds of the launch, StepArgs::hit_store etc.): also the
+// ray's hit cell and noisy range at the caller row of the scan's rows.
+template <bool kRec>
 struct FinObs {
   Chunk c;
   int D;
   double max_range, inv_max_range, proximity;
+  // recording only
+  int32_t *hit_store, *hit_state;
+  double* scan_state;
+  const float* store_base;  // a.store_states (null outside MODE_STEP)
+  uint64_t store_span;      // n * D floats
+  uint32_t gid0;            // (uint32) env_id_offset: row = gid - gid0
+  int R;
   // z of beam j, parked in the output row by the noise pass: loaded when the
   // ray is dispatched so the L2 round trip overlaps its march
   __device__ __forceinline__ float pre(int slot, int j) const { return c.out0[slot][5 + j]; }
-  __device__ __forceinline__ void operator()(int slot, int j, double t, int, int steps,
+  __device__ __forceinline__ void operator()(int slot, int j, double t, int hit, int steps,
                                              float zpre) const {
     float* rowp = c.out0[slot];
     const double z = (double)zpre;
     const double v = dclip(dadd(t, dadd(0.0, dmul(c.sig[slot], z))), 0.0, max_range);
     const float o = (float)div_by(v, max_range, inv_max_range);
     rowp[5 + j] = o;
-    if (float* r1 = c.out1[slot]) r1[5 + j] = o;
+    float* r1 = c.out1[slot];
+    if (r1) r1[5 + j] = o;
     if (t < proximity) c.prox[slot] = 1;
     atomicMax(&c.qacc[slot], (uint32_t)steps);
+    if constexpr (kRec) {
+      const int64_t k = (int64_t)(c.gid[slot] - gid0) * R + j;
+      // post-step scans fill a store_states row (and the states row too when
+      // the env keeps running); fresh-spawn scans fill a states row
+      const bool store = store_base && (uint64_t)(rowp - store_base) < store_span;
+      if (store && hit_store) hit_store[k] = hit;
+      if (!store || r1) {
+        if (hit_state) hit_state[k] = hit;
+        if (scan_state) scan_state[k] = v;
+      }
+    }
   }
 };
 
@@ -855,7 +877,7 @@ __device__ __forceinline__ void finish_env(const EnvDev& d, const StepArgs& a, c
 
 
 // ------------------------------------------------------------ the kernel ---
-template <bool kSmem>
+template <bool kSmem, bool kRec>
 __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     env_step_kernel(const __grid_constant__ EnvDev d, const __grid_constant__ StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -871,7 +893,9 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
   if (threadIdx.x == 0) bar[1] = (uint64_t)clock64();  // CTA start (kept in smem, not a register)
   const int64_t sb = d.cta_begin[blockIdx.x], se = d.cta_begin[blockIdx.x + 1];
   const int D = d.D;
-  const FinObs fin{c, D, d.max_range, d.inv_max_range, d.proximity};
+  const FinObs<kRec> fin{c, D, d.max_range, d.inv_max_range, d.proximity, a.hit_store,
+                         a.hit_state, a.scan_state, a.store_states,
+                         (uint64_t)d.n * (uint64_t)D, (uint32_t)d.env_id_offset, d.R};
   int m = 0, cur_map = -1;
   int map_par = -1;  // parity of a map load not yet waited for, or -1
   // shared-memory tables always sit at the start of smem: seeding the view with
@@ -970,7 +994,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     noise_phase(d, c, n_slots, kpre, cta_grp());
     __syncthreads();
     SP_STAMP(4);
-    ray_phase<false>(mv, d, c, beam, n_slots, fin);
+    ray_phase<kRec>(mv, d, c, beam, n_slots, fin);
     __syncthreads();
     SP_STAMP(5);
     store_history(d, c, n_slots);
@@ -1002,7 +1026,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       order_slots(c, n2, cta_grp());
       noise_phase(d, c, n2, 0, cta_grp());
       __syncthreads();
-      ray_phase<false>(mv, d, c, beam, n2, fin);
+      ray_phase<kRec>(mv, d, c, beam, n2, fin);
       __syncthreads();
       store_history(d, c, n2);
     }

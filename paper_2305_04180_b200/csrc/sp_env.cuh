@@ -2,9 +2,9 @@
 #pragma once
 #include "sp_common.cuh"
 
-// Launch shape: SP_CTAS_PER_SM resident CTAs of SP_CTA_THREADS threads.  Two
-// CTAs per SM let one CTA's ray-queue tail and phase barriers overlap the
-// other's work; each holds its own copy of its map's tables.
+// Launch shape: SP_CTAS_PER_SM resident CTAs of SP_CTA_THREADS threads (one
+// 768-thread CTA per SM by default; a build with SP_CTAS_PER_SM=2 gives each
+// of two CTAs its own copy of its map's tables).
 #ifndef SP_CTAS_PER_SM
 #define SP_CTAS_PER_SM 1
 #endif
@@ -90,6 +90,15 @@ struct StepArgs {
   uint8_t* dones;
   uint8_t* truncated;
   int8_t* events;
+  // optional recording (sp_env_set_recording; null = off, the default): per
+  // caller row x beam, the occupied cell iy*W+ix each ray stopped in (-1:
+  // max range / grid exit) for the post-step scan (store_states rows) and the
+  // scan behind the returned states rows, and that scan's noisy clipped range
+  // in cm (SimBatch.last_scan, core.py:97, 237-241).  Only the kRec kernel
+  // instantiation writes them.
+  int32_t* hit_store;
+  int32_t* hit_state;
+  double* scan_state;
 };
 
 struct ScanArgs {

@@ -116,29 +116,65 @@ __global__ void disc_collides_kernel(const uint8_t* __restrict__ occ, int64_t H,
 }
 
 // ---------------------------------------------------------------- replay ---
-__global__ void rb_append_kernel(float* __restrict__ rs, int64_t* __restrict__ ra,
-                                 float* __restrict__ rr, float* __restrict__ rs2,
-                                 uint8_t* __restrict__ rd, int64_t cap, int32_t dim,
-                                 int64_t cursor, const float* __restrict__ s,
-                                 const int64_t* __restrict__ a, const void* __restrict__ r,
-                                 int r_f64, const float* __restrict__ s2,
-                                 const uint8_t* __restrict__ dn, int64_t n,
-                                 int64_t* __restrict__ d_size, int64_t new_size) {
-  const int64_t flat = n * dim, ring = cap * dim, base = cursor * dim;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *d_size = new_size;  // the ring's fill, on device
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < flat;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t dst = base + i;
-    if (dst >= ring) dst -= ring;
-    rs[dst] = s[i];
-    rs2[dst] = s2[i];
-    if (i < n) {
-      int64_t row = cursor + i;
-      if (row >= cap) row -= cap;
-      ra[row] = a[i];
-      rr[row] = r_f64 ? (float)((const double*)r)[i] : ((const float*)r)[i];  // replay.py:53
-      rd[row] = dn[i] ? 1 : 0;
+// Ring append (replay.py:48-67): the n new rows land at rows cursor .. and
+// wrap to 0, so each column is at most two contiguous segments.  The state
+// columns s, s2 are row-contiguous float32 (D per row): per segment one flat
+// float copy with 16-byte stores at 16-byte aligned ring addresses (sources
+// read as float4 when equally aligned -- always when the cursor is a
+// multiple of 4 rows -- else as 4 coalesced scalars), several independent
+// vectors in flight per thread.  The small columns (a i64, r f32, done u8,
+// 13 B/row) follow in the same launch, one thread per row.
+
+// dst[0..count) = src[0..count) over `nt` threads (thread index `t`)
+__device__ __forceinline__ void copy_f32(float* __restrict__ dst, const float* __restrict__ src,
+                                         int64_t count, int64_t t, int64_t nt) {
+  const int head = (int)((((uintptr_t)16 - ((uintptr_t)dst & 15)) & 15) >> 2);
+  const int64_t h = head < count ? head : count;
+  if (t < h) dst[t] = src[t];
+  const int64_t nvec = (count - h) >> 2;
+  float4* __restrict__ d4 = (float4*)(dst + h);
+  const float* sv = src + h;
+  if (((uintptr_t)sv & 15) == 0) {
+    const float4* __restrict__ s4 = (const float4*)sv;
+    int64_t i = t;
+    for (; i + 3 * nt < nvec; i += 4 * nt) {  // four loads in flight
+      const float4 a = __ldcs(s4 + i), b = __ldcs(s4 + i + nt);
+      const float4 c = __ldcs(s4 + i + 2 * nt), e = __ldcs(s4 + i + 3 * nt);
+      d4[i] = a; d4[i + nt] = b; d4[i + 2 * nt] = c; d4[i + 3 * nt] = e;
     }
+    for (; i < nvec; i += nt) d4[i] = __ldcs(s4 + i);
+  } else {
+    for (int64_t i = t; i < nvec; i += nt) {
+      const float* q = sv + 4 * i;
+      d4[i] = make_float4(__ldcs(q), __ldcs(q + 1), __ldcs(q + 2), __ldcs(q + 3));
+    }
+  }
+  const int64_t done = h + 4 * nvec;
+  if (t < count - done) dst[done + t] = src[done + t];
+}
+
+__global__ void __launch_bounds__(256) rb_append_kernel(
+    float* __restrict__ rs, int64_t* __restrict__ ra, float* __restrict__ rr,
+    float* __restrict__ rs2, uint8_t* __restrict__ rd, int64_t cap, int32_t dim, int64_t cursor,
+    const float* __restrict__ s, const int64_t* __restrict__ a, const void* __restrict__ r,
+    int r_f64, const float* __restrict__ s2, const uint8_t* __restrict__ dn, int64_t n,
+    int64_t* __restrict__ d_size, int64_t new_size) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  if (t == 0) *d_size = new_size;  // the ring's fill, on device (sp_rb_sample_dev)
+  const int64_t n1 = n < cap - cursor ? n : cap - cursor;  // rows before the wrap
+  const int64_t D = dim;
+  copy_f32(rs + cursor * D, s, n1 * D, t, nt);
+  copy_f32(rs2 + cursor * D, s2, n1 * D, t, nt);
+  if (n > n1) {
+    copy_f32(rs, s + n1 * D, (n - n1) * D, t, nt);
+    copy_f32(rs2, s2 + n1 * D, (n - n1) * D, t, nt);
+  }
+  for (int64_t i = t; i < n; i += nt) {
+    const int64_t row = i < n1 ? cursor + i : i - n1;
+    ra[row] = a[i];
+    rr[row] = r_f64 ? (float)((const double*)r)[i] : ((const float*)r)[i];  // replay.py:53
+    rd[row] = dn[i] ? 1 : 0;
   }
 }
 

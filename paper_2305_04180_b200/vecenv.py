@@ -159,6 +159,32 @@ class SimView:
     def episode_return(self) -> np.ndarray:
         return self._read(16)
 
+    @property
+    def last_scan(self) -> np.ndarray:
+        """(N, R) noisy clipped ranges (cm) behind the last returned states rows
+        (``core.py:97, 159-161, 206``).  Exact float64 while recording is on
+        (``VecEnv.record``); otherwise recovered from those rows' float32
+        LiDAR columns (relative error <= 6e-8)."""
+        return self._env._last_scan()
+
+    @property
+    def params(self) -> list:
+        """Per-lane ``SimParams`` of the current episodes (``core.py:104, 126``)."""
+        from paper_2305_04180_b200.sim import SimParams
+        k, dt, d = self._read(7), self._read(8), self._read(9)
+        vl, va, sg = self._read(10), self._read(11), self._read(12)
+        return [SimParams(k=float(k[i]), control_interval_s=float(dt[i]),
+                          control_delay_steps=int(d[i]), v_linear_max_cm_s=float(vl[i]),
+                          v_angular_max_rad_s=float(va[i]), lidar_noise_std_cm=float(sg[i]))
+                for i in range(self.n_lanes)]
+
+    @property
+    def _pending(self) -> list:
+        """Per-lane delay queues of (v_linear, v_angular) targets, oldest first
+        (``core.py:106, 156, 176-182``), decoded from the device FIFO."""
+        from collections import deque
+        return [deque(q) for q in self._env.pending_actions()]
+
 
 class VecEnv:
     def __init__(self, maps: Sequence, n_copies: int,
@@ -241,6 +267,8 @@ class VecEnv:
         self.env_id_offset = int(env_id_offset)
         self._sim = None
         self._seeded = False
+        self._last_states = None  # the states rows last returned (SimView.last_scan)
+        self._rec = None          # recording buffers (record())
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -295,6 +323,7 @@ class VecEnv:
                                               states.data_ptr(), self._stream()), "reset_all")
         self._seeded = True
         self.check()  # MapError if a lane found no spawn pose (core.py:144-147)
+        self._last_states = states
         return states
 
     def step_batch(self, actions, out: StepBatch | None = None) -> StepBatch:
@@ -323,6 +352,7 @@ class VecEnv:
                                    out.dones.data_ptr(), out.truncated.data_ptr(),
                                    out.events.data_ptr(), self._stream())
         _lib.check(rc, "step")
+        self._last_states = out.states
         return out
 
     def host_buffers(self) -> "HostStep":
@@ -399,6 +429,12 @@ class VecEnv:
         _lib.check(self._lib.sp_env_reset_lanes(self._h, m.data_ptr(), states.data_ptr(),
                                                 self._stream()), "reset_lanes")
         self.check()
+        if self._last_states is not None and self._last_states.shape == states.shape:
+            keep = self._last_states.clone()
+            keep[m.bool()] = states[m.bool()]
+            self._last_states = keep
+        else:
+            self._last_states = states
         return states
 
     def place(self, field: str, values) -> None:
@@ -410,6 +446,60 @@ class VecEnv:
                                                  (self.n_copies,)))
         _lib.check(self._lib.sp_env_write_state(self._h, ids[field], v.ctypes.data_as(_lib.c_dp),
                                                 self._stream()), "place")
+
+    # -- recording (parity / inspection) -------------------------------------
+    def record(self, on: bool = True) -> None:
+        """Make every following launch also record, per row and beam, the
+        occupied cell each LiDAR ray stopped in (post-step scan and the scan
+        behind the states rows) and the noisy float64 ranges behind the states
+        rows (``sp_env_set_recording``).  Off by default: it costs a kernel
+        variant with a few extra stores per ray."""
+        torch = self._torch
+        if on:
+            n, R = self.n_copies, self.n_beams
+            dev = self.device
+            self._rec = {"hit_store": torch.full((n, R), -2, dtype=torch.int32, device=dev),
+                         "hit_state": torch.full((n, R), -2, dtype=torch.int32, device=dev),
+                         "scan_state": torch.zeros((n, R), dtype=torch.float64, device=dev)}
+            ptrs = [self._rec[k].data_ptr() for k in ("hit_store", "hit_state", "scan_state")]
+        else:
+            self._rec = None
+            ptrs = [None, None, None]
+        _lib.check(self._lib.sp_env_set_recording(self._h, *ptrs), "record")
+
+    def recorded(self) -> dict:
+        """The recording buffers (device tensors, overwritten by the next launch):
+        ``hit_store`` / ``hit_state`` int32 (N, R) cells iy*W+ix or -1,
+        ``scan_state`` float64 (N, R) cm."""
+        if self._rec is None:
+            raise RuntimeError("recording is off: call record() before stepping")
+        return self._rec
+
+    def _last_scan(self) -> np.ndarray:
+        if self._rec is not None:
+            return self._rec["scan_state"].cpu().numpy()
+        if self._last_states is None:
+            return np.full((self.n_copies, self.n_beams), float(self.config.lidar.max_range_cm))
+        cols = self._last_states[:, 5:].double().cpu().numpy()
+        return cols * float(self.config.lidar.max_range_cm)
+
+    def pending_actions(self) -> list:
+        """Per-lane tuples of pending (v_linear, v_angular) targets, oldest
+        first: the delay queue ``SimBatch._pending`` (``core.py:156, 176-182``)."""
+        n = self.n_copies
+        words = np.empty((n, 4), dtype=np.uint64)
+        _lib.check(self._lib.sp_env_read_fifo(self._h, words.ctypes.data, self._stream()),
+                   "read_fifo")
+        delay = self._read_state(9).astype(np.int64)
+        table = [tuple(float(v) for v in p) for p in self.config.action_table]
+        out = []
+        for i in range(n):
+            q = []
+            for k in range(int(delay[i]) - 1, -1, -1):  # nibble k = issued k steps ago
+                code = int((int(words[i, k >> 4]) >> (4 * (k & 15))) & 15)
+                q.append((0.0, 0.0) if code == 15 else table[code])
+            out.append(tuple(q))
+        return out
 
     # -- reporting -------------------------------------------------------------
     def _per_copy_arrays(self) -> dict:

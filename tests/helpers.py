@@ -10,11 +10,26 @@ from paper_2305_04180_b200.sim import DiversityRanges, EnvConfig, GridMap, Lidar
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
-# Parity tolerance for floating outputs (north star: 1e-5 relative, fp32);
-# absolute floor = fp32 resolution of each component's scale.
+# Parity tolerances.  The north star allows 1e-5 relative (fp32) for poses,
+# velocities, LiDAR ranges and rewards; the kernels meet far tighter bars, and
+# the tests hold them there so regressions show:
+# * obs (float32, normalized to [-1, 1]): 2 float32 ulps at 1.0 -- the two
+#   sides round fp64 values that agree to ~1e-13 (CUDA vs glibc libm ulps,
+#   fp32 Box-Muller LiDAR noise ~1e-7 of sigma) to float32, so they may land
+#   on adjacent floats, never further apart.  The oracle meets the same bar
+#   against the reference (test_oracle_golden.OBS_ATOL);
+# * rewards (float64): 1e-10 absolute + relative.  The reward arithmetic
+#   itself agrees to ulps, but poses drift apart by up to ~1e-9 cm over an
+#   episode: integrate_unicycle's x += (v/w)(sin h1 - sin h0) (kinematics.py:
+#   52-55) multiplies a 1-ulp libm sin difference (CUDA vs glibc) by v/w,
+#   up to 1.8e7 at |w| just above the 1e-6 straight-line cut.  Largest
+#   reward difference observed at cfg3 scale: 1.2e-12;
+# * poses: 1e-5 relative (the north star's own bar; observed ~1e-13).
 RTOL = 1e-5
-ATOL_OBS = 2e-6     # obs are normalized to [-1, 1]
-ATOL_REWARD = 1e-6
+ATOL_OBS = 2.4e-7
+RTOL_OBS = 2.4e-7
+ATOL_REWARD = 1e-10
+RTOL_REWARD = 1e-10
 
 
 def golden(name):
@@ -61,3 +76,11 @@ def assert_close(got, want, rtol=RTOL, atol=0.0, what=""):
         raise AssertionError(
             f"{what}: {int(bad.sum())}/{bad.size} outside rtol={rtol} atol={atol}; first "
             f"{[(tuple(i), float(got[tuple(i)]), float(want[tuple(i)])) for i in idx]}")
+
+
+def assert_obs(got, want, what=""):
+    assert_close(got, want, rtol=RTOL_OBS, atol=ATOL_OBS, what=what)
+
+
+def assert_rewards(got, want, what=""):
+    assert_close(got, want, rtol=RTOL_REWARD, atol=ATOL_REWARD, what=what)

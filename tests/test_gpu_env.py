@@ -403,7 +403,7 @@ def test_many_resets_in_one_step_use_the_overflow_pass():
     slots -- the overflow pass must produce the same rows as the oracle."""
     from paper_2305_04180_b200 import VecEnv
     from oracle.oracle import OracleVecEnv
-    from helpers import ATOL_OBS, assert_close
+    from helpers import assert_close, assert_obs
     maps = [make_map(40)]
     cfg = config(32, timeout_steps=3)
     n = 3000
@@ -415,8 +415,8 @@ def test_many_resets_in_one_step_use_the_overflow_pass():
         a = np.zeros(n, dtype=np.int64)  # slow turns: everyone survives to the timeout
         g, c = gpu.step_batch(a), cpu.step_batch(a)
         assert np.array_equal(g.events.cpu().numpy(), c.events)
-        assert_close(g.states.cpu().numpy(), c.states, atol=ATOL_OBS, what=f"states {t}")
-        assert_close(g.store_states.cpu().numpy(), c.store_states, atol=ATOL_OBS, what="store")
+        assert_obs(g.states.cpu().numpy(), c.states, what=f"states {t}")
+        assert_obs(g.store_states.cpu().numpy(), c.store_states, what="store")
 
 
 def test_mass_timeouts_across_all_ctas():
@@ -425,7 +425,7 @@ def test_mass_timeouts_across_all_ctas():
     of reset scans) and the rows still match the oracle."""
     from paper_2305_04180_b200 import VecEnv
     from oracle.oracle import OracleVecEnv
-    from helpers import ATOL_OBS, assert_close
+    from helpers import assert_close, assert_obs
     import torch
     maps = load_maps(16)
     cfg = config(32, timeout_steps=4)
@@ -439,8 +439,8 @@ def test_mass_timeouts_across_all_ctas():
         g, c = gpu.step_batch(a), cpu.step_batch(a)
         torch.cuda.synchronize()
         assert np.array_equal(g.events.cpu().numpy(), c.events), t
-        assert_close(g.states.cpu().numpy(), c.states, atol=ATOL_OBS, what=f"states {t}")
-        assert_close(g.store_states.cpu().numpy(), c.store_states, atol=ATOL_OBS, what="store")
+        assert_obs(g.states.cpu().numpy(), c.states, what=f"states {t}")
+        assert_obs(g.store_states.cpu().numpy(), c.store_states, what="store")
     gpu.check()
 
 
@@ -573,3 +573,95 @@ def test_c_abi_host_step_with_pageable_buffers():
         assert np.array_equal(x.truncated.cpu().numpy(), tr.astype(bool))
         assert np.array_equal(x.events.cpu().numpy(), ev)
     del ctypes
+
+
+# -- drop-in surface: SimBatch views the reference's own tests read ----------
+
+@pytest.mark.parametrize("delay", [0, 2, 17])
+def test_pending_actions_queue(delay):  # sim/env.py:39, 94; core.py:156, 176-182
+    """RobotState.pending_actions / sim._pending mirror the reference deque:
+    d (0, 0) fillers after a reset, then each issued target in order."""
+    env = make_env(60, k=0.5, control_delay_steps=delay)
+    env.reset(4)
+    place(env, 20.0, 20.0, 0.0)
+    assert env.state.pending_actions == ((0.0, 0.0),) * delay
+    table = [tuple(p) for p in EnvConfig().action_table]
+    issued = []
+    for t in range(delay + 3):
+        a = (1, 3, 2, 0, 4)[t % 5]
+        env.step(a)
+        issued.append(table[a])
+        want = ([(0.0, 0.0)] * delay + issued)[-delay:] if delay else []
+        assert env.state.pending_actions == tuple(want), t
+        assert list(env.vec.sim._pending[0]) == want
+
+
+def test_last_scan_and_params_views():  # core.py:97, 104; sim/env.py:80-99
+    """sim.last_scan is the noisy clipped range behind the states rows: exact
+    f64 while recording, and equal (to float32 rounding) to the obs columns."""
+    from oracle.oracle import OracleVecEnv
+    from paper_2305_04180_b200 import VecEnv
+    maps = load_maps(4)
+    n, seed = 96, 21
+    g = VecEnv(maps, n, ranges(0.3), config(32))
+    c = OracleVecEnv(maps, n, ranges(0.3), config(32))
+    s_plain = g.reset_all(seed)
+    approx = g.sim.last_scan  # not recording: from the float32 obs columns
+    c.reset_all(seed)
+    want = c.cells()["last_scan"]
+    assert_close = __import__("helpers").assert_close
+    assert_close(approx, want, rtol=1.2e-7, atol=1e-9, what="last_scan (obs-derived)")
+    g.record()
+    for t in range(6):
+        a = random_actions(seed, np.arange(n), t)
+        g.step_batch(a)
+        c.step_batch(a)
+        assert_close(g.sim.last_scan, c.cells()["last_scan"], rtol=1e-9, atol=1e-5,
+                     what=f"last_scan step {t}")
+    ps = g.sim.params
+    assert len(ps) == n and all(isinstance(p, SimParams) for p in ps)
+    assert [p.control_delay_steps for p in ps] == list(g.sim.param_delay)
+    assert np.allclose([p.k for p in ps], g.sim.param_k)
+    del s_plain
+
+
+def test_overlapping_state_buffers_rejected():
+    """states and store_states must be distinct rows (each scan parks its
+    noise in its own row): overlapping buffers raise ValueError."""
+    import torch
+    from paper_2305_04180_b200 import VecEnv
+    from paper_2305_04180_b200.vecenv import StepBatch
+    env = VecEnv(load_maps(1), 8, ranges(0.0), config(32))
+    env.reset_all(1)
+    D = env.state_dim
+    rows = torch.empty((8, D), dtype=torch.float32, device=env.device)
+    out = StepBatch(rows, torch.empty(8, dtype=torch.float64, device=env.device),
+                    torch.empty(8, dtype=torch.bool, device=env.device),
+                    torch.empty(8, dtype=torch.bool, device=env.device), rows,
+                    torch.empty(8, dtype=torch.int8, device=env.device))
+    with pytest.raises(ValueError):
+        env.step_batch(np.zeros(8, np.int64), out=out)
+
+
+def test_recent_returns_keep_time_order_across_reset_all():  # vecenv.py:79, 84-92, 109
+    """reset_all does not clear the recent-returns deque in the reference; the
+    returns of episodes after a second reset_all are the newest entries."""
+    from oracle.oracle import OracleVecEnv
+    from paper_2305_04180_b200 import VecEnv
+    maps = load_maps(2)
+    n = 64
+    cfg = config(32, timeout_steps=4)
+    g = VecEnv(maps, n, ranges(0.3), cfg)
+    c = OracleVecEnv(maps, n, ranges(0.3), cfg)
+    for seed, steps in ((1, 9), (2, 9)):
+        g.reset_all(seed)
+        c.reset_all(seed)
+        for t in range(steps):
+            a = random_actions(seed, np.arange(n), t)
+            g.step_batch(a)
+            c.step_batch(a)
+    got = g.snapshot_stats().recent_returns
+    want = c.stats()["recent_returns"]
+    assert len(got) == len(want) == 256
+    # the same multiset per step; order within a step follows env id on both sides
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-12)

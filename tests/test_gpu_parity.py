@@ -9,7 +9,7 @@ within 1e-5 relative (+ fp32-resolution absolute floor, see helpers.py).
 import numpy as np
 import pytest
 
-from helpers import ATOL_OBS, ATOL_REWARD, assert_close, config, golden, load_maps, make_map, ranges
+from helpers import assert_close, assert_obs, assert_rewards, config, golden, load_maps, make_map, ranges
 from oracle.philox_shim import random_actions
 
 pytestmark = pytest.mark.gpu
@@ -25,7 +25,7 @@ def _replay_golden(name, maps, rg, n):
     seed = int(z["seed"])
     env = _vec(maps, n, rg, config(32))
     s0 = env.reset_all(seed).cpu().numpy()
-    assert_close(s0, z["reset_states"], atol=ATOL_OBS, what="reset states")
+    assert_obs(s0, z["reset_states"], what="reset states")
     steps = z["rewards"].shape[0]
     obs_steps = list(z["obs_steps"])
     k = 0
@@ -35,13 +35,10 @@ def _replay_golden(name, maps, rg, n):
         assert np.array_equal(ev, z["events"][t]), f"events differ at step {t}"
         assert np.array_equal(b.dones.cpu().numpy(), z["dones"][t]), t
         assert np.array_equal(b.truncated.cpu().numpy(), z["truncated"][t]), t
-        assert_close(b.rewards.cpu().numpy(), z["rewards"][t], atol=ATOL_REWARD,
-                     what=f"rewards step {t}")
+        assert_rewards(b.rewards.cpu().numpy(), z["rewards"][t], what=f"rewards step {t}")
         if k < len(obs_steps) and obs_steps[k] == t:
-            assert_close(b.store_states.cpu().numpy(), z["store_states"][k], atol=ATOL_OBS,
-                         what=f"store_states step {t}")
-            assert_close(b.states.cpu().numpy(), z["states"][k], atol=ATOL_OBS,
-                         what=f"states step {t}")
+            assert_obs(b.store_states.cpu().numpy(), z["store_states"][k], what=f"store_states step {t}")
+            assert_obs(b.states.cpu().numpy(), z["states"][k], what=f"states step {t}")
             k += 1
     sim = env.sim
     assert_close(sim.x, z["final_x"], what="x")
@@ -73,18 +70,16 @@ def test_vs_oracle(n, steps, div):
     seed = 4242
     gpu = _vec(maps, n, ranges(div), cfg)
     cpu = OracleVecEnv(maps, n, ranges(div), cfg)
-    assert_close(gpu.reset_all(seed).cpu().numpy(), cpu.reset_all(seed), atol=ATOL_OBS,
-                 what="reset")
+    assert_obs(gpu.reset_all(seed).cpu().numpy(), cpu.reset_all(seed), what="reset")
     for t in range(steps):
         a = random_actions(seed, np.arange(n), t)
         g = gpu.step_batch(a)
         c = cpu.step_batch(a)
         assert np.array_equal(g.events.cpu().numpy(), c.events), f"events step {t}"
         assert np.array_equal(g.dones.cpu().numpy(), c.dones)
-        assert_close(g.rewards.cpu().numpy(), c.rewards, atol=ATOL_REWARD, what=f"reward {t}")
-        assert_close(g.store_states.cpu().numpy(), c.store_states, atol=ATOL_OBS,
-                     what=f"store {t}")
-        assert_close(g.states.cpu().numpy(), c.states, atol=ATOL_OBS, what=f"states {t}")
+        assert_rewards(g.rewards.cpu().numpy(), c.rewards, what=f"reward {t}")
+        assert_obs(g.store_states.cpu().numpy(), c.store_states, what=f"store {t}")
+        assert_obs(g.states.cpu().numpy(), c.states, what=f"states {t}")
     p = cpu.pose()
     assert_close(gpu.sim.x, p["x"], what="x")
     assert_close(gpu.sim.heading, p["heading"], atol=1e-12, what="heading")
@@ -162,15 +157,15 @@ def _vs_oracle_run(maps, n, div, steps, seed, n_beams=32):
     cfg = config(n_beams)
     gpu = _vec(maps, n, ranges(div), cfg)
     cpu = OracleVecEnv(maps, n, ranges(div), cfg)
-    assert_close(gpu.reset_all(seed).cpu().numpy(), cpu.reset_all(seed), atol=ATOL_OBS, what="reset")
+    assert_obs(gpu.reset_all(seed).cpu().numpy(), cpu.reset_all(seed), what="reset")
     for t in range(steps):
         a = random_actions(seed, np.arange(n), t)
         g = gpu.step_batch(a)
         c = cpu.step_batch(a)
         assert np.array_equal(g.events.cpu().numpy(), c.events), f"events step {t}"
-        assert_close(g.rewards.cpu().numpy(), c.rewards, atol=ATOL_REWARD, what=f"reward {t}")
-        assert_close(g.states.cpu().numpy(), c.states, atol=ATOL_OBS, what=f"states {t}")
-        assert_close(g.store_states.cpu().numpy(), c.store_states, atol=ATOL_OBS, what=f"store {t}")
+        assert_rewards(g.rewards.cpu().numpy(), c.rewards, what=f"reward {t}")
+        assert_obs(g.states.cpu().numpy(), c.states, what=f"states {t}")
+        assert_obs(g.store_states.cpu().numpy(), c.store_states, what=f"store {t}")
     return gpu
 
 

@@ -196,3 +196,32 @@ def test_mapgen_matches_reference_small(tmp_path):
     assert np.array_equal(m.edt_cells(), ref_m.edt_cells())
     assert m.to_ascii((30.0, 30.0)) == ref_m.to_ascii((30.0, 30.0))
     assert m.to_ascii() == ref_m.to_ascii()
+
+
+@pytest.mark.parametrize("max_range", [150.0, 300.0, 500.0])
+def test_ray_cell_count_equals_pure_dda(max_range):
+    """raycells.dda_cells (the bench's ray-cells/s accounting: Manhattan
+    distance origin cell -> stopping cell, + 1) equals the oracle's
+    cell-by-cell pure DDA count (_cy.pyx:89-105 without the EDT jump)."""
+    import torch
+    from paper_2305_04180_b200.raycells import dda_cells
+    maps = load_maps(16)
+    occ = np.stack([m.occupancy for m in maps]).astype(np.uint8)
+    edt = np.stack([O.edt_cells(m.occupancy) for m in maps])
+    rng = np.random.default_rng(int(max_range))
+    n, R = 400, 32
+    qm = rng.integers(0, 16, n)
+    qx, qy = rng.uniform(12, 354, n), rng.uniform(12, 354, n)
+    qh = rng.uniform(-np.pi, np.pi, n)
+    off = LidarConfig(n_beams=R).beam_offsets()
+    ang = qh[:, None] + off[None, :]
+    args = (np.repeat(qm, R), np.repeat(qx, R), np.repeat(qy, R), np.cos(ang).ravel(),
+            np.sin(ang).ravel(), 1.0, max_range)
+    _, hit = O.cast_rays(occ, edt, *args, return_cells=True)
+    want = O.count_dda_cells(occ, *args).reshape(n, R)
+    hit = hit.reshape(n, R)
+    got = dda_cells(qx, qy, qh, off, hit, 366, 1.0, max_range)
+    assert (got == want).mean() > 0.9999 and np.abs(got - want).max() <= 1
+    got_t = dda_cells(torch.from_numpy(qx), torch.from_numpy(qy), torch.from_numpy(qh), off,
+                      torch.from_numpy(hit), 366, 1.0, max_range)
+    assert np.array_equal(got_t.numpy(), got)
