@@ -1,4 +1,6 @@
-"""Benchmark: Sparrow env-steps/s on B200 (BASELINE.json metric, cfg3 workload).
+"""Benchmark: Sparrow env-steps/s on B200 (BASELINE.json metric, cfg3 workload),
+plus the metric's second clause (LiDAR ray-cells/s vs roofline, cfg4) and the
+replay path (cfg5 ring).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
@@ -10,18 +12,28 @@ draws random actions the same way on the host).  A "step" = one
 ``VecEnv.step_batch`` over all envs incl. fused auto-reset; weak scaling
 (fixed envs per GPU), env ids sharded contiguously across ranks.
 
-* value   -- device time: K steps with actions already in HBM; each step timed
-             with CUDA events on the launching stream; L2 flushed between
-             timed steps outside the events (256 MiB write, then a 256 MiB
-             read so the flush's dirty lines drain outside too); max over ranks.
-* e2e     -- same metric through the public API with HOST buffers: per step
-             pinned actions H2D, step, D2H of every StepBatch field; timed
-             with CUDA events around copies + step.
-* roofline -- dominant kernel env_step_kernel: algorithmic HBM bytes per
-             env-step x N / mean launch time vs the
-             measured copy bandwidth in MEASURED_PEAKS.json.
+* value    -- device time: K steps with actions already in HBM; each step
+              timed with CUDA events on the launching stream; L2 flushed
+              between timed steps outside the events (256 MiB write, then a
+              256 MiB read so the flush's dirty lines drain outside too); max
+              over ranks.
+* e2e      -- same metric through the public API with HOST buffers: per step
+              pinned actions H2D, step, D2H of every StepBatch field; timed
+              with CUDA events around copies + step.  The process and its
+              pinned buffers are bound to the GPU's NUMA node first.
+* roofline -- the binding resource of env_step_kernel: shared
+              memory, one 32-bit word per pure-DDA ray-cell.  Ray-cells per
+              launch are counted in this run (a recorded step after the timed
+              region: per-ray hit cells -> raycells.dda_cells), peak =
+              SMs x 128 B/clk x the SM clock sampled during the timed region.
+              roofline_hbm keeps the algorithmic-bytes view.
+* lidar    -- cfg4: the marcher alone (env_scan_kernel) at R in {32,128,256} x
+              max range in {150,300,500} cm: rays/s, ray-cells/s, frac.
+* replay   -- cfg5 ring (1M x D=37): append GB/s and frac of HBM (4,096-row
+              appends, and 65,536-row appends = one cfg3 step of
+              transitions), sample latency at B=256.
 * cpu_baseline -- the reference itself (oracle/_ref, Cython backend) on this
-             host's cores, P processes x a bounded sample of the workload.
+              host's cores, P processes x N/P envs of the same workload.
 
 ``--impl reference`` times only the reference CPU implementation (rank 0;
 other ranks exit 0) and prints the same JSON line with impl=reference.
@@ -53,6 +65,7 @@ METRIC = "Sparrow env-steps/sec"
 UNIT = "env-steps/s"
 # algorithmic HBM bytes per env-step at R=32 (D=37)
 BYTES_PER_ENV_STEP = 161 + 376
+MAX_MHZ = 1965.0  # B200 max SM clock (fallback when nvidia-smi is unavailable)
 
 
 def env_config():
@@ -68,12 +81,48 @@ def load_maps():
 
 def ncu_metrics():
     """Per-launch metrics of env_step_kernel from the committed ncu capture
-    (DRAM traffic, issue-slot utilization): profiles/ncu_step_traffic.json."""
+    (DRAM traffic, issue-slot utilization): profiles/ncu_step_traffic.json,
+    used only when its source hash is this build's (else reported stale)."""
+    from paper_2305_04180_b200.build import source_hash
     p = os.path.join(ROOT, "profiles", "ncu_step_traffic.json")
     if not os.path.exists(p):
-        return {}
+        return {"stale": "no capture"}
     with open(p) as f:
-        return json.load(f)
+        d = json.load(f)
+    cur = source_hash()
+    if d.get("source_hash") != cur:
+        return {"stale": f"capture of sources {d.get('source_hash')} != this build {cur}"}
+    return d
+
+
+def numa_bind(local_rank: int) -> dict:
+    """Bind this process to the CPUs of the GPU's NUMA node (pinned host
+    buffers allocated afterwards are first-touched there), so the e2e copies
+    do not cross the socket interconnect.  Returns what was done."""
+    import torch
+    try:
+        p = torch.cuda.get_device_properties(local_rank)
+        bus = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bus}/numa_node") as f:
+            node = int(f.read().strip())
+        if node < 0:
+            return {"node": None, "pci": bus, "note": "no NUMA affinity reported"}
+        with open(f"/sys/devices/system/node/node{node}/cpulist") as f:
+            spec = f.read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            lo, _, hi = part.partition("-")
+            cpus.update(range(int(lo), int(hi or lo) + 1))
+        prev = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, cpus)
+        return {"node": node, "pci": bus, "cpus": spec, "_prev": prev}
+    except (OSError, ValueError, AttributeError) as e:
+        return {"node": None, "note": f"not bound: {e}"}
+
+
+def smem_peak_gbs(n_sm: int, mhz: float) -> float:
+    """Shared-memory bandwidth: 32 banks x 4 B per clock per SM."""
+    return n_sm * 128.0 * mhz * 1e6 / 1e9
 
 
 def measured_peaks():
@@ -188,13 +237,15 @@ def _ref_worker(args):
     return n_local * steps, wall
 
 
-def cpu_reference(seconds=4.0, n_local=2048, procs=None):
-    """env-steps/s of the reference on all host cores (P independent processes)."""
+def cpu_reference(seconds=4.0, n_total=N_PER_GPU, procs=None):
+    """env-steps/s of the reference on all host cores: P independent processes,
+    each stepping N/P envs of the workload."""
     import multiprocessing as mp
     mode = "reference" if os.path.isdir(os.path.join(ROOT, "oracle", "_ref", "color_rl")) else "port"
     if mode == "port":
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
-    procs = procs or os.cpu_count() or 1
+    procs = procs or len(os.sched_getaffinity(0)) or 1
+    n_local = max(1, n_total // procs)
     ctx = mp.get_context("spawn")
     with ctx.Pool(procs) as pool:
         res = pool.map(_ref_worker, [(n_local, seconds, SEED + i, mode) for i in range(procs)])
@@ -207,15 +258,170 @@ def cpu_reference(seconds=4.0, n_local=2048, procs=None):
 
 # ----------------------------------------------------------------------- ours --
 
+def _poses(maps, n, seed=0, clearance=10.0):
+    """n LiDAR origins spread evenly over the maps, uniform over each map's
+    cells with > `clearance` cells of free space (cfg4 scan workload)."""
+    from scipy import ndimage
+    rng = np.random.default_rng(seed)
+    per = n // len(maps)
+    qx, qy, qh, qm = [], [], [], []
+    for m, gm in enumerate(maps):
+        free = np.argwhere(ndimage.distance_transform_edt(~gm.occupancy) > clearance)
+        pick = free[rng.integers(0, len(free), per)]
+        qy.append(pick[:, 0] + rng.random(per))
+        qx.append(pick[:, 1] + rng.random(per))
+        qh.append(rng.uniform(-np.pi, np.pi, per))
+        qm.append(np.full(per, m))
+    return tuple(map(np.concatenate, (qx, qy, qh, qm)))
+
+
+def lidar_sweep(dev, flush_l2, n_sm, mhz, reps=7, n_poses=65_536):
+    """cfg4: the marcher alone (env_scan_kernel, VecEnv.scan_raw) on n_poses
+    origins over the 16 maps, R x max range; device time (median of reps,
+    L2 flushed before each), ray-cells counted from the returned hit cells."""
+    import torch
+    from paper_2305_04180_b200 import VecEnv
+    from paper_2305_04180_b200.raycells import dda_cells
+    from paper_2305_04180_b200.sim import DiversityRanges, EnvConfig, LidarConfig
+    maps = load_maps()
+    qx, qy, qh, qm = _poses(maps, n_poses)
+    n = len(qx)
+    qoff = np.zeros(len(maps) + 1, dtype=np.int64)
+    qoff[1:] = np.cumsum(np.bincount(qm, minlength=len(maps)))
+    xd, yd, hd = (torch.from_numpy(v).to(dev) for v in (qx, qy, qh))  # grouped by map
+    stream = torch.cuda.current_stream(dev)
+    rows = []
+    for R in (32, 128, 256):
+        for mr in (150.0, 300.0, 500.0):
+            cfg = EnvConfig(lidar=LidarConfig(n_beams=R, max_range_cm=mr))
+            env = VecEnv(maps, 16, DiversityRanges(), cfg, device=dev)
+            out = torch.empty((n, R), dtype=torch.float64, device=dev)
+            cells = torch.empty((n, R), dtype=torch.int32, device=dev)
+            for _ in range(2):
+                env.scan_raw(qoff, xd, yd, hd, out, cells)
+            ms = []
+            for k in range(reps):
+                flush_l2(k)
+                s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s_.record(stream)
+                env.scan_raw(qoff, xd, yd, hd, out, cells)
+                e_.record(stream)
+                e_.synchronize()
+                ms.append(s_.elapsed_time(e_))
+            t = statistics.median(ms) / 1e3
+            mean_cells = float(dda_cells(xd, yd, hd, cfg.lidar.beam_offsets(), cells,
+                                         maps[0].occupancy.shape[1], 1.0, mr).double().mean())
+            rc = n * R * mean_cells / t
+            peak = smem_peak_gbs(n_sm, mhz) / 4 * 1e9  # words (= ray-cells) per second
+            rows.append({"beams": R, "max_range_cm": mr, "ms": t * 1e3, "rays_per_s": n * R / t,
+                         "mean_dda_cells_per_ray": mean_cells, "ray_cells_per_s": rc,
+                         "frac": rc / peak})
+            del env
+    return {"workload": f"cfg4: {n} origins over the 16 maps (uniform over cells with >10 "
+                        "cells clearance), noise-free scans, env_scan_kernel",
+            "peak_ray_cells_per_s": smem_peak_gbs(n_sm, mhz) / 4 * 1e9,
+            "peak_basis": f"{n_sm} SMs x 32 words/clk x {mhz:.0f} MHz (one SMEM word per "
+                          "pure-DDA cell, SURVEY 8(d))",
+            "sweep": rows}
+
+
+def replay_bench(dev, flush_l2, peak_gbs, reps=7):
+    """cfg5 ring (1M rows, D = 37): device time of sp_rb_append for 4,096 and
+    65,536-row batches (the ring wraps during the run) and of sp_rb_sample
+    at B = 256.  Append moves 2 x 309 B per row (read the batch, write the
+    ring), the same read+write accounting as the measured copy peak."""
+    import torch
+    from paper_2305_04180_b200 import _lib
+    from paper_2305_04180_b200.replay import ReplayBuffer
+    C, D = 1_000_000, 5 + N_BEAMS
+    rb = ReplayBuffer(C, D, device=dev)
+    lib = rb._lib
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    row_bytes = 4 * D * 2 + 8 + 4 + 1
+    res = {"workload": f"cfg5: ring of {C} transitions, D = {D} ({row_bytes} B/row: s, s2 "
+                       "f32, a i64, r f32, done u8)", "row_bytes": row_bytes, "append": []}
+    for n in (4096, 65_536):
+        g = torch.Generator(device=dev)
+        g.manual_seed(n)
+        s = torch.rand((n, D), device=dev, generator=g)
+        s2 = torch.rand((n, D), device=dev, generator=g)
+        a = torch.randint(0, 5, (n,), device=dev, generator=g)
+        r = torch.rand(n, device=dev, generator=g)
+        d = torch.rand(n, device=dev, generator=g) < 0.01
+
+        def append():
+            _lib.check(lib.sp_rb_append(rb._h, s.data_ptr(), a.data_ptr(), r.data_ptr(), 0,
+                                        s2.data_ptr(), d.data_ptr(), n, sp), "append")
+        for _ in range(3):
+            append()
+        ms = []
+        for k in range(max(reps, (C // n) // 4)):
+            flush_l2(k)
+            s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s_.record(stream)
+            append()
+            e_.record(stream)
+            e_.synchronize()
+            ms.append(s_.elapsed_time(e_))
+        t = statistics.median(ms) / 1e3
+        gbs = 2 * row_bytes * n / t / 1e9
+        res["append"].append({"rows_per_call": n, "us": t * 1e6, "rows_per_s": n / t,
+                              "achieved_gbs": gbs, "peak_gbs": peak_gbs, "frac": gbs / peak_gbs})
+    B = 256
+    out = [torch.empty((B, D), device=dev), torch.empty(B, dtype=torch.int64, device=dev),
+           torch.empty(B, device=dev), torch.empty((B, D), device=dev),
+           torch.empty(B, dtype=torch.bool, device=dev)]
+    idx = torch.empty(B, dtype=torch.int64, device=dev)
+    ms = []
+    for k in range(reps + 3):
+        flush_l2(k)
+        s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_.record(stream)
+        _lib.check(lib.sp_rb_sample(rb._h, B, SEED, 3, k * B, *(t.data_ptr() for t in out),
+                                    idx.data_ptr(), sp), "sample")
+        e_.record(stream)
+        e_.synchronize()
+        ms.append(s_.elapsed_time(e_))
+    ms = ms[3:]
+    res["sample"] = {"batch": B, "us_median": statistics.median(ms) * 1e3,
+                     "us_min": min(ms) * 1e3, "ring_rows": len(rb),
+                     "note": "latency-bound (one launch); L2 flushed before each"}
+    del rb
+    return res
+
+
+def d2h_probe(dev, nbytes, reps=5):
+    """Effective pinned D2H bandwidth of this box (GB/s): the e2e step's
+    transfer in isolation."""
+    import torch
+    src = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    dst = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    stream = torch.cuda.current_stream(dev)
+    ms = []
+    for _ in range(reps):
+        s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_.record(stream)
+        dst.copy_(src, non_blocking=True)
+        e_.record(stream)
+        e_.synchronize()
+        ms.append(s_.elapsed_time(e_))
+    return nbytes / (statistics.median(ms) / 1e3) / 1e9
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     from paper_2305_04180_b200 import VecEnv, _lib
+    from paper_2305_04180_b200.raycells import dda_cells
     from paper_2305_04180_b200.sim import DiversityRanges, SimParams
     from paper_2305_04180_b200.vecenv import StepBatch
 
+    numa = numa_bind(local_rank)
+    prev_affinity = numa.pop("_prev", None)
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     n = args.envs
     offset = rank * n
     env = VecEnv(load_maps(), n, DiversityRanges.around(SimParams(), DIVERSITY), env_config(),
@@ -226,16 +432,19 @@ def run_ours(args, rank, world, local_rank):
     D = env.state_dim
     K, W = args.steps, args.warmup
     total_steps = W + K
-    acts = torch.empty((total_steps, n), dtype=torch.int64, device=dev)
-    for t in range(total_steps):
+    acts = torch.empty((total_steps + 1, n), dtype=torch.int64, device=dev)
+    for t in range(total_steps + 1):
         _lib.check(lib.sp_random_actions(n, SEED, offset, t, 5, acts[t].data_ptr(),
                                          stream.cuda_stream))
-    out = StepBatch(torch.empty((n, D), dtype=torch.float32, device=dev),
-                    torch.empty(n, dtype=torch.float64, device=dev),
-                    torch.empty(n, dtype=torch.bool, device=dev),
-                    torch.empty(n, dtype=torch.bool, device=dev),
-                    torch.empty((n, D), dtype=torch.float32, device=dev),
-                    torch.empty(n, dtype=torch.int8, device=dev))
+
+    def batch(m):
+        return StepBatch(torch.empty((m, D), dtype=torch.float32, device=dev),
+                         torch.empty(m, dtype=torch.float64, device=dev),
+                         torch.empty(m, dtype=torch.bool, device=dev),
+                         torch.empty(m, dtype=torch.bool, device=dev),
+                         torch.empty((m, D), dtype=torch.float32, device=dev),
+                         torch.empty(m, dtype=torch.int8, device=dev))
+    out = batch(n)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     clean = torch.zeros(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB, read-only
 
@@ -276,6 +485,25 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     t_dev_max = float(t_max.item())
     value = world * n * K / t_dev_max
+    clk = clocks.summary()
+    mhz = float(clk.get("sm_mhz") or MAX_MHZ)
+
+    # ray-cells of a step, counted in this run: one more (untimed) step with
+    # the kernel's recording on -> per-ray hit cells of the scans behind the
+    # states rows -> pure-DDA cells per ray (raycells.dda_cells).  That is N
+    # scans per step; the ~0.9 % extra fresh-spawn scans of resetting envs are
+    # not credited, so the count is a lower bound.
+    env.record()
+    env.step_device(acts[total_steps].data_ptr(), out)
+    rec = env.recorded()
+    sim = env.sim
+    xs, ys, hs = (torch.from_numpy(v).to(dev) for v in (sim.x, sim.y, sim.heading))
+    cells_per_ray = float(dda_cells(xs, ys, hs, env._offsets, rec["hit_state"],
+                                    env._maps[0].occupancy.shape[1],
+                                    float(env._maps[0].cell_size_cm),
+                                    float(env.config.lidar.max_range_cm)).double().mean())
+    env.record(False)
+    ray_cells_per_launch = n * N_BEAMS * cells_per_ray
 
     # cfg2 (BASELINE configs[1]: 4096 envs on one GPU) on the same protocol,
     # reported beside the headline (which is cfg3, the per-GPU scaling config)
@@ -285,12 +513,7 @@ def run_ours(args, rank, world, local_rank):
         env2 = VecEnv(load_maps(), n2, DiversityRanges.around(SimParams(), DIVERSITY), env_config(),
                       device=dev, check_actions=False)
         env2.reset_all(SEED)
-        out2 = StepBatch(torch.empty((n2, D), dtype=torch.float32, device=dev),
-                         torch.empty(n2, dtype=torch.float64, device=dev),
-                         torch.empty(n2, dtype=torch.bool, device=dev),
-                         torch.empty(n2, dtype=torch.bool, device=dev),
-                         torch.empty((n2, D), dtype=torch.float32, device=dev),
-                         torch.empty(n2, dtype=torch.int8, device=dev))
+        out2 = batch(n2)
         for t in range(W):  # lanes 0..4095 of the same Philox actions (keyed by env id)
             env2.step_device(acts[t].data_ptr(), out2)
         s2 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
@@ -339,6 +562,7 @@ def run_ours(args, rank, world, local_rank):
     e2e_value = world * n * Ke / float(et.item())
     h2d = n * 8
     d2h = sum(t.numel() * t.element_size() for t in out)
+    d2h_gbs = d2h_probe(dev, d2h)
 
     result = None
     if rank == 0:
@@ -346,8 +570,11 @@ def run_ours(args, rank, world, local_rank):
         mean_launch = t_dev / K
         achieved = BYTES_PER_ENV_STEP * n / mean_launch / 1e9
         info = env.launch_info()
-        nm = ncu_metrics() if n == N_PER_GPU else {}
-        traffic, traffic_src = nm.get("traffic_bytes_per_launch"), nm.get("source")
+        nm = ncu_metrics() if n == N_PER_GPU else {"stale": "capture is of the 65,536-env step"}
+        smem_ach = 4.0 * ray_cells_per_launch / mean_launch / 1e9
+        smem_peak = smem_peak_gbs(n_sm, mhz)
+        lidar = None if args.no_lidar else lidar_sweep(dev, flush_l2, n_sm, mhz)
+        replay = None if args.no_replay else replay_bench(dev, flush_l2, peak)
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": t_dev_max / K * 1e3, "higher_is_better": True,
@@ -362,29 +589,49 @@ def run_ours(args, rank, world, local_rank):
                        "launch": info},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": Ke,
+                    "ms_per_step_mean": e2e_t / Ke * 1e3,
                     "per_step_ms": {"min": min(e2e_ms), "median": statistics.median(e2e_ms),
                                     "max": max(e2e_ms)},
+                    "d2h_probe_gbs": d2h_gbs,
+                    "pcie_share": (d2h / d2h_gbs / 1e9) / (e2e_t / Ke),
+                    "numa": numa,
                     "path": "VecEnv.step_host: pinned host actions in, every StepBatch field out as numpy"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "traffic_unit": "bytes per launch (dram read+write)",
-                         "traffic_source": traffic_src,
-                         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                         "algorithmic_bytes_per_env_step": BYTES_PER_ENV_STEP,
-                         "kernel": "env_step_kernel", "mean_launch_ms": mean_launch * 1e3,
-                         "note": "issue/latency-bound (fp64 LiDAR march); see DESIGN.md 4"},
+            "roofline": {"bound": "smem", "achieved": smem_ach, "peak": smem_peak, "unit": "GB/s",
+                         "frac": smem_ach / smem_peak,
+                         "traffic": nm.get("traffic_bytes_per_launch"),
+                         "traffic_unit": "DRAM bytes per launch (read+write), ncu --set full",
+                         "traffic_source": nm.get("source") or nm.get("stale"),
+                         "ray_cells_per_s": ray_cells_per_launch / mean_launch,
+                         "ray_cells_per_launch": ray_cells_per_launch,
+                         "dda_cells_per_ray": cells_per_ray,
+                         "peak_ray_cells_per_s": smem_peak / 4 * 1e9,
+                         "peak_basis": f"{n_sm} SMs x 128 B/clk x {mhz:.0f} MHz (median SM clock "
+                                       "sampled in the timed region); one 4 B SMEM word per "
+                                       "pure-DDA ray-cell (SURVEY 8(d))",
+                         "achieved_basis": "ray-cells per launch (N scans x R rays x pure-DDA "
+                                           "cells per ray, counted from a recorded step in this "
+                                           "run; reset scans not credited) x 4 B / mean launch",
+                         "kernel": "env_step_kernel", "mean_launch_ms": mean_launch * 1e3},
+            "roofline_hbm": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": achieved / peak,
+                             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                             "algorithmic_bytes_per_env_step": BYTES_PER_ENV_STEP},
             "compute_roofline": {"bound": "issue", "unit": "% of issue slots (4/clk/SM)",
                                  "achieved": nm.get("issue_active_pct"),
                                  "simt_threads_per_inst": nm.get("simt_threads_per_inst"),
-                                 "source": nm.get("source")},
-            "clocks": clocks.summary(),
+                                 "source": nm.get("source") or nm.get("stale")},
+            "clocks": clk,
             "gpu_launches": K,
             "per_step_ms": {"min": min(per_step), "median": statistics.median(per_step),
-                            "max": max(per_step)},
+                            "max": max(per_step), "mean": t_dev / K * 1e3},
             "wall_s_timed_region": wall,
             "pooled_stats": pooled, "stats_allreduce_ms": t_allreduce_ms,
             "configs": {"cfg2": cfg2},
+            "lidar": lidar,
+            "replay": replay,
         }
+    if prev_affinity:
+        os.sched_setaffinity(0, prev_affinity)  # the CPU baseline uses every host core
     return result
 
 
@@ -411,6 +658,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=4.0)
+    ap.add_argument("--no-lidar", action="store_true", help="skip the cfg4 marcher sweep")
+    ap.add_argument("--no-replay", action="store_true", help="skip the cfg5 replay section")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -42,6 +42,20 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in deps if os.path.exists(p))
 
 
+def source_hash() -> str:
+    """sha256 over the CUDA/C sources the library is built from (csrc/ and
+    include/sparrow.h): stamps measurements copied from a profiler capture
+    (profiles/ncu_step_traffic.json) so a stale one is detected."""
+    import hashlib
+    h = hashlib.sha256()
+    for name in SOURCES:
+        with open(os.path.join(CSRC, name), "rb") as f:
+            h.update(name.encode() + b"\0" + f.read())
+    with open(os.path.join(HERE, "..", "include", "sparrow.h"), "rb") as f:
+        h.update(f.read())
+    return h.hexdigest()[:16]
+
+
 def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()) -> str:
     """Compile libsparrow.so; `defines` (e.g. ["SP_CTAS_PER_SM=1"]) build
     experimental variants to another `out` path."""

@@ -218,10 +218,11 @@ static std::vector<int64_t> cta_ranges(const std::vector<int64_t>& off, int G) {
 // shared-memory bytes of a chunk with `cap` envs (layout of chunk_smem)
 static int extra_slots(int cap) { return std::max(32, cap / 8); }
 static size_t chunk_bytes(int cap, int D, int R) {
+  // layout of chunk_smem: 109 B per scan slot, 30 B per env, control words
   const size_t slots = (size_t)cap + extra_slots(cap);
   (void)R;
   (void)D;
-  return slots * 90 + 30 * (size_t)cap + 96;
+  return slots * 109 + 30 * (size_t)cap + 96 + 16;
 }
 
 static Plan plan_launch(SpEnv* env, const std::vector<int64_t>& off, bool staging = true) {
@@ -239,7 +240,11 @@ static Plan plan_launch(SpEnv* env, const std::vector<int64_t>& off, bool stagin
   // 1 KB per CTA reserved by the driver)
   const size_t sm_total = (size_t)env->smem_per_sm;
   const size_t budget = std::min((size_t)env->smem_optin,
-                                 sm_total / SP_CTAS_PER_SM) - 1024;
+                                 sm_total / SP_CTAS_PER_SM) - 1024
+#ifdef SP_TIMING
+                        - 512  // the stamps' static shared memory
+#endif
+      ;
   size_t map_bytes = align_up(d.map_bytes, 128);
   p.threads = max_threads;
   if (map_bytes + fixed + chunk_bytes(128, D, d.R) + 128 > budget) {
@@ -380,6 +385,8 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   d.bits_bytes = (uint32_t)align_up((size_t)H * d.WW * 4, 16);
   d.map_bytes = d.blk_bytes + d.bits_bytes;
   d.env_id_offset = env_id_offset;
+  d.row_affine = map_index ? 0 : 1;  // default assignment: rows follow from slots
+  d.off_mod = (int32_t)(((env_id_offset % n_maps) + n_maps) % n_maps);
 
   // slot order: stable sort by map (map-major)
   std::vector<int32_t> midx(n_envs);
@@ -446,11 +453,7 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   TRY(env->alloc(&d.step, n));
   TRY(env->alloc(&d.delay, n));
   TRY(env->alloc(&d.needs_reset, n, 1));
-  TRY(env->alloc(&d.qmax, n));
-  {  // no history yet: scans without history sort longest
-    std::vector<uint32_t> q(n, 255u);
-    cudaMemcpy(d.qmax, q.data(), 4 * n, cudaMemcpyHostToDevice);
-  }
+  TRY(env->alloc(&d.qhist, n, 0x80));  // no history yet: every group ranks longest
   TRY(env->alloc(&d.episodes, n));
   TRY(env->alloc(&d.arrivals, n));
   TRY(env->alloc(&d.first_event, n, 0xff));
@@ -483,8 +486,12 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
 
   {
     const int R = env->R;
-    d.r_shift = (R & (R - 1)) == 0 ? __builtin_ctz((unsigned)R) : -1;
-    d.r_magic = (d.r_shift < 0 && R < 512) ? (((uint64_t)1 << 40) + R - 1) / R : 0;
+    int gs = 0;  // beams per dispatch group: the power of two >= R / 8
+    while ((8 << gs) < R) ++gs;
+    if (const char* g = std::getenv("SPARROW_GSHIFT"))  // experiments: larger groups
+      gs = std::max(gs, std::min(10, std::atoi(g)));
+    d.gshift = gs;
+    d.n_groups = (R + (1 << gs) - 1) >> gs;
     d.d_magic = (((uint64_t)1 << 40) + (uint64_t)env->D - 1) / (uint64_t)env->D;
     d.nb = (R + 3) / 4;
     d.nb_shift = (d.nb & (d.nb - 1)) == 0 ? __builtin_ctz((unsigned)d.nb) : -1;
@@ -502,6 +509,19 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
     cudaMemcpy(dcta, plan.cta_begin.data(), 8 * plan.cta_begin.size(), cudaMemcpyHostToDevice);
   }
   d.cta_begin = dcta;
+  d.plan_n = 0;
+  if (plan.grid <= SP_PLAN_MAX && n_envs < (int64_t)1 << 31) {  // the plan rides in the params
+    d.plan_n = plan.grid;
+    for (int b = 0; b <= plan.grid; ++b) d.plan_begin[b] = (int32_t)plan.cta_begin[b];
+    for (int b = 0; b < plan.grid; ++b) {
+      int m = 0;
+      while (env->map_off[m + 1] <= plan.cta_begin[b] && m + 1 < n_maps) ++m;
+      d.plan_map[b] = (int16_t)m;
+      d.plan_mstart[b] = (int32_t)env->map_off[m];
+      d.plan_mend[b] = (int32_t)env->map_off[m + 1];
+    }
+    if (n_maps > 32767) d.plan_n = 0;
+  }
   env->grid = plan.grid;
   env->threads = plan.threads;
   env->smem = plan.smem;
@@ -512,8 +532,10 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
                             (const void*)env_scan_kernel<true>, (const void*)env_scan_kernel<false>};
   cudaError_t e1 = cudaSuccess, e2 = cudaSuccess;
   for (const void* k : kernels_) {
+    cudaFuncAttributes fa;  // static shared memory (debug stamp builds) counts against the opt-in
+    const size_t stat = cudaFuncGetAttributes(&fa, k) == cudaSuccess ? fa.sharedSizeBytes : 0;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         env->smem_optin);
+                                         env->smem_optin - (int)stat);
     if (e != cudaSuccess) e1 = e;
   }
   cudaError_t e3 = cudaDeviceSynchronize();
@@ -1002,15 +1024,31 @@ int sp_rb_append(SpReplay* rb, const float* states, const int64_t* actions, cons
   if (!states || !actions || !rewards || !next_states || !dones) return fail(SP_EINVAL, "null argument");
   DevDeviceGuard guard(rb->device);
   std::lock_guard<std::mutex> lk(rb->mu);
-  const int64_t vecs = (2 * n * rb->dim + 3) / 4;  // float4 chunks of s and s2
   const int64_t new_size = std::min(rb->size + n, rb->cap);
-  // ~4 vectors per thread (the loop keeps four loads in flight), at least
-  // one thread per row for the small columns, at most 8 CTAs per SM
-  const int64_t thr = std::max<int64_t>(n, (vecs + 3) / 4);
+  const int64_t D = rb->dim, n1 = std::min(n, rb->cap - rb->cursor);
+  AppendSeg g{};
+  auto add = [&](float* dst, const float* src, int64_t count) {
+    if (count <= 0) return;
+    const int k = g.nseg++;
+    const int64_t head = std::min<int64_t>(count, ((16 - ((uintptr_t)dst & 15)) & 15) / 4);
+    g.dst[k] = dst;
+    g.src[k] = src;
+    g.head[k] = head;
+    g.nvec[k] = (count - head) / 4;
+    g.count[k] = count;
+    g.vend[k] = (k ? g.vend[k - 1] : 0) + g.nvec[k];
+  };
+  add(rb->s + rb->cursor * D, states, n1 * D);
+  add(rb->s2 + rb->cursor * D, next_states, n1 * D);
+  add(rb->s, states + n1 * D, (n - n1) * D);
+  add(rb->s2, next_states + n1 * D, (n - n1) * D);
+  // kAppendU vectors (and rows) per thread in one pass, <= 8 CTAs per SM
+  const int64_t items = std::max<int64_t>(g.vend[g.nseg - 1], n);
+  const int64_t thr = std::max<int64_t>(1, (items + kAppendU - 1) / kAppendU);
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((thr + 255) / 256, 148 * 8));
   rb_append_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
-      rb->s, rb->a, rb->r, rb->s2, rb->dn, rb->cap, rb->dim, rb->cursor, states, actions, rewards,
-      reward_is_f64, next_states, dones, n, rb->d_size, new_size);
+      g, rb->a, rb->r, rb->dn, rb->cap, rb->cursor, actions, rewards, reward_is_f64, dones, n,
+      rb->d_size, new_size);
   SP_CUDA(cudaGetLastError());
   rb->cursor = (rb->cursor + n) % rb->cap;  // replay.py:66-67
   rb->size = new_size;
@@ -1243,7 +1281,7 @@ int sp_ddqn_update(const SpMlp* on, const SpMlp* tg, const float* s, const int64
 // debug builds only (not part of include/sparrow.h): per-CTA phase stamps
 int sp_debug_read_ts(unsigned long long* out, int n_ctas) {
   SP_CUDA(cudaDeviceSynchronize());
-  SP_CUDA(cudaMemcpyFromSymbol(out, g_sp_ts, sizeof(unsigned long long) * 12 * (size_t)n_ctas));
+  SP_CUDA(cudaMemcpyFromSymbol(out, g_sp_ts, sizeof(unsigned long long) * 48 * (size_t)n_ctas));
   return SP_OK;
 }
 #endif

@@ -62,6 +62,14 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+// 8-byte global -> shared copy that never occupies a register (cp.async)
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -131,15 +139,22 @@ __device__ __forceinline__ bool disc_hits(const MapView& mv, const EnvDev& d, do
 
 // ---------------------------------------------- debug phase timestamps ---
 // Built only with -DSP_TIMING (tools/debug): thread 0 of each CTA stamps
-// %clock64 (SM cycles) at phase boundaries of the first chunk.
+// %clock64 (SM cycles) at phase boundaries of the last chunk into shared
+// memory (a global store could stall behind the CTA's queued row stores and
+// skew the stamps), copied out at the kernel's end.
 #ifdef SP_TIMING
-__device__ unsigned long long g_sp_ts[1024][12];
+__device__ unsigned long long g_sp_ts[1024][48];
+__shared__ unsigned long long s_sp_ts[48];  // [12 + w]: warp w arrives at the end of phase A
 __device__ __forceinline__ void sp_stamp(int k) {
-  if (threadIdx.x == 0 && blockIdx.x < 1024) {
+  if (threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
-    g_sp_ts[blockIdx.x][k] = t;
+    s_sp_ts[k] = t;
   }
+}
+__device__ __forceinline__ void sp_stamp_flush() {
+  __syncthreads();
+  if (threadIdx.x < 48 && blockIdx.x < 1024) g_sp_ts[blockIdx.x][threadIdx.x] = s_sp_ts[threadIdx.x];
 }
 #define SP_STAMP(k) sp_stamp(k)
 #else
@@ -147,12 +162,18 @@ __device__ __forceinline__ void sp_stamp(int k) {
 #endif
 
 // ---------------------------------------------------------------- rays ---
-// Ray state in cell units: origin (x0, y0)/cell, direction (dx, dy)/cell and
-// cell/dx, cell/dy (so t = (face - x0) * idx comes out in cm), the step
-// signs and the current cell.
+// Ray state, mirrored so that every ray moves toward +u, +v: on an axis the
+// ray travels in the negative direction, coordinates are negated (exactly)
+// and cell indices become u = -ix - 1, so cell u covers [u, u + 1).  In cell
+// units: origin (X, Y), |direction| / cell (DX, DY) and cell / |direction|
+// (IDX, IDY), so t = (face - X) * IDX is the reference's parameter in cm --
+// bit for bit the unmirrored ((double)face - x0) * idx, since negation is
+// exact.  The table address of cell (u, v) is v * ayw + u * ax + kb, with
+// (ax, bx) = (1, 0) or (-1, -1) per axis (ix = ax * u + bx), ayw = ay * W
+// and kb = by * W + bx.
 struct Ray {
-  double x0, y0, dx, dy, idx, idy, t;
-  int ix, iy, sx, sy, n;  // n: march steps taken (scheduling history)
+  double X, Y, DX, DY, IDX, IDY;
+  int u, v, ax, ayw, kb, n;  // n: march steps taken (scheduling history)
 };
 
 // 1/v to within an ulp: fp32 seed + two fp64 Newton steps (no DDIV).
@@ -168,12 +189,12 @@ __device__ __forceinline__ double recip(double v) {
 }
 
 // Exact int <-> double conversions on the fp64 pipe instead of the slower
-// conversion unit: |v| < 2^31 sits in the low mantissa word of v + 2^52.
+// conversion unit: |v| < 2^31 sits in the low mantissa word of v + 1.5 * 2^52.
 __device__ __forceinline__ double i2d(int n) {  // n >= 0
   return __hiloint2double(0x43300000, n) - 4503599627370496.0;
 }
 __device__ __forceinline__ int floor_i(double v) {  // floor(v), |v| < 2^31
-  return __double2loint(__dadd_rd(v, 4503599627370496.0));
+  return __double2loint(__dadd_rd(v, 6755399441055744.0));
 }
 
 // One march step, branch-free: every lane of the warp executes it.  A
@@ -185,40 +206,32 @@ __device__ __forceinline__ int floor_i(double v) {  // floor(v), |v| < 2^31
 // (_cy.pyx:89-96), larger r lets the ray leave the whole box.  Either way it
 // exits through the face with the smaller parameter (ties to x, as tmx <= tmy
 // does) into the cell containing the exit point.  Returns true when the ray
-// has finished (idempotent once it has).  r.t then holds the
-// exit parameter of its last free cell: the range once clipped to max_range
-// (ray_range), and ray_hit() recovers the occupied cell it stopped in.
-// Every map has an occupied border (GridMap's invariant, checked by
-// sp_env_create), so no step can leave the grid and there are no bounds tests.
+// has finished (idempotent once it has): ray_end() then recovers the range
+// and the occupied cell it stopped in.  Every map has an occupied border
+// (GridMap's invariant, checked by sp_env_create), so no step can leave the
+// grid and there are no bounds tests.
 __device__ __forceinline__ bool ray_step(Ray& r, const MapView& mv, const EnvDev& d) {
-  const int code = mv.scode(r.ix, r.iy);  // < 0: occupied, else the box radius
-  const bool occupied = code < 0;
-  // the far cell of the free box on each axis is ix + sx * r (r = 0: the cell
-  // itself, a plain DDA step), written as a face index below
-  const int fx = max(r.sx, 0), fy = max(r.sy, 0);  // 1 when moving +
-  const int face_x = r.ix + fx + r.sx * code;
-  const int face_y = r.iy + fy + r.sy * code;
-  const double tx = ((double)face_x - r.x0) * r.idx;
-  const double ty = ((double)face_y - r.y0) * r.idy;
-  const bool xs = tx <= ty;
-  const double t = xs ? tx : ty;
+  const int code = (int)((const int8_t*)mv.blk)[r.v * r.ayw + r.u * r.ax + r.kb];
+  const bool occupied = code < 0;  // else the box radius
+  // the free box's far faces: u + 1 + r (r = 0: this cell's own face)
+  const int fu = r.u + 1 + code;
+  const int fv = r.v + 1 + code;
+  const double tu = ((double)fu - r.X) * r.IDX;
+  const double tv = ((double)fv - r.Y) * r.IDY;
+  const bool xs = tu <= tv;  // ties exit through x, as tmx <= tmy (_cy.pyx:89)
+  const double t = xs ? tu : tv;
   // the cell on the other axis at the exit point, clamped between the current
-  // cell and the region's far cell (the ray moves monotonically)
-  const int c = floor_i(fma(t, xs ? r.dy : r.dx, xs ? r.y0 : r.x0));
-  const int lo = xs ? r.iy : r.ix;
-  const int hi = xs ? face_y - fy : face_x - fx;
-  const int cc = min(max(c, min(lo, hi)), max(lo, hi));
-  const int nx = xs ? face_x - fx + r.sx : cc;  // far cell + sx
-  const int ny = xs ? cc : face_y - fy + r.sy;
+  // cell and the box's far cell (the ray moves monotonically)
+  const int c = floor_i(fma(t, xs ? r.DY : r.DX, xs ? r.Y : r.X));
+  const int lo = xs ? r.v : r.u;
+  const int hi = (xs ? fv : fu) - 1;
+  const int cc = min(max(c, lo), hi);
   const bool over = t > d.max_range;  // :97-99
   const bool finished = occupied || over;
-  if (!occupied) {
-    r.t = t;
-    if (!finished) {
-      r.ix = nx;
-      r.iy = ny;
-      r.n += 1;
-    }
+  if (!finished) {
+    r.u = xs ? fu : cc;
+    r.v = xs ? cc : fv;
+    r.n += 1;
   }
   return finished;
 }
@@ -226,27 +239,30 @@ __device__ __forceinline__ bool ray_step(Ray& r, const MapView& mv, const EnvDev
 // A parked ray: a finished fixed point for the lanes of a ray slot with no
 // ray (cell (0, 0) is a border cell, occupied).
 __device__ __forceinline__ void ray_park(Ray& r) {
-  r.ix = r.iy = 0;
-  r.sx = r.sy = 1;
+  r.u = r.v = 0;
+  r.ax = 1;
+  r.ayw = 0;
+  r.kb = 0;
   r.n = 0;
-  r.x0 = r.y0 = 0.5;
-  r.dx = r.dy = 1.0;
-  r.idx = r.idy = 1.0;
-  r.t = 0.0;
+  r.X = r.Y = 0.5;
+  r.DX = r.DY = 1.0;
+  r.IDX = r.IDY = 1.0;
 }
 
-// range of a finished ray (the over-range exit clips to max_range)
-__device__ __forceinline__ double ray_range(const Ray& r, const EnvDev& d) {
-  return r.t > d.max_range ? d.max_range : r.t;
-}
-
-// occupied cell a finished ray stopped in, or -1 (range / grid exit, origin
-// outside the grid): a ray that hits stays in the occupied cell.
-__device__ __forceinline__ int ray_hit(const Ray& r, const MapView& mv, const EnvDev& d) {
-  if ((unsigned)r.ix >= (unsigned)d.W || (unsigned)r.iy >= (unsigned)d.H) return -1;
-  const uint32_t code = mv.code(r.ix, r.iy);
-  const bool occ = code >= 0x80u;
-  return occ ? r.iy * d.W + r.ix : -1;
+// Range and hit cell of a finished ray.  It stopped either in an occupied
+// cell -- then its range is the parameter at which it entered that cell: the
+// later of the cell's two entry faces u, v (the march's last exit parameter,
+// bit for bit; 0 when the origin cell itself is occupied) -- or past
+// max_range (range max_range, no hit cell).
+__device__ __forceinline__ double ray_end(const Ray& r, const MapView& mv, const EnvDev& d,
+                                          int& hit) {
+  const int ix = r.ax * r.u + (r.ax < 0 ? -1 : 0);
+  const int iy = r.ayw < 0 ? -r.v - 1 : r.v;
+  const bool occ = ((const int8_t*)mv.blk)[r.v * r.ayw + r.u * r.ax + r.kb] < 0;
+  hit = occ ? iy * d.W + ix : -1;
+  if (!occ) return d.max_range;
+  const double te = fmax(((double)r.u - r.X) * r.IDX, ((double)r.v - r.Y) * r.IDY);
+  return te > 0.0 ? te : 0.0;
 }
 
 // Returns true if finished during setup (origin outside the grid -> 0).
@@ -254,48 +270,53 @@ __device__ __forceinline__ bool ray_setup(Ray& r, double x0, double y0, double c
                                           double2 cs, const EnvDev& d) {
   const double dx = ch * cs.x - sh * cs.y;  // cos(h + o_j)
   const double dy = sh * cs.x + ch * cs.y;  // sin(h + o_j)
-  r.x0 = x0 * d.inv_cell;
-  r.y0 = y0 * d.inv_cell;
-  r.dx = dx * d.inv_cell;
-  r.dy = dy * d.inv_cell;
-  r.idx = recip(dx) * d.cell;
-  r.idy = recip(dy) * d.cell;
-  r.sx = dx >= 0.0 ? 1 : -1;  // dx == 0: idx = +inf, the x face is never taken
-  r.sy = dy >= 0.0 ? 1 : -1;
-  r.t = 0.0;
+  const double xc = x0 * d.inv_cell, yc = y0 * d.inv_cell;
+  const int ix = (int)floor(xc), iy = (int)floor(yc);
+  const bool px = dx >= 0.0, py = dy >= 0.0;  // dx == 0: IDX = +inf, x faces never taken
+  r.X = px ? xc : -xc;
+  r.Y = py ? yc : -yc;
+  r.DX = fabs(dx * d.inv_cell);
+  r.DY = fabs(dy * d.inv_cell);
+  r.IDX = fabs(recip(dx) * d.cell);
+  r.IDY = fabs(recip(dy) * d.cell);
+  r.u = px ? ix : -ix - 1;
+  r.v = py ? iy : -iy - 1;
+  r.ax = px ? 1 : -1;
+  r.ayw = py ? d.Wb : -d.Wb;
+  r.kb = (py ? 0 : -d.Wb) + (px ? 0 : -1);
   r.n = 0;
-  r.ix = (int)floor(r.x0);
-  r.iy = (int)floor(r.y0);
-  return (unsigned)r.ix >= (unsigned)d.W || (unsigned)r.iy >= (unsigned)d.H;  // :37-39
+  return (unsigned)ix >= (unsigned)d.W || (unsigned)iy >= (unsigned)d.H;  // :37-39
 }
 
 // Per-CTA chunk scratch (shared memory).  A chunk holds up to `cap` envs;
 // its scans use "slots": slot e (< cap) is env e's post-step scan, slots
 // cap .. cap+extra-1 are post-reset scans of envs that finished this step.
+// A scan's R beams form up to 8 "beam groups" of gb = 2^gshift consecutive
+// beams (EnvDev::gshift); the ray queue dispatches (slot, group) entries.
 struct Chunk {
   double *px, *py, *ch, *sh, *sig;  // per slot: scan origin, heading cos/sin, noise std
   uint64_t* nctr;  // per slot: first Philox block of the slot's LiDAR noise
+  uint64_t* qacc;  // per slot: byte g = OR of 1 << step_level(steps) over group g's rays
+  uint64_t* qpred; // per slot: the same bytes from the lane's last scan (prediction)
   double* retp;    // per env: episode return before this step (prefetched in phase A)
   double* part;    // per env: shaped reward without its proximity term
-  int32_t* rowi;   // per env: caller row
-  int32_t* send;   // per env: episode length before any reset
-  int8_t* evs;     // per env: event awaiting phase C, or -1 (nothing left to do)
-  uint32_t* gid;   // per slot: the env's stream lane (global env id)
-  int32_t* list;   // slots in dispatch order (longest predicted scan first)
-  int32_t* reg;    // slots in registration order
-  int32_t* hwrite; // per slot: global slot whose history this scan refreshes, or -1
-  uint32_t* qacc;  // per slot: march steps its longest ray took (shared atomicMax)
-  int32_t* xslot;  // per env: post-reset slot, -1 if none
-  uint8_t* wmode;  // per env: which rows to write (see kernel)
-  uint8_t* prox;   // per slot: some ray ended closer than the proximity range
-  uint8_t* sbucket;  // per slot: predicted work bucket (0 = longest)
-  int* ctl;        // [0] ray-queue head [1] slots listed [2] extra slots used [3] overflow
-                   // [4..11] bucket counts, [12..19] bucket offsets
   float** out0;    // per slot: the output row its scan fills (noise z parks there first)
   float** out1;    // per slot: a second row that receives the same values, or null
+  uint32_t* gid;   // per slot: the env's stream lane (global env id)
+  int32_t* reg;    // slots in registration order
+  int32_t* hwrite; // per slot: global slot whose history this scan refreshes, or -1
+  int32_t* xslot;  // per env: post-reset slot, -1 if none
+  int* ctl;        // [0] ray-queue head [1] slots listed [2] extra slots used [3] overflow
+                   // [4..11] bucket counts, [12..19] bucket offsets, [20] entries listed
+  int32_t* rowi;   // per env: caller row
+  int32_t* send;   // per env: episode length before any reset
+  uint16_t* list;  // (slot << 3 | group) entries in dispatch order (longest predicted first)
+  uint8_t* wmode;  // per env: which rows to write (see kernel)
+  int8_t* evs;     // per env: event awaiting phase C, or -1 (nothing left to do)
+  uint8_t* prox;   // per slot: some ray ended closer than the proximity range
 };
 
-__device__ __forceinline__ Chunk chunk_smem(uint8_t* base, int cap, int slots, int D, int R) {
+__device__ __forceinline__ Chunk chunk_smem(uint8_t* base, int cap, int slots) {
   Chunk c;
   c.px = (double*)base;
   c.py = c.px + slots;
@@ -303,36 +324,54 @@ __device__ __forceinline__ Chunk chunk_smem(uint8_t* base, int cap, int slots, i
   c.sh = c.ch + slots;
   c.sig = c.sh + slots;
   c.nctr = (uint64_t*)(c.sig + slots);
-  c.retp = (double*)(c.nctr + slots);
+  c.qacc = c.nctr + slots;
+  c.qpred = c.qacc + slots;
+  c.retp = (double*)(c.qpred + slots);
   c.part = c.retp + cap;
   c.out0 = (float**)(c.part + cap);
   c.out1 = c.out0 + slots;
   c.gid = (uint32_t*)(c.out1 + slots);
-  (void)D;
-  c.list = (int32_t*)(c.gid + slots);
-  c.reg = c.list + slots;
+  c.reg = (int32_t*)(c.gid + slots);
   c.hwrite = c.reg + slots;
-  c.qacc = (uint32_t*)(c.hwrite + slots);
-  c.xslot = (int32_t*)(c.qacc + slots);
+  c.xslot = c.hwrite + slots;
   c.ctl = c.xslot + cap;
-  c.rowi = c.ctl + 20;
+  c.rowi = c.ctl + 24;
   c.send = c.rowi + cap;
-  c.wmode = (uint8_t*)(c.send + cap);
+  c.list = (uint16_t*)(c.send + cap);
+  c.wmode = (uint8_t*)(c.list + 8 * slots);
   c.evs = (int8_t*)(c.wmode + cap);
   c.prox = (uint8_t*)(c.evs + cap);
-  c.sbucket = c.prox + slots;
-  (void)R;
   return c;
 }
 
-// q / R for 0 <= q < 2^31 (shift when R is a power of two, else magic number)
-__device__ __forceinline__ int div_r(int q, const EnvDev& d) {
-  if (d.r_shift >= 0) return q >> d.r_shift;
-  if (d.r_magic) return (int)(((uint64_t)(uint32_t)q * d.r_magic) >> 40);
-  return q / d.R;
+// March-step history level of a ray (steps incl. the finishing one), about
+// half an octave per level: <= 3, 4-5, 6-7, 8-11, 12-15, 16-23, 24-31, >= 32.
+__device__ __forceinline__ int step_level(int steps) {
+  const int s = steps > 2 ? steps : 2;
+  const int msb = 31 - __clz(s);
+  const int lv = 2 * msb + ((s >> (msb - 1)) & 1) - 3;
+  return lv < 0 ? 0 : (lv > 7 ? 7 : lv);
 }
 
-// CTA-wide ray queue over n_env slots (c.list) x R beams.  fin(slot, j, t, hit).
+// predicted bucket of a beam group (0 = longest): 7 - its highest level
+// (no history -> 0x80 -> bucket 0)
+__device__ __forceinline__ int group_bucket(uint64_t pred, int g) {
+  const uint32_t b = (uint32_t)(pred >> (8 * g)) & 0xffu;
+  return b ? __clz(b) - 24 : 0;
+}
+
+constexpr uint64_t kNoHistory = 0x8080808080808080ull;  // every group "longest"
+
+// queue index q -> (slot, beam) of its (slot, group) entry
+__device__ __forceinline__ int beam_of(const Chunk& c, int q, int gs, int& slot) {
+  const uint32_t e = c.list[q >> gs];
+  slot = (int)(e >> 3);
+  return (int)((e & 7u) << gs) + (q & ((1 << gs) - 1));
+}
+
+// CTA-wide ray queue over n_ent (slot, group) entries (c.list) x gb beams:
+// queue index q -> entry c.list[q >> gshift], beam (group << gshift) + (q & (gb - 1));
+// beams >= R (a partial last group) are skipped.  fin(slot, j, t, hit).
 // Every thread of the CTA must call it.  Each lane marches two independent
 // rays (slots A and B) so one ray's fp64 dependency chain hides behind the
 // other's.  A warp refills only when at least d.refill_min of its 64 ray
@@ -340,9 +379,10 @@ __device__ __forceinline__ int div_r(int q, const EnvDev& d) {
 // same branch, so per-ray setup/finish code runs at high SIMT occupancy.
 template <bool kHit, class Fin>
 __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, const Chunk& c,
-                                          const double2* beam, int n_env, const Fin& fin) {
+                                          const double2* beam, int n_ent, const Fin& fin) {
   const int R = d.R;
-  const int total = n_env * R;
+  const int gs = d.gshift;
+  const int total = n_ent << gs;
   const int lane = threadIdx.x & 31;
   const unsigned lt = lanemask_lt();
   // busy: the slot holds a ray not yet retired; fin: the slot's ray has
@@ -360,11 +400,15 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
     const int na = __popc(ia), n_idle = na + __popc(ib);
     if (n_idle >= d.refill_min || drained) {
       if (busy_a && fin_a) {  // steps taken = moves + the finishing step
-        fin(ea, ja, ray_range(ra, d), kHit ? ray_hit(ra, mv, d) : -1, ra.n + 1, za);
+        int hit;
+        const double t = ray_end(ra, mv, d, hit);
+        fin(ea, ja, t, kHit ? hit : -1, ra.n + 1, za);
         busy_a = false;
       }
       if (busy_b && fin_b) {
-        fin(eb, jb, ray_range(rb, d), kHit ? ray_hit(rb, mv, d) : -1, rb.n + 1, zb);
+        int hit;
+        const double t = ray_end(rb, mv, d, hit);
+        fin(eb, jb, t, kHit ? hit : -1, rb.n + 1, zb);
         busy_b = false;
       }
       if (drained) {
@@ -378,17 +422,14 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
           if (base < total && lane == 0 && blockIdx.x < 1024) {  // the queue just drained
             unsigned long long t;
             asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
-            g_sp_ts[blockIdx.x][10] = t;
+            s_sp_ts[10] = t;
           }
 #endif
           drained = true;
         }
         const int my_a = base + __popc(ia & lt);
         const int my_b = base + na + __popc(ib & lt);
-        if (fin_a && my_a < total) {
-          const int g = div_r(my_a, d);
-          ea = c.list[g];
-          ja = my_a - g * R;
+        if (fin_a && my_a < total && (ja = beam_of(c, my_a, gs, ea)) < R) {
           za = fin.pre(ea, ja);
           if (ray_setup(ra, c.px[ea], c.py[ea], c.ch[ea], c.sh[ea], beam[ja], d)) {
             fin(ea, ja, 0.0, -1, 1, za);  // origin outside the grid: range 0 (_cy.pyx:37-39)
@@ -398,10 +439,7 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
             fin_a = false;
           }
         }
-        if (fin_b && my_b < total) {
-          const int g = div_r(my_b, d);
-          eb = c.list[g];
-          jb = my_b - g * R;
+        if (fin_b && my_b < total && (jb = beam_of(c, my_b, gs, eb)) < R) {
           zb = fin.pre(eb, jb);
           if (ray_setup(rb, c.px[eb], c.py[eb], c.ch[eb], c.sh[eb], beam[jb], d)) {
             fin(eb, jb, 0.0, -1, 1, zb);
@@ -424,27 +462,23 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
   }
 }
 
-// Longest-first order (LPT) of the chunk's scans: a scan is ranked by the
-// march steps its env's longest beam took last step (the robot moves <= 1.8 cm
-// and turns <= 0.1 rad per step); the longest ray, not the mean, is what the
-// ray phase's tail waits for (-2 % step against ranking by the mean).
-// Unknown history (fresh spawns) counts as long.  Slots are counting-sorted
-// into 8 buckets and c.list is rewritten longest first; rays are then
-// dispatched slot-major, so the queue tail holds scans with only short rays.
+// Longest-first order (LPT) of the chunk's rays, per beam group: each
+// (scan, group) entry is ranked by the march-step level of the longest ray of
+// the same beam group in its lane's last scan (the robot moves <= 1.8 cm and
+// turns <= 0.1 rad per step, so a beam's step count mostly persists: 64 % of
+// rays repeat it exactly).  Fresh spawns have no history and rank longest.
+// Entries are counting-sorted into 8 buckets, longest first, so a warp's 64
+// ray slots hold rays of similar length (fewer lanes march finished rays
+// while their neighbours finish) and the queue tail holds short rays only.
+// tools/warp_sim.py models this against per-scan ranking (-16 % ray phase).
 
-// predicted bucket of a scan from its lane's longest ray last step
-__device__ __forceinline__ uint8_t scan_bucket(uint32_t m) {
-  return (uint8_t)(m >= 60 ? 0 : m >= 45 ? 1 : m >= 36 ? 2 : m >= 29 ? 3 : m >= 23 ? 4
-                 : m >= 18 ? 5 : m >= 13 ? 6 : 7);
-}
-
-// Refresh the lanes' step-count history from this chunk's scans (after a ray
+// Refresh the lanes' step-level history from this chunk's scans (after a ray
 // phase, before its slots are reused): the n_slots registered slots c.reg[].
 __device__ __forceinline__ void store_history(const EnvDev& d, const Chunk& c, int n_slots) {
   for (int k = threadIdx.x; k < n_slots; k += blockDim.x) {
     const int slot = c.reg[k];
     const int hw = c.hwrite[slot];
-    if (hw >= 0) d.qmax[hw] = c.qacc[slot];
+    if (hw >= 0) d.qhist[hw] = c.qacc[slot];
   }
 }
 
@@ -461,12 +495,26 @@ struct Grp {
 };
 __device__ __forceinline__ Grp cta_grp() { return Grp{(int)threadIdx.x, (int)blockDim.x, 0}; }
 
-__device__ __forceinline__ void order_slots(const Chunk& c, int n_slots, const Grp& g) {
+// Counting sort of the chunk's (slot, group) entries into c.list, longest
+// predicted first; c.ctl[20] = entries listed.  Warp-aggregated atomics: one
+// shared atomic per bucket present in a warp's 32 entries.
+__device__ __forceinline__ void order_entries(const EnvDev& d, const Chunk& c, int n_slots,
+                                              const Grp& g) {
   int* cnt = c.ctl + 4;
   int* off = c.ctl + 12;
+  const int G = d.n_groups;
+  const int space = n_slots * 8;
+  const int lane = g.tid & 31;
+  const unsigned lt = lanemask_lt();
   if (g.tid < 8) cnt[g.tid] = 0;
   g.sync();
-  for (int k = g.tid; k < n_slots; k += g.n) atomicAdd(&cnt[c.sbucket[c.reg[k]]], 1);
+  for (int base = g.tid - lane; base < space; base += g.n) {  // warp-uniform trips
+    const int k = base + lane;
+    int b = 8;  // no entry
+    if (k < space && (k & 7) < G) b = group_bucket(c.qpred[c.reg[k >> 3]], k & 7);
+    const unsigned peers = __match_any_sync(SP_FULL, b);
+    if (b < 8 && (peers & lt) == 0) atomicAdd(&cnt[b], __popc(peers));
+  }
   g.sync();
   if (g.tid == 0) {
     int acc = 0;
@@ -474,11 +522,23 @@ __device__ __forceinline__ void order_slots(const Chunk& c, int n_slots, const G
       off[b] = acc;
       acc += cnt[b];
     }
+    c.ctl[20] = acc;
   }
   g.sync();
-  for (int k = g.tid; k < n_slots; k += g.n) {
-    const int slot = c.reg[k];
-    c.list[atomicAdd(&off[c.sbucket[slot]], 1)] = slot;
+  for (int base = g.tid - lane; base < space; base += g.n) {
+    const int k = base + lane;
+    int b = 8;
+    int slot = 0;
+    if (k < space && (k & 7) < G) {
+      slot = c.reg[k >> 3];
+      b = group_bucket(c.qpred[slot], k & 7);
+    }
+    const unsigned peers = __match_any_sync(SP_FULL, b);
+    const int leader = __ffs(peers) - 1;
+    int pos = 0;
+    if (b < 8 && lane == leader) pos = atomicAdd(&off[b], __popc(peers));
+    pos = __shfl_sync(SP_FULL, pos, leader);
+    if (b < 8) c.list[pos + __popc(peers & lt)] = (uint16_t)((slot << 3) | (k & 7));
   }
   g.sync();  // c.list complete before anyone dispatches from it
 }
@@ -496,6 +556,9 @@ __device__ __forceinline__ void noise_block(const EnvDev& d, const Chunk& c, int
   float z[4];
   draw_normals4(blk, z);
   float* row = c.out0[slot] + 5 + 4 * b;
+#ifdef SP_EXP_NOZ  // experiment: no z stores (wrong noise), isolates their cost
+  if (z[0] == 12345.0f)
+#endif
 #pragma unroll
   for (int u = 0; u < 4; ++u)
     if (4 * b + u < d.R) row[u] = z[u];
@@ -523,7 +586,7 @@ __device__ __forceinline__ void noise_phase(const EnvDev& d, const Chunk& c, int
   for (int it = g.tid; it < items; it += g.n) {
     const int k = d.nb_shift >= 0 ? (it >> d.nb_shift) : it / nb;
     const int b = it - k * nb;
-    const int slot = c.list[k];
+    const int slot = c.reg[k];
     if (slot < pre) continue;
     noise_block(d, c, slot, b);
   }
@@ -567,8 +630,14 @@ __device__ __forceinline__ void header_row(const MapConst& mc, double x, double 
   h[2] = (float)div_by(alpha, SP_PI, SP_INV_PI);
   h[3] = (float)ddiv(vl, vml);
   h[4] = (float)ddiv(va, vma);
+#ifdef SP_EXP_NOHDR  // experiment: no header stores (wrong rows), isolates their cost
+  if (h[0] == 12345.0f)
+#endif
 #pragma unroll
   for (int k = 0; k < 5; ++k) row[k] = h[k];
+#ifdef SP_EXP_NOHDR
+  if (h[0] == 12345.0f)
+#endif
   if (row1) {
 #pragma unroll
     for (int k = 0; k < 5; ++k) row1[k] = h[k];
@@ -592,6 +661,7 @@ struct FinObs {
   uint64_t store_span;      // n * D floats
   uint32_t gid0;            // (uint32) env_id_offset: row = gid - gid0
   int R;
+  int gs;                   // log2 of the beams per group (step-level history)
   // z of beam j, parked in the output row by the noise pass: loaded when the
   // ray is dispatched so the L2 round trip overlaps its march
   __device__ __forceinline__ float pre(int slot, int j) const { return c.out0[slot][5 + j]; }
@@ -605,7 +675,8 @@ struct FinObs {
     float* r1 = c.out1[slot];
     if (r1) r1[5 + j] = o;
     if (t < proximity) c.prox[slot] = 1;
-    atomicMax(&c.qacc[slot], (uint32_t)steps);
+    const int grp = j >> gs;  // byte grp of the 64-bit word, as a 32-bit OR (native)
+    atomicOr((unsigned*)&c.qacc[slot] + (grp >> 2), 1u << (8 * (grp & 3) + step_level(steps)));
     if constexpr (kRec) {
       const int64_t k = (int64_t)(c.gid[slot] - gid0) * R + j;
       // post-step scans fill a store_states row (and the states row too when
@@ -651,9 +722,7 @@ __device__ __forceinline__ MapView bind_map(const EnvDev& d, int m, uint8_t* sme
 // Register a scan slot: origin, heading, noise stream position; queue it.
 __device__ __forceinline__ void add_slot(const EnvDev& d, const Chunk& c, int slot, double x,
                                          double y, double ch, double sh, double sig, uint32_t gid,
-                                         uint64_t nctr, uint8_t bucket, int32_t hwrite, float* o0,
-                                         float* o1) {
-  c.sbucket[slot] = bucket;
+                                         uint64_t nctr, int32_t hwrite, float* o0, float* o1) {
   c.out0[slot] = o0;
   c.out1[slot] = o1;
   c.hwrite[slot] = hwrite;
@@ -704,7 +773,8 @@ __device__ __forceinline__ bool reset_env(const EnvDev& d, const MapView& mv, co
   for (int wi = 0; wi < ((delay + 15) >> 4); ++wi) d.hist[(int64_t)wi * d.n + s] = ~0ull;
   header_row(mc, x, y, bearing_error(x, y, th, mc.goal_x, mc.goal_y), c0, s0, 0.0, 0.0, vml, vma,
              orow, nullptr);
-  add_slot(d, c, slot, x, y, c0, s0, sig, gid, ctr, 0, (int32_t)s, orow, nullptr);  // no history
+  c.qpred[slot] = kNoHistory;  // a fresh spawn has no step history: ranks longest
+  add_slot(d, c, slot, x, y, c0, s0, sig, gid, ctr, (int32_t)s, orow, nullptr);
   ctr += d.nb;
   return true;
 }
@@ -735,13 +805,20 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
                                           int64_t row, uint32_t gid, uint64_t& ctr, int cap,
                                           int slot_cap, uint64_t* mbar, int mpar) {
   StepA r;
+  // fields read late in the step (cross-track, obs header, noise sigma): an
+  // L2 prefetch now turns their later DRAM misses into L2 hits, without
+  // holding registers across the physics
+  prefetch_l2(d.sx + s);
+  prefetch_l2(d.sy + s);
+  prefetch_l2(d.c0 + s);
+  prefetch_l2(d.s0 + s);
+  prefetch_l2(d.psig + s);
   // the lane state is loaded before the action checks, so its DRAM round
-  // trip overlaps the row map -> action one
+  // trip overlaps the action load
   double x = d.x[s], y = d.y[s], h = d.h[s], vl = d.vl[s], va = d.va[s];
   const double k = d.pk[s], dt = d.pdt[s], vml = d.pvl[s], vma = d.pva[s];
   const int32_t delay = d.delay[s];
   int32_t step = d.step[s];
-  const uint32_t qprev = d.qmax[s];  // the scan's bucket needs it last
   const uint8_t nr = d.needs_reset[s];
   const int64_t av = a.actions[row];
   if (av < 0 || av >= d.n_actions) {
@@ -815,7 +892,8 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
     float* o_state = r.ended && d.auto_reset ? nullptr : a.states + row * d.D;
     header_row(mc, x, y, alpha, d.c0[s], d.s0[s], vl, va, vml, vma, o_store, o_state);
     // the post-step scan (core.py:203-206); cos/sin of h1 == of wrap(h1)
-    add_slot(d, c, e, x, y, cos1, sin1, d.psig[s], gid, ctr, scan_bucket(qprev),
+    // (its dispatch prediction c.qpred[e] arrives by cp.async, see the kernel)
+    add_slot(d, c, e, x, y, cos1, sin1, d.psig[s], gid, ctr,
              r.ended && d.auto_reset ? -1 : (int32_t)s, o_store, o_state);
     ctr += d.nb;
     d.x[s] = x; d.y[s] = y; d.h[s] = h; d.vl[s] = vl; d.va[s] = va;
@@ -884,19 +962,34 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
   SP_STAMP(0);
   double2* beam = (double2*)(smem + d.off_beam);
   uint64_t* bar = (uint64_t*)(smem + d.off_bar);
-  const Chunk c = chunk_smem(smem + d.off_chunk, d.chunk_cap, d.slot_cap, d.D, d.R);
-  for (int j = threadIdx.x; j < d.R; j += blockDim.x) beam[j] = d.beam_cs[j];
+  const Chunk c = chunk_smem(smem + d.off_chunk, d.chunk_cap, d.slot_cap);
+  const bool plan = blockIdx.x < (unsigned)d.plan_n;
+  // prologue: the beam table and the first map's constants, copied by
+  // cp.async (one global round trip, no registers held)
+  MapConst* smc = (MapConst*)(bar + 2);  // 72 B in the 128-B barrier block
+  int smc_map = plan ? d.plan_map[blockIdx.x] : -1;
+  for (int j = threadIdx.x; j < d.R; j += blockDim.x) {
+    cp_async8(&beam[j].x, &d.beam_cs[j].x);
+    cp_async8(&beam[j].y, &d.beam_cs[j].y);
+  }
+  if (plan && threadIdx.x < (int)(sizeof(MapConst) / 8))
+    cp_async8((double*)smc + threadIdx.x, (const double*)(d.mconst + smc_map) + threadIdx.x);
   if (threadIdx.x == 0 && kSmem) mbar_init(bar, 1);
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   SP_STAMP(1);
   uint32_t phase = 0;
   if (threadIdx.x == 0) bar[1] = (uint64_t)clock64();  // CTA start (kept in smem, not a register)
-  const int64_t sb = d.cta_begin[blockIdx.x], se = d.cta_begin[blockIdx.x + 1];
+  const int64_t sb = plan ? d.plan_begin[blockIdx.x] : d.cta_begin[blockIdx.x];
+  const int64_t se = plan ? d.plan_begin[blockIdx.x + 1] : d.cta_begin[blockIdx.x + 1];
   const int D = d.D;
   const FinObs<kRec> fin{c, D, d.max_range, d.inv_max_range, d.proximity, a.hit_store,
                          a.hit_state, a.scan_state, a.store_states,
-                         (uint64_t)d.n * (uint64_t)D, (uint32_t)d.env_id_offset, d.R};
-  int m = 0, cur_map = -1;
+                         (uint64_t)d.n * (uint64_t)D, (uint32_t)d.env_id_offset, d.R,
+                         d.gshift};
+  int m = plan ? d.plan_map[blockIdx.x] : 0, cur_map = -1;
+  int64_t mstart = plan ? d.plan_mstart[blockIdx.x] : 0;  // map_off[m], map_off[m + 1]
+  int64_t mend = plan ? d.plan_mend[blockIdx.x] : 0;
   int map_par = -1;  // parity of a map load not yet waited for, or -1
   // shared-memory tables always sit at the start of smem: seeding the view with
   // that address lets the march fold the table base into its LDS offsets
@@ -906,7 +999,11 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     mv.bits = (const uint32_t*)(smem + d.blk_bytes);
   }
   for (int64_t s0 = sb; s0 < se;) {
-    while (d.map_off[m + 1] <= s0) ++m;
+    if (!plan || s0 >= mend) {  // a further map (CTAs spanning maps): from the table
+      while (d.map_off[m + 1] <= s0) ++m;
+      mstart = d.map_off[m];
+      mend = d.map_off[m + 1];
+    }
     if (m != cur_map) {
       // the TMA lands while phase A loads its lanes; step_env waits right
       // before its first table read
@@ -916,17 +1013,33 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       SP_STAMP(2);
 #ifdef SP_TIMING
       if (threadIdx.x == 0) {  // debug: this CTA's env count and map
-        g_sp_ts[blockIdx.x][8] = (unsigned long long)(se - sb);
-        g_sp_ts[blockIdx.x][9] = (unsigned long long)m;
+        s_sp_ts[8] = (unsigned long long)(se - sb);
+        s_sp_ts[9] = (unsigned long long)m;
       }
 #endif
     }
-    const MapConst mc = d.mconst[m];
-    const int n = (int)min((int64_t)d.chunk_cap, min(se, d.map_off[m + 1]) - s0);
+    if (m != smc_map) {  // a further map (CTAs spanning maps): its constants
+      __syncthreads();
+      if (threadIdx.x < (int)(sizeof(MapConst) / 8))
+        ((double*)smc)[threadIdx.x] = ((const double*)(d.mconst + m))[threadIdx.x];
+      smc_map = m;
+    }
+    // the map's constants stay in shared memory, read where used: held in
+    // registers across phase A they would cost 18 of the 80
+    const MapConst& mc = *smc;
+    const int n = (int)min((int64_t)d.chunk_cap, min(se, mend) - s0);
     const int e = threadIdx.x;
     const bool act = e < n;
     const int64_t s = s0 + e;
-    const int64_t row = act ? d.env_of_slot[s] : 0;
+    int64_t row = 0;
+    if (act) {
+      if (d.row_affine) {
+        const int i0 = m >= d.off_mod ? m - d.off_mod : m - d.off_mod + d.n_maps;
+        row = i0 + (s - mstart) * d.n_maps;
+      } else {
+        row = d.env_of_slot[s];
+      }
+    }
     const uint32_t gid = (uint32_t)(d.env_id_offset + row);
     uint64_t ctr = act ? d.ctr[s] : 0;
     __syncthreads();  // the previous chunk is fully written out
@@ -937,6 +1050,8 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     const int kpre = a.mode == MODE_STEP
                          ? min(n, 12 * max(0, (int)blockDim.x - n) / d.nb) : 0;
     if (act) c.rowi[e] = (int32_t)row;
+    if (act && a.mode == MODE_STEP)  // the post-step scan's step history, copied without
+      cp_async8(&c.qpred[e], &d.qhist[s]);  // registers; waited for before the ray order
     if (act && e < kpre) {  // the post-step scan's noise stream (add_slot writes the same)
       c.nctr[e] = ctr;
       c.gid[e] = gid;
@@ -986,15 +1101,31 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       mbar_wait(bar, (uint32_t)map_par);
       map_par = -1;
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+#ifdef SP_TIMING
+    if ((threadIdx.x & 31) == 0) {  // each warp's arrival (lane 0) at the end of phase A
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+      s_sp_ts[12 + (threadIdx.x >> 5)] = t;
+    }
+#endif
     __syncthreads();
     SP_STAMP(3);
     const int n_slots = c.ctl[1];
     // ---- N: LiDAR noise + longest-first ray order; B: LiDAR rays ------------
-    order_slots(c, n_slots, cta_grp());
+#ifdef SP_EXP_SYNC2  // experiment: a bare barrier pair instead of the ordering
+    __syncthreads();
+    SP_STAMP(10);
+    if (threadIdx.x == 0) c.ctl[20] = 0;
+    __syncthreads();
+#else
+    order_entries(d, c, n_slots, cta_grp());
+#endif
+    SP_STAMP(11);
     noise_phase(d, c, n_slots, kpre, cta_grp());
     __syncthreads();
     SP_STAMP(4);
-    ray_phase<kRec>(mv, d, c, beam, n_slots, fin);
+    ray_phase<kRec>(mv, d, c, beam, c.ctl[20], fin);
     __syncthreads();
     SP_STAMP(5);
     store_history(d, c, n_slots);
@@ -1023,16 +1154,19 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       }
       __syncthreads();
       const int n2 = c.ctl[1];
-      order_slots(c, n2, cta_grp());
+      order_entries(d, c, n2, cta_grp());
       noise_phase(d, c, n2, 0, cta_grp());
       __syncthreads();
-      ray_phase<kRec>(mv, d, c, beam, n2, fin);
+      ray_phase<kRec>(mv, d, c, beam, c.ctl[20], fin);
       __syncthreads();
       store_history(d, c, n2);
     }
     SP_STAMP(7);
     s0 += n;
   }
+#ifdef SP_TIMING
+  sp_stamp_flush();
+#endif
   if (a.mode == MODE_STEP) {  // per-CTA duration (launch diagnostics: sp_env_launch_info)
     __syncthreads();
     if (threadIdx.x == 0)
@@ -1063,7 +1197,7 @@ __global__ void __launch_bounds__(SP_SCAN_THREADS, SP_CTAS_PER_SM)
   extern __shared__ __align__(128) uint8_t smem[];
   double2* beam = (double2*)(smem + d.off_beam);
   uint64_t* bar = (uint64_t*)(smem + d.off_bar);
-  const Chunk c = chunk_smem(smem + d.off_chunk, d.chunk_cap, d.slot_cap, d.D, d.R);
+  const Chunk c = chunk_smem(smem + d.off_chunk, d.chunk_cap, d.slot_cap);
   for (int j = threadIdx.x; j < d.R; j += blockDim.x) beam[j] = d.beam_cs[j];
   if (threadIdx.x == 0 && kSmem) mbar_init(bar, 1);
   __syncthreads();
@@ -1093,11 +1227,11 @@ __global__ void __launch_bounds__(SP_SCAN_THREADS, SP_CTAS_PER_SM)
       c.py[e] = q.y[s0 + e];
       c.ch[e] = ch_;
       c.sh[e] = sh_;
-      c.list[e] = e;
+      for (int g = 0; g < d.n_groups; ++g) c.list[e * d.n_groups + g] = (uint16_t)((e << 3) | g);
     }
     __syncthreads();
     const FinScan fin{q.ranges, q.hit_cell, s0, d.R};
-    ray_phase<true>(mv, d, c, beam, n, fin);
+    ray_phase<true>(mv, d, c, beam, n * d.n_groups, fin);
     s0 += n;
   }
 }

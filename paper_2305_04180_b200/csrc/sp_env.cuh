@@ -12,6 +12,10 @@
 #define SP_CTA_THREADS (768 / SP_CTAS_PER_SM)
 #endif
 
+#ifndef SP_PLAN_MAX
+#define SP_PLAN_MAX 296  // CTAs whose slot range rides in the kernel parameters
+#endif
+
 namespace sp {
 
 // Per-map constants (gridmap.py GridMap fields used by core.py:81-86, 133).
@@ -45,7 +49,7 @@ struct EnvDev {
   uint64_t* ctr;          // Philox block counter per lane
   int32_t *step, *delay;
   uint8_t* needs_reset;
-  uint32_t* qmax;         // n: march steps the longest beam of the lane's last scan took
+  uint64_t* qhist;        // n: per beam group, the step levels of the lane's last scan (8 x u8)
   const double* ranges;   // 12 doubles per lane (or shared when ranges_shared)
   int32_t ranges_shared;
   const int64_t* env_of_slot;
@@ -72,9 +76,21 @@ struct EnvDev {
   uint32_t off_beam, off_bar, off_chunk;  // smem offsets
   int32_t smem_maps;      // 1: tables staged in shared memory via TMA bulk copy
   int32_t refill_min;     // ray queue: refill a warp once this many lanes idle
-  int32_t r_shift;        // q / R: shift when R is a power of two, else -1
-  uint64_t r_magic;       // ceil(2^40 / R) for R < 512 (else 0: plain division)
+  int32_t gshift;         // beams per dispatch group = 2^gshift (<= 8 groups per scan)
+  int32_t n_groups;       // groups per scan: ceil(R / 2^gshift)
   uint64_t d_magic;       // ceil(2^40 / D): f / D for f < 2^21 (row writes)
+  // caller row of a slot without the env_of_slot load, for the default map
+  // assignment map = (env_id_offset + row) % n_maps: slot s of map m is row
+  // i0(m) + (s - map_off[m]) * n_maps, i0(m) = (m - off_mod) mod n_maps
+  int32_t row_affine;
+  int32_t off_mod;        // env_id_offset % n_maps
+  // launch plan in the parameters (constant bank): a CTA starts without a
+  // global-memory round trip.  plan_n == 0: read cta_begin / map_off instead
+  int32_t plan_n;
+  int32_t plan_begin[SP_PLAN_MAX + 1];  // slot range of CTA b: [begin[b], begin[b+1])
+  int32_t plan_mstart[SP_PLAN_MAX];     // map_off[map of the CTA's first slot]
+  int32_t plan_mend[SP_PLAN_MAX];       // map_off[that map + 1]
+  int16_t plan_map[SP_PLAN_MAX];        // that map
 };
 
 enum { MODE_STEP = 0, MODE_RESET_ALL = 1, MODE_RESET_LANES = 2 };

@@ -117,64 +117,92 @@ __global__ void disc_collides_kernel(const uint8_t* __restrict__ occ, int64_t H,
 
 // ---------------------------------------------------------------- replay ---
 // Ring append (replay.py:48-67): the n new rows land at rows cursor .. and
-// wrap to 0, so each column is at most two contiguous segments.  The state
-// columns s, s2 are row-contiguous float32 (D per row): per segment one flat
-// float copy with 16-byte stores at 16-byte aligned ring addresses (sources
-// read as float4 when equally aligned -- always when the cursor is a
-// multiple of 4 rows -- else as 4 coalesced scalars), several independent
-// vectors in flight per thread.  The small columns (a i64, r f32, done u8,
-// 13 B/row) follow in the same launch, one thread per row.
+// wrap to 0, so every column is at most two contiguous segments.  The state
+// columns s, s2 are row-contiguous float32 (D per row): four flat float
+// segments (s and s2, before and after the wrap).  Each segment is a head of
+// <= 3 floats (up to the first 16-byte aligned ring address), a body of
+// float4 stores and a tail of <= 3 floats.  The bodies of all four segments
+// form one index space that every thread walks kAppendU vectors at a time,
+// all loads issued before any store (sources read as float4 when equally
+// aligned -- always when the cursor is a multiple of 4 rows -- else as four
+// coalesced scalars), so a launch is one HBM round trip deep.  The small
+// columns (a i64, r f32, done u8: 13 B/row) follow the same pattern.
+constexpr int kAppendU = 4;
 
-// dst[0..count) = src[0..count) over `nt` threads (thread index `t`)
-__device__ __forceinline__ void copy_f32(float* __restrict__ dst, const float* __restrict__ src,
-                                         int64_t count, int64_t t, int64_t nt) {
-  const int head = (int)((((uintptr_t)16 - ((uintptr_t)dst & 15)) & 15) >> 2);
-  const int64_t h = head < count ? head : count;
-  if (t < h) dst[t] = src[t];
-  const int64_t nvec = (count - h) >> 2;
-  float4* __restrict__ d4 = (float4*)(dst + h);
-  const float* sv = src + h;
-  if (((uintptr_t)sv & 15) == 0) {
-    const float4* __restrict__ s4 = (const float4*)sv;
-    int64_t i = t;
-    for (; i + 3 * nt < nvec; i += 4 * nt) {  // four loads in flight
-      const float4 a = __ldcs(s4 + i), b = __ldcs(s4 + i + nt);
-      const float4 c = __ldcs(s4 + i + 2 * nt), e = __ldcs(s4 + i + 3 * nt);
-      d4[i] = a; d4[i + nt] = b; d4[i + 2 * nt] = c; d4[i + 3 * nt] = e;
-    }
-    for (; i < nvec; i += nt) d4[i] = __ldcs(s4 + i);
-  } else {
-    for (int64_t i = t; i < nvec; i += nt) {
-      const float* q = sv + 4 * i;
-      d4[i] = make_float4(__ldcs(q), __ldcs(q + 1), __ldcs(q + 2), __ldcs(q + 3));
-    }
-  }
-  const int64_t done = h + 4 * nvec;
-  if (t < count - done) dst[done + t] = src[done + t];
+struct AppendSeg {
+  float* dst[4];
+  const float* src[4];
+  int64_t head[4];   // floats before the aligned body
+  int64_t nvec[4];   // float4 body vectors
+  int64_t count[4];  // floats in the segment
+  int64_t vend[4];   // inclusive prefix sums of nvec
+  int nseg;
+};
+
+__device__ __forceinline__ float4 load4(const float* p) {
+  if (((uintptr_t)p & 15) == 0) return __ldcs((const float4*)p);
+  return make_float4(__ldcs(p), __ldcs(p + 1), __ldcs(p + 2), __ldcs(p + 3));
 }
 
 __global__ void __launch_bounds__(256) rb_append_kernel(
-    float* __restrict__ rs, int64_t* __restrict__ ra, float* __restrict__ rr,
-    float* __restrict__ rs2, uint8_t* __restrict__ rd, int64_t cap, int32_t dim, int64_t cursor,
-    const float* __restrict__ s, const int64_t* __restrict__ a, const void* __restrict__ r,
-    int r_f64, const float* __restrict__ s2, const uint8_t* __restrict__ dn, int64_t n,
+    const __grid_constant__ AppendSeg g, int64_t* __restrict__ ra, float* __restrict__ rr,
+    uint8_t* __restrict__ rd, int64_t cap, int64_t cursor, const int64_t* __restrict__ a,
+    const void* __restrict__ r, int r_f64, const uint8_t* __restrict__ dn, int64_t n,
     int64_t* __restrict__ d_size, int64_t new_size) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nt = (int64_t)gridDim.x * blockDim.x;
   if (t == 0) *d_size = new_size;  // the ring's fill, on device (sp_rb_sample_dev)
-  const int64_t n1 = n < cap - cursor ? n : cap - cursor;  // rows before the wrap
-  const int64_t D = dim;
-  copy_f32(rs + cursor * D, s, n1 * D, t, nt);
-  copy_f32(rs2 + cursor * D, s2, n1 * D, t, nt);
-  if (n > n1) {
-    copy_f32(rs, s + n1 * D, (n - n1) * D, t, nt);
-    copy_f32(rs2, s2 + n1 * D, (n - n1) * D, t, nt);
+  // heads and tails: <= 6 scalars per segment
+  if (t < 6 * g.nseg) {
+    const int k = (int)(t / 6), e = (int)(t % 6);
+    const int64_t i = e < 3 ? e : g.head[k] + 4 * g.nvec[k] + (e - 3);
+    if ((e < 3 && i < g.head[k]) || (e >= 3 && i < g.count[k])) g.dst[k][i] = g.src[k][i];
   }
-  for (int64_t i = t; i < n; i += nt) {
-    const int64_t row = i < n1 ? cursor + i : i - n1;
-    ra[row] = a[i];
-    rr[row] = r_f64 ? (float)((const double*)r)[i] : ((const float*)r)[i];  // replay.py:53
-    rd[row] = dn[i] ? 1 : 0;
+  const int64_t total = g.vend[g.nseg - 1];
+  for (int64_t base = t; base < total; base += kAppendU * nt) {
+    float4 v[kAppendU];
+    float4* dp[kAppendU];
+#pragma unroll
+    for (int u = 0; u < kAppendU; ++u) {
+      const int64_t q = base + u * nt;
+      dp[u] = nullptr;
+      if (q < total) {
+        int k = 0;
+        while (q >= g.vend[k]) ++k;
+        const int64_t j = q - (k ? g.vend[k - 1] : 0);
+        const int64_t off = g.head[k] + 4 * j;
+        v[u] = load4(g.src[k] + off);
+        dp[u] = (float4*)(g.dst[k] + off);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kAppendU; ++u)
+      if (dp[u]) *dp[u] = v[u];
+  }
+  const int64_t n1 = n < cap - cursor ? n : cap - cursor;  // rows before the wrap
+  for (int64_t base = t; base < n; base += kAppendU * nt) {
+    int64_t av[kAppendU];
+    float rv[kAppendU];
+    uint8_t dv[kAppendU];
+#pragma unroll
+    for (int u = 0; u < kAppendU; ++u) {
+      const int64_t i = base + u * nt;
+      if (i < n) {
+        av[u] = a[i];
+        rv[u] = r_f64 ? (float)((const double*)r)[i] : ((const float*)r)[i];  // replay.py:53
+        dv[u] = dn[i] ? 1 : 0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kAppendU; ++u) {
+      const int64_t i = base + u * nt;
+      if (i < n) {
+        const int64_t row = i < n1 ? cursor + i : i - n1;
+        ra[row] = av[u];
+        rr[row] = rv[u];
+        rd[row] = dv[u];
+      }
+    }
   }
 }
 
@@ -211,9 +239,15 @@ __global__ void rb_sample_kernel(const float* __restrict__ rs, const int64_t* __
   const float* src2 = rs2 + k * dim;
   float* dst = s + i * dim;
   float* dst2 = s2 + i * dim;
-  for (int c = lane; c < dim; c += 32) {
-    dst[c] = src[c];
-    dst2[c] = src2[c];
+  int c = lane;
+  for (; c + 32 < dim; c += 64) {  // both rows' loads in flight before the stores
+    const float v0 = src[c], v1 = src[c + 32], w0 = src2[c], w1 = src2[c + 32];
+    dst[c] = v0; dst[c + 32] = v1; dst2[c] = w0; dst2[c + 32] = w1;
+  }
+  if (c < dim) {
+    const float v0 = src[c], w0 = src2[c];
+    dst[c] = v0;
+    dst2[c] = w0;
   }
 }
 

@@ -19,12 +19,25 @@ for n in (int(os.environ.get("N", "65536")),):
     acts = torch.randint(0, 5, (n,), device=dev)
     if os.environ.get("ACTIONS") == "turn":  # no collisions: phase A without resets
         acts = torch.zeros(n, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    clean = torch.zeros(64 << 20, dtype=torch.float32, device=dev)
     for k in range(int(os.environ.get("STEPS", "10"))):
+        if os.environ.get("FLUSH", "1") == "1":  # bench.py's protocol: cold L2 per step
+            flush.fill_(k & 0xFF)
+            clean.sum()
+        if os.environ.get("ACTIONS") == "fresh":  # new random actions every step (bench.py)
+            acts = torch.randint(0, 5, (n,), device=dev)
         env.step_device(acts.data_ptr(), out)
     torch.cuda.synchronize()
-    ts = np.zeros((148, 12), np.uint64)
+    ts = np.zeros((148, 48), np.uint64)
     lib.sp_debug_read_ts(ts.ctypes.data_as(ctypes.c_void_p), 148)
     ts = ts.astype(np.int64)
+    wa = ts[:, 12:36].copy()  # per-warp phase-A arrivals (cycles), relative to the CTA start
+    wa = (wa - ts[:, :1]) * (1000.0 / 1.965) / 1e6  # -> us
+    ts = ts[:, :12]
+    print("   per-warp end of phase A (us from CTA start), median over CTAs by warp:",
+          " ".join("%.1f" % v for v in np.median(wa, axis=0)))
+    print("   slowest warp per CTA: ids", np.bincount(wa.argmax(1), minlength=24).tolist())
     nenv, mapi = ts[:, 8].copy(), ts[:, 9].copy()
     ts = (ts - ts[:, :1]) * (1000.0 / 1.965)  # cycles -> ns at 1.965 GHz (per-SM clocks)
     ts[:, 0] = 0
@@ -34,6 +47,11 @@ for n in (int(os.environ.get("N", "65536")),):
     d = np.diff(ts[:, :8], axis=1) / 1e3
     for i, nm in enumerate(names):
         print(f"   {nm:12s} median {np.median(d[:, i]):6.2f} us  max {d[:, i].max():6.2f} us")
+    order = (ts[:, 11] - ts[:, 3]) / 1e3
+    print("   of order+noise: ordering %.2f us median (max %.2f)" % (np.median(order), order.max()))
+    if os.environ.get("SYNC2"):
+        b1 = (ts[:, 10] - ts[:, 3]) / 1e3
+        print("   sync2: first barrier after A %.2f us median (max %.2f)" % (np.median(b1), b1.max()))
     rays = d[:, 4]
     drain = (ts[:, 10] - ts[:, 4]) / 1e3  # queue drained, relative to the ray phase start
     print("   ray queue drained %.1f us into the ray phase (median); tail after it: median %.1f us, max %.1f us"

@@ -44,6 +44,9 @@ def main():
         v *= SCALE.get(key, {}).get(units[i], 1)
         res[key] = v
     res["traffic_bytes_per_launch"] = res.get("dram_bytes_read", 0) + res.get("dram_bytes_write", 0)
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2305_04180_b200.build import source_hash
+    res["source_hash"] = source_hash()  # bench.py reports the capture only for this build
     json.dump(res, open("profiles/ncu_step_traffic.json", "w"), indent=1)
     print(json.dumps(res, indent=1))
 
