@@ -497,7 +497,9 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
     d.nb_shift = (d.nb & (d.nb - 1)) == 0 ? __builtin_ctz((unsigned)d.nb) : -1;
     d.inv_max_range = 1.0 / cfg->max_range_cm;
     const char* rm = std::getenv("SPARROW_REFILL_MIN");
-    d.refill_min = rm ? std::max(1, std::min(64, std::atoi(rm))) : 32;
+    d.refill_min = rm ? std::max(1, std::min(64, std::atoi(rm))) : 40;
+    const char* pn = std::getenv("SPARROW_PRENOISE");
+    d.prenoise = pn ? std::max(0, std::min(64, std::atoi(pn))) : 12;
   }
   Plan plan = plan_launch(env, env->map_off);
   apply_plan(plan, d);

@@ -154,14 +154,27 @@ __device__ __forceinline__ void sp_stamp(int k) {
 }
 __device__ __forceinline__ void sp_stamp_flush() {
   __syncthreads();
+  if (threadIdx.x == 0) {  // CTA end on the GPU-wide clock (ns)
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)::"memory");
+    s_sp_ts[37] = g;
+  }
+  __syncthreads();
   if (threadIdx.x < 48 && blockIdx.x < 1024) g_sp_ts[blockIdx.x][threadIdx.x] = s_sp_ts[threadIdx.x];
 }
 #define SP_STAMP(k) sp_stamp(k)
+// env thread 0 inside step_env (slots 38..)
+#define SP_ESTAMP(k) do { if (threadIdx.x == 0) { unsigned long long t_; \
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_)::"memory"); s_sp_ts[k] = t_; } } while (0)
 #else
+#define SP_ESTAMP(k)
 #define SP_STAMP(k)
 #endif
 
 // ---------------------------------------------------------------- rays ---
+#ifndef SP_MARCH_GROUP
+#define SP_MARCH_GROUP 4  // march steps per slot between refill checks
+#endif
 // Ray state, mirrored so that every ray moves toward +u, +v: on an axis the
 // ray travels in the negative direction, coordinates are negated (exactly)
 // and cell indices become u = -ix - 1, so cell u covers [u, u + 1).  In cell
@@ -455,7 +468,7 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
     // branch are paid once per four steps (2 -> 4: -2 % step with the cheaper
     // per-cell steps); a finished ray stays put for the rest of the group
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < SP_MARCH_GROUP; ++u) {
       fin_a = ray_step(ra, mv, d);
       fin_b = ray_step(rb, mv, d);
     }
@@ -547,6 +560,16 @@ __device__ __forceinline__ void set_error(const EnvDev& d, int code, int64_t row
   if (atomicCAS(d.err, 0, code) == 0) d.err[1] = (int32_t)row;
 }
 
+// caller row of slot s of map m (map_off[m] = mstart): computed for the default
+// map assignment (EnvDev::row_affine), else the env_of_slot table
+__device__ __forceinline__ int64_t row_of(const EnvDev& d, int m, int64_t mstart, int64_t s) {
+  if (d.row_affine) {
+    const int i0 = m >= d.off_mod ? m - d.off_mod : m - d.off_mod + d.n_maps;
+    return i0 + (s - mstart) * d.n_maps;
+  }
+  return d.env_of_slot[s];
+}
+
 // LiDAR noise (core.py:237-241): every listed slot needs R standard normals
 // from blocks nctr[slot] .. nctr[slot]+nb-1 of its stream.  One work item per
 // Philox block, spread over the whole CTA; z parks in the slot's output row.
@@ -569,9 +592,21 @@ __device__ __forceinline__ void noise_block(const EnvDev& d, const Chunk& c, int
 // counter at step start (c.nctr/c.gid snapshot at chunk start), and only z is
 // staged (sigma is applied when the ray retires), so nothing here depends on
 // phase A.  first = the first idle thread.
-__device__ __forceinline__ void prenoise(const EnvDev& d, const Chunk& c, int n, int first) {
+__device__ __forceinline__ void prenoise(const EnvDev& d, const StepArgs& a, const Chunk& c,
+                                         int n, int first, int64_t s0, int m, int64_t mstart) {
   const int nb = d.nb;
   const int idle = (int)blockDim.x - first;
+  // the noise streams of env slots 0..n-1 (the values add_slot later writes
+  // into the same words): loaded by the noise warps themselves, so the env
+  // threads never wait for them; then a barrier among the noise warps only
+  for (int k = (int)threadIdx.x - first; k < n; k += idle) {
+    const int64_t s = s0 + k;
+    const int64_t row = row_of(d, m, mstart, s);
+    c.nctr[k] = d.ctr[s];
+    c.gid[k] = (uint32_t)(d.env_id_offset + row);
+    c.out0[k] = a.store_states + row * d.D;  // z parks in the store_states row
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(idle) : "memory");
   for (int it = (int)threadIdx.x - first; it < n * nb; it += idle) {
     const int k = d.nb_shift >= 0 ? (it >> d.nb_shift) : it / nb;
     noise_block(d, c, k, it - k * nb);
@@ -802,8 +837,8 @@ struct StepA {
 
 __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, const MapView& mv,
                                           const MapConst& mc, const Chunk& c, int e, int64_t s,
-                                          int64_t row, uint32_t gid, uint64_t& ctr, int cap,
-                                          int slot_cap, uint64_t* mbar, int mpar) {
+                                          int64_t row, uint32_t gid, uint64_t& ctr, int64_t av,
+                                          int cap, int slot_cap, uint64_t* mbar, int mpar) {
   StepA r;
   // fields read late in the step (cross-track, obs header, noise sigma): an
   // L2 prefetch now turns their later DRAM misses into L2 hits, without
@@ -820,7 +855,6 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
   const int32_t delay = d.delay[s];
   int32_t step = d.step[s];
   const uint8_t nr = d.needs_reset[s];
-  const int64_t av = a.actions[row];
   if (av < 0 || av >= d.n_actions) {
     set_error(d, SP_EACTION, row);
   } else if (nr) {
@@ -828,6 +862,7 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
   } else {
     r.live = true;
     // delay queue (core.py:176-182): matured = action issued `delay` steps ago
+    SP_ESTAMP(38);
     uint32_t code = (uint32_t)av;
     if (delay > 0) {
       const int q = delay - 1;
@@ -865,8 +900,11 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
     y = dadd(y, ddy);
     h = wrap_angle(h1);
     // events (core.py:189-201)
+    SP_ESTAMP(39);
     if (mpar >= 0) mbar_wait(mbar, (uint32_t)mpar);  // the map tables (staged during the loads above)
+    SP_ESTAMP(40);
     const bool coll = disc_hits(mv, d, x, y);
+    SP_ESTAMP(41);
     const double gdx = dsub(mc.goal_x, x), gdy = dsub(mc.goal_y, y);
     const double d1 = __dsqrt_rn(dadd(dmul(gdx, gdx), dmul(gdy, gdy)));
     const bool arrived = !coll && d1 <= mc.goal_r;
@@ -890,7 +928,9 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
     // the episode ended and resets (then states gets the fresh scan)
     float* o_store = a.store_states + row * d.D;
     float* o_state = r.ended && d.auto_reset ? nullptr : a.states + row * d.D;
+    SP_ESTAMP(42);
     header_row(mc, x, y, alpha, d.c0[s], d.s0[s], vl, va, vml, vma, o_store, o_state);
+    SP_ESTAMP(43);
     // the post-step scan (core.py:203-206); cos/sin of h1 == of wrap(h1)
     // (its dispatch prediction c.qpred[e] arrives by cp.async, see the kernel)
     add_slot(d, c, e, x, y, cos1, sin1, d.psig[s], gid, ctr,
@@ -960,6 +1000,13 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     env_step_kernel(const __grid_constant__ EnvDev d, const __grid_constant__ StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   SP_STAMP(0);
+#ifdef SP_TIMING
+  if (threadIdx.x == 0) {  // CTA start on the GPU-wide clock (ns)
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)::"memory");
+    s_sp_ts[36] = g;
+  }
+#endif
   double2* beam = (double2*)(smem + d.off_beam);
   uint64_t* bar = (uint64_t*)(smem + d.off_bar);
   const Chunk c = chunk_smem(smem + d.off_chunk, d.chunk_cap, d.slot_cap);
@@ -1031,34 +1078,27 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     const int e = threadIdx.x;
     const bool act = e < n;
     const int64_t s = s0 + e;
-    int64_t row = 0;
-    if (act) {
-      if (d.row_affine) {
-        const int i0 = m >= d.off_mod ? m - d.off_mod : m - d.off_mod + d.n_maps;
-        row = i0 + (s - mstart) * d.n_maps;
-      } else {
-        row = d.env_of_slot[s];
-      }
-    }
+    const int64_t row = act ? row_of(d, m, mstart, s) : 0;
     const uint32_t gid = (uint32_t)(d.env_id_offset + row);
+    // the lane's counter and action: loads in flight across the barrier below
     uint64_t ctr = act ? d.ctr[s] : 0;
+    const int64_t av = act && a.mode == MODE_STEP ? a.actions[row] : 0;
     __syncthreads();  // the previous chunk is fully written out
     if (threadIdx.x < 4) c.ctl[threadIdx.x] = 0;
-    // idle threads pre-noise the first kpre env slots during phase A: about
-    // 12 blocks per idle thread fit in phase A's latency (more would make
-    // them its tail); the rest is done after phase A
+    // the warps without an env pre-noise the first kpre env slots during phase
+    // A, d.prenoise blocks per thread (what fits in phase A's latency: more
+    // would make them its tail); every thread does the rest after phase A.
+    // Only whole idle warps: a warp mixing env and noise threads runs both
+    // paths one after the other and became phase A's slowest warp
+    const int first_idle = (n + 31) & ~31;
     const int kpre = a.mode == MODE_STEP
-                         ? min(n, 12 * max(0, (int)blockDim.x - n) / d.nb) : 0;
+                         ? min(n, d.prenoise * max(0, (int)blockDim.x - first_idle) / d.nb)
+                         : 0;
     if (act) c.rowi[e] = (int32_t)row;
     if (act && a.mode == MODE_STEP)  // the post-step scan's step history, copied without
       cp_async8(&c.qpred[e], &d.qhist[s]);  // registers; waited for before the ray order
-    if (act && e < kpre) {  // the post-step scan's noise stream (add_slot writes the same)
-      c.nctr[e] = ctr;
-      c.gid[e] = gid;
-      c.out0[e] = a.store_states + row * d.D;  // z parks in the store_states row
-    }
     __syncthreads();
-    if (kpre > 0 && !act) prenoise(d, c, kpre, n);
+    if (kpre > 0 && e >= first_idle) prenoise(d, a, c, kpre, first_idle, s0, m, mstart);
 
     // ---- A: physics, collision, events, reward partial, resets -----------
     if (act) {
@@ -1083,8 +1123,8 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       }
     } else if (act) {
       const double ret_prev = d.ret[s];  // issued early: only the outputs wait on it
-      const StepA r = step_env(d, a, mv, mc, c, e, s, row, gid, ctr, d.chunk_cap, d.slot_cap, bar,
-                               map_par);
+      const StepA r = step_env(d, a, mv, mc, c, e, s, row, gid, ctr, av, d.chunk_cap, d.slot_cap,
+                               bar, map_par);
       d.ctr[s] = ctr;
       if (r.live) {
         if (r.ev == 1 || r.ev == 2) {  // terminal reward: no scan needed

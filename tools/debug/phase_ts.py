@@ -32,6 +32,16 @@ for n in (int(os.environ.get("N", "65536")),):
     ts = np.zeros((148, 48), np.uint64)
     lib.sp_debug_read_ts(ts.ctypes.data_as(ctypes.c_void_p), 148)
     ts = ts.astype(np.int64)
+    g0, g1 = ts[:, 36].copy(), ts[:, 37].copy()
+    print("   globaltimer: CTA starts span %.2f us, ends span %.2f us, kernel span %.2f us; "
+          "CTA durations median %.1f max %.1f us"
+          % ((g0.max() - g0.min()) / 1e3, (g1.max() - g1.min()) / 1e3, (g1.max() - g0.min()) / 1e3,
+             np.median(g1 - g0) / 1e3, (g1 - g0).max() / 1e3))
+    es = ts[:, 38:44].copy()
+    rel = (es - ts[:, 2:3]) * (1000.0 / 1.965) / 1e6  # us from stamp 2 (phase A start)
+    print("   env 0 in step_env (us after phase A start, median): action loaded %.2f, physics done %.2f, "
+          "map ready %.2f, disc %.2f, reward %.2f, header %.2f"
+          % tuple(np.median(rel, axis=0)))
     wa = ts[:, 12:36].copy()  # per-warp phase-A arrivals (cycles), relative to the CTA start
     wa = (wa - ts[:, :1]) * (1000.0 / 1.965) / 1e6  # -> us
     ts = ts[:, :12]
