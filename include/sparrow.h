@@ -30,6 +30,8 @@
  *   sp_philox_fill      asl/vem.py:57-66 draws (rng.random / rng.integers), on device
  *   sp_adam_step        net.py:141-161 adam_step, fused over all tensors, on device
  *   sp_ddqn_update      ddqn.py:54-77 DdqnLearner.update (targets, backprop, Adam), on device
+ *   sp_actor_select     asl/loops.py:57-60 + net.py:77-80 + asl/vem.py:38-66: forward, VEM
+ *                       epsilons and epsilon-greedy selection in one launch
  */
 #ifndef SPARROW_H_
 #define SPARROW_H_
@@ -257,6 +259,24 @@ int64_t sp_ddqn_scratch_floats(const int32_t* sizes, int64_t batch);
  * A <= 16, 16-byte aligned weights and sp_ddqn_scratch_floats(...) >= 0 (the
  * three staged weight matrices fit in shared memory: e.g. [32|37,256,128,5]).
  * The target net is read only. */
+/* VemSchedule (asl/vem.py:19-35) */
+typedef struct {
+  int64_t n_envs, or_init, or_final, decay_steps;
+  double e_min, e_max;
+} SpVem;
+
+/* The actor's input to an env step in one launch (asl/loops.py:57-60):
+ * Q = MLP(states) (net.py:77-80), the VEM epsilon of copy env0 + i at t_step
+ * computed on the device (vem.py:38-54), epsilon-greedy selection
+ * (vem.py:57-66) drawing explore tests from blocks ctr .. ctr+n-1 and random
+ * actions from ctr+n .. ctr+2n-1 of Philox stream (seed, lane, tag) -- the
+ * caller advances its counter by 2n.  actions: dev int64 [n]; q_out: dev f32
+ * [n][A] or NULL.  Weights: 16-byte aligned fp32 device tensors, layer
+ * sizes D0 <= 64, H1, H2 <= 256, A <= 16, each matrix a multiple of 4 floats. */
+int sp_actor_select(const SpMlp* net, const float* states, int64_t n, int64_t env0,
+                    const SpVem* vem, int64_t t_step, uint64_t seed, uint32_t lane, uint32_t tag,
+                    uint64_t ctr, int64_t* actions, float* q_out, void* stream);
+
 int sp_ddqn_update(const SpMlp* online, const SpMlp* target, const float* s, const int64_t* a,
                    const float* r, const float* s2, const uint8_t* d, int64_t batch, float gamma,
                    float* const* m, float* const* v, double* step_dev, double lr, double beta1,

@@ -120,6 +120,9 @@ SIGNATURES = [
                                     ctypes.c_int64, c_vp, ctypes.c_double, ctypes.c_double,
                                     ctypes.c_double, ctypes.c_double, c_vp]),
     ("sp_ddqn_scratch_floats", ctypes.c_int64, [c_i32p, ctypes.c_int64]),
+    ("sp_actor_select", ctypes.c_int, [c_vp, c_vp, ctypes.c_int64, ctypes.c_int64, c_vp,
+                                       ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint32,
+                                       ctypes.c_uint32, ctypes.c_uint64, c_vp, c_vp, c_vp]),
     ("sp_ddqn_update", ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_int64,
                                       ctypes.c_float, c_vp, c_vp, c_vp, ctypes.c_double,
                                       ctypes.c_double, ctypes.c_double, ctypes.c_double, c_vp,
@@ -134,6 +137,13 @@ class SpMlp(ctypes.Structure):
         ("sizes", ctypes.c_int32 * 4),
         ("W", ctypes.c_void_p * 3),
         ("b", ctypes.c_void_p * 3),
+    ]
+
+
+class SpVem(ctypes.Structure):
+    _fields_ = [
+        ("n_envs", ctypes.c_int64), ("or_init", ctypes.c_int64), ("or_final", ctypes.c_int64),
+        ("decay_steps", ctypes.c_int64), ("e_min", ctypes.c_double), ("e_max", ctypes.c_double),
     ]
 
 

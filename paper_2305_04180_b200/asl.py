@@ -631,6 +631,36 @@ def select_actions(q, epsilons, rng):
     return torch.where(explore, randoms, greedy)
 
 
+def select_actions_fused(params: QNet, states, vem: VemSchedule, t_step: int, rng,
+                         env0: int = 0, out=None, q_out=None):
+    """The actor's ``net.forward`` -> ``vem.epsilons(t_step)`` -> ``select_actions``
+    (loops.py:57-59) as one kernel launch (``sp_actor_select``): the epsilons
+    are computed on the device from the scalar ``t_step``, so nothing crosses
+    the host per step.  Same draws as ``select_actions`` (random(n), then
+    integers(0, A, n) from ``rng``; its counter advances by 2n).  ``env0``: VEM
+    copy index of row 0 (a shard's env id offset)."""
+    torch = _torch()
+    n = int(states.shape[0])
+    dev = states.device
+    if out is None:
+        out = torch.empty(n, dtype=torch.int64, device=dev)
+    m = _lib.SpMlp()
+    m.sizes[:] = list(params.sizes)
+    for i in range(3):
+        m.W[i] = params.weights[i].data_ptr()
+        m.b[i] = params.biases[i].data_ptr()
+    v = _lib.SpVem(vem.n_envs, vem.or_init, vem.or_final, vem.decay_steps, vem.e_min, vem.e_max)
+    st = states if states.dtype == torch.float32 and states.is_contiguous() else \
+        states.to(torch.float32).contiguous()
+    tag = int(getattr(rng, "tag", 3))
+    _lib.check(_lib.load().sp_actor_select(
+        ctypes.byref(m), st.data_ptr(), n, int(env0), ctypes.byref(v), int(t_step), rng.seed,
+        rng.lane, tag, rng.ctr, out.data_ptr(), q_out.data_ptr() if q_out is not None else None,
+        _lib.stream_ptr(dev)), "actor_select")
+    rng.ctr += 2 * n
+    return out
+
+
 # -- TFM (asl/tfm.py) -------------------------------------------------------------------
 
 @dataclass(frozen=True)
@@ -702,16 +732,25 @@ class PublishedModel:
     device-to-host read and a CRC every ``upload_period`` updates. Unpacks
     like the reference's NamedTuple."""
 
-    __slots__ = ("version", "params", "_crc")
+    __slots__ = ("version", "params", "_crc", "ready")
 
-    def __init__(self, version: int, params: QNet, checksum: int | None = None):
+    def __init__(self, version: int, params: QNet, checksum: int | None = None, ready=None):
         self.version = int(version)
         self.params = params
         self._crc = checksum
+        self.ready = ready  # CUDA event: the copy kernels have written params
+
+    def wait(self, stream=None) -> None:
+        """Order `stream` (default: the current one) after the copy that made
+        this snapshot; the reader must call it before touching params."""
+        if self.ready is not None:
+            (stream or _torch().cuda.current_stream()).wait_event(self.ready)
 
     @property
     def checksum(self) -> int:
         if self._crc is None:
+            if self.ready is not None:
+                self.ready.synchronize()
             self._crc = _checksum(self.params)
         return self._crc
 
@@ -741,8 +780,14 @@ class Sharer:
         self._error: BaseException | None = None
 
     def publish_params(self, params: QNet) -> PublishedModel:
-        snap_params = params.copy()
-        snap = PublishedModel(params.version, snap_params)  # crc32 on first read
+        torch = _torch()
+        snap_params = params.copy()  # clone kernels on the publisher's stream
+        ready = torch.cuda.Event()
+        ready.record(torch.cuda.current_stream(snap_params.weights[0].device))
+        # readers order their stream after `ready` (PublishedModel.wait) before
+        # touching the copy: the reference copies on the host, so it has no
+        # window in which a half-written snapshot is visible
+        snap = PublishedModel(params.version, snap_params, ready=ready)  # crc32 on first read
         self._published = snap  # atomic reference swap
         self.publish_count += 1
         return snap
@@ -777,33 +822,54 @@ _IDLE_POLL_S = 0.002
 
 
 def actor_loop(sharer: Sharer, vec_env, initial_states, params: QNet, vem: VemSchedule,
-               tfm_cfg: TfmConfig, max_steps: int, rng) -> None:
-    """loops.py:43-71 on device: forward -> VEM -> step -> append, no host data."""
+               tfm_cfg: TfmConfig, max_steps: int, rng, env0: int = 0) -> None:
+    """loops.py:43-71 on device with no host round trip per iteration: one
+    ``sp_actor_select`` launch (forward, VEM epsilons from the scalar t_step,
+    epsilon-greedy), the fused env step, the ring append.  Outputs alternate
+    between two StepBatch buffers (stream order keeps iteration k's append
+    reading its rows while step k + 1 writes the other set).  The host runs at
+    most two iterations ahead of the GPU, and the TFM interaction period is
+    the CUDA-event time between iteration ends, recorded once completed."""
+    from collections import deque
     torch = _torch()
     dev = vec_env.device
-    with torch.cuda.stream(torch.cuda.Stream(dev)):
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
         states = initial_states
         params = params.copy()
         version = params.version
         n = vec_env.n_copies
+        outs = [vec_env.new_batch(), vec_env.new_batch()]
+        acts = [torch.empty(n, dtype=torch.int64, device=dev) for _ in range(2)]
+        ends = deque()  # iteration-end events not yet folded into the TFM
+        k = 0
         try:
             while sharer.t_step < max_steps and not sharer.stop.is_set():
-                started = time.perf_counter()
+                if len(ends) >= 3:  # bounded run-ahead: wait for iteration k - 2
+                    ends[-3].synchronize()
+                while len(ends) >= 2 and ends[1].query():
+                    sharer.tfm.record_interaction(ends[0].elapsed_time(ends[1]) / 1e3)
+                    ends.popleft()
                 snap = sharer.fetch_params(version)
                 if snap is not None:
+                    snap.wait(stream)
                     params, version = snap.params, snap.version
-                q = params.forward(states)
-                actions = select_actions(q, vem.epsilons(sharer.t_step), rng)
-                batch = vec_env.step_batch(actions)
-                sharer.buffer.append_batch(states, actions, batch.rewards, batch.store_states,
+                a = select_actions_fused(params, states, vem, sharer.t_step, rng, env0,
+                                         out=acts[k & 1])
+                batch = outs[k & 1]
+                vec_env.step_device(a.data_ptr(), batch)  # actions valid by construction
+                sharer.buffer.append_batch(states, a, batch.rewards, batch.store_states,
                                            batch.dones)
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(stream)
+                ends.append(ev)
                 states = batch.states
-                torch.cuda.current_stream(dev).synchronize()  # the period TFM measures
-                sharer.tfm.record_interaction(time.perf_counter() - started)
                 sharer.t_step += n
+                k += 1
                 nap = sharer.tfm.actor_sleep(tfm_cfg)
                 if nap > 0:
                     time.sleep(nap)
+            stream.synchronize()
         finally:
             sharer.stop.set()
 

@@ -16,7 +16,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib", "libsparrow.so")
-SOURCES = ["sp_capi.cu", "sp_env.cu", "sp_ops.cu", "sp_learn.cu", "sp_env.cuh", "sp_common.cuh"]
+SOURCES = ["sp_capi.cu", "sp_env.cu", "sp_ops.cu", "sp_learn.cu", "sp_actor.cu", "sp_env.cuh",
+           "sp_common.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -18,6 +18,7 @@
 #include "sp_env.cu"
 #include "sp_ops.cu"
 #include "sp_learn.cu"
+#include "sp_actor.cu"
 
 using namespace sp;
 
@@ -1275,6 +1276,53 @@ int sp_ddqn_update(const SpMlp* on, const SpMlp* tg, const float* s, const int64
                                                 stats_out);
   SP_CUDA(cudaGetLastError());
   adam_tick_stats_kernel<<<1, 1, 0, st>>>(step_dev, stats_out);
+  SP_CUDA(cudaGetLastError());
+  return SP_OK;
+}
+
+int sp_actor_select(const SpMlp* net, const float* states, int64_t n, int64_t env0,
+                    const SpVem* vem, int64_t t_step, uint64_t seed, uint32_t lane, uint32_t tag,
+                    uint64_t ctr, int64_t* actions, float* q_out, void* stream) {
+  if (!net || !vem || (n > 0 && (!states || !actions))) return fail(SP_EINVAL, "null argument");
+  if (n < 1) return SP_OK;
+  const int D0 = net->sizes[0], H1 = net->sizes[1], H2 = net->sizes[2], A = net->sizes[3];
+  if (D0 < 1 || D0 > kActMaxD0 || H1 < 1 || H1 > kActMaxH || H2 < 1 || H2 > kActMaxH || A < 1 ||
+      A > kActMaxA)
+    return fail(SP_EINVAL, "actor: unsupported layer sizes");
+  if ((D0 * H1) % 4 || (H1 * H2) % 4 || (H2 * A) % 4)
+    return fail(SP_EINVAL, "actor: each weight matrix must hold a multiple of 4 floats");
+  for (int l = 0; l < 3; ++l)
+    if (!net->W[l] || !net->b[l] || ((uintptr_t)net->W[l] & 15))
+      return fail(SP_EINVAL, "actor: weights must be 16-byte aligned device tensors");
+  if (!(vem->n_envs >= 1 && 1 <= vem->or_final && vem->or_final <= vem->or_init &&
+        vem->or_init <= vem->n_envs && vem->decay_steps >= 1 && 0.0 <= vem->e_min &&
+        vem->e_min <= vem->e_max && vem->e_max <= 1.0))
+    return fail(SP_EINVAL, "actor: bad VEM schedule");  // vem.py:28-35
+  if (env0 < 0 || env0 + n > vem->n_envs) return fail(SP_EINVAL, "actor: rows outside the VEM copies");
+  int dev = 0;
+  SP_CUDA(cudaGetDevice(&dev));
+  int optin = 0, n_sm = 0;
+  SP_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  SP_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  int rows = 32;
+  while (rows > 4 && actor_smem_bytes(D0, H1, H2, A, rows) > (size_t)optin) rows /= 2;
+  const size_t sm = actor_smem_bytes(D0, H1, H2, A, rows);
+  if (sm > (size_t)optin) return fail(SP_EINVAL, "actor: weights do not fit in shared memory");
+  ActorArgs a{};
+  for (int l = 0; l < 3; ++l) {
+    a.W[l] = net->W[l];
+    a.b[l] = net->b[l];
+  }
+  a.D0 = D0; a.H1 = H1; a.H2 = H2; a.A = A; a.L0 = pad4(D0); a.rows = rows;
+  a.states = states; a.n = n; a.env0 = env0;
+  a.vem = VemDev{vem->n_envs, vem->or_init, vem->or_final, vem->decay_steps, vem->e_min,
+                 vem->e_max};
+  a.t_step = t_step; a.seed = seed; a.lane = lane; a.tag = tag; a.ctr = ctr;
+  a.actions = actions; a.q_out = q_out;
+  SP_CUDA(cudaFuncSetAttribute(actor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  const int64_t tiles = (n + rows - 1) / rows;
+  const int grid = (int)std::min<int64_t>(tiles, n_sm);
+  actor_kernel<<<grid, kActThreads, sm, (cudaStream_t)stream>>>(a);
   SP_CUDA(cudaGetLastError());
   return SP_OK;
 }

@@ -18,6 +18,26 @@
 #define SP_INV_PI 0.3183098861837907  // 1 / SP_PI, correctly rounded
 #define SP_FULL 0xffffffffu
 
+// SP_CHECKED builds (tools/gpu_checked.sh): device-side bounds checks on
+// the step kernel's shared-memory slots, queue entries, table cells and
+// output rows -- compute-sanitizer is closed on this pool, so the checks
+// are our own.  A failed check prints its site and traps.
+#ifdef SP_CHECKED
+#include <cstdio>
+#define SP_CHECK(cond)                                                              \
+  do {                                                                              \
+    if (!(cond)) {                                                                  \
+      printf("SP_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                          \
+      __trap();                                                                     \
+    }                                                                               \
+  } while (0)
+#else
+#define SP_CHECK(cond) \
+  do {             \
+  } while (0)
+#endif
+
 namespace sp {
 
 // ---------------------------------------------------------------- Philox ---

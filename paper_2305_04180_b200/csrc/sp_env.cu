@@ -224,6 +224,7 @@ __device__ __forceinline__ int floor_i(double v) {  // floor(v), |v| < 2^31
 // (GridMap's invariant, checked by sp_env_create), so no step can leave the
 // grid and there are no bounds tests.
 __device__ __forceinline__ bool ray_step(Ray& r, const MapView& mv, const EnvDev& d) {
+  SP_CHECK((unsigned)(r.v * r.ayw + r.u * r.ax + r.kb) < (unsigned)(d.Wb * d.Hb));
   const int code = (int)((const int8_t*)mv.blk)[r.v * r.ayw + r.u * r.ax + r.kb];
   const bool occupied = code < 0;  // else the box radius
   // the free box's far faces: u + 1 + r (r = 0: this cell's own face)
@@ -377,6 +378,7 @@ constexpr uint64_t kNoHistory = 0x8080808080808080ull;  // every group "longest"
 
 // queue index q -> (slot, beam) of its (slot, group) entry
 __device__ __forceinline__ int beam_of(const Chunk& c, int q, int gs, int& slot) {
+  SP_CHECK((q >> gs) < c.ctl[20]);
   const uint32_t e = c.list[q >> gs];
   slot = (int)(e >> 3);
   return (int)((e & 7u) << gs) + (q & ((1 << gs) - 1));
@@ -551,6 +553,7 @@ __device__ __forceinline__ void order_entries(const EnvDev& d, const Chunk& c, i
     int pos = 0;
     if (b < 8 && lane == leader) pos = atomicAdd(&off[b], __popc(peers));
     pos = __shfl_sync(SP_FULL, pos, leader);
+    SP_CHECK(b >= 8 || pos + __popc(peers & lt) < 8 * d.slot_cap);
     if (b < 8) c.list[pos + __popc(peers & lt)] = (uint16_t)((slot << 3) | (k & 7));
   }
   g.sync();  // c.list complete before anyone dispatches from it
@@ -578,6 +581,7 @@ __device__ __forceinline__ void noise_block(const EnvDev& d, const Chunk& c, int
   const Block4 blk = stream_block(d.seed, c.gid[slot], 0u, c.nctr[slot] + (uint64_t)b);
   float z[4];
   draw_normals4(blk, z);
+  SP_CHECK(slot >= 0 && slot < d.slot_cap && b >= 0 && b < d.nb);
   float* row = c.out0[slot] + 5 + 4 * b;
 #ifdef SP_EXP_NOZ  // experiment: no z stores (wrong noise), isolates their cost
   if (z[0] == 12345.0f)
@@ -697,12 +701,14 @@ struct FinObs {
   uint32_t gid0;            // (uint32) env_id_offset: row = gid - gid0
   int R;
   int gs;                   // log2 of the beams per group (step-level history)
+  int d_slot_cap;           // SP_CHECKED bounds
   // z of beam j, parked in the output row by the noise pass: loaded when the
   // ray is dispatched so the L2 round trip overlaps its march
   __device__ __forceinline__ float pre(int slot, int j) const { return c.out0[slot][5 + j]; }
   __device__ __forceinline__ void operator()(int slot, int j, double t, int hit, int steps,
                                              float zpre) const {
     float* rowp = c.out0[slot];
+    SP_CHECK(slot >= 0 && slot < d_slot_cap && j >= 0 && j < R);
     const double z = (double)zpre;
     const double v = dclip(dadd(t, dadd(0.0, dmul(c.sig[slot], z))), 0.0, max_range);
     const float o = (float)div_by(v, max_range, inv_max_range);
@@ -758,6 +764,7 @@ __device__ __forceinline__ MapView bind_map(const EnvDev& d, int m, uint8_t* sme
 __device__ __forceinline__ void add_slot(const EnvDev& d, const Chunk& c, int slot, double x,
                                          double y, double ch, double sh, double sig, uint32_t gid,
                                          uint64_t nctr, int32_t hwrite, float* o0, float* o1) {
+  SP_CHECK(slot >= 0 && slot < d.slot_cap && c.ctl[1] < d.slot_cap);
   c.out0[slot] = o0;
   c.out1[slot] = o1;
   c.hwrite[slot] = hwrite;
@@ -1033,7 +1040,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
   const FinObs<kRec> fin{c, D, d.max_range, d.inv_max_range, d.proximity, a.hit_store,
                          a.hit_state, a.scan_state, a.store_states,
                          (uint64_t)d.n * (uint64_t)D, (uint32_t)d.env_id_offset, d.R,
-                         d.gshift};
+                         d.gshift, d.slot_cap};
   int m = plan ? d.plan_map[blockIdx.x] : 0, cur_map = -1;
   int64_t mstart = plan ? d.plan_mstart[blockIdx.x] : 0;  // map_off[m], map_off[m + 1]
   int64_t mend = plan ? d.plan_mend[blockIdx.x] : 0;
@@ -1259,7 +1266,10 @@ __global__ void __launch_bounds__(SP_SCAN_THREADS, SP_CTAS_PER_SM)
     }
     const int n = (int)min((int64_t)d.chunk_cap, min(se, q.qoff[m + 1]) - s0);
     __syncthreads();
-    if (threadIdx.x == 0) c.ctl[0] = 0;
+    if (threadIdx.x == 0) {
+      c.ctl[0] = 0;
+      c.ctl[20] = n * d.n_groups;  // entries listed (the order is the query order)
+    }
     for (int e = threadIdx.x; e < n; e += blockDim.x) {
       double sh_, ch_;
       sincos(q.h[s0 + e], &sh_, &ch_);

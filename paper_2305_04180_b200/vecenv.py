@@ -355,6 +355,17 @@ class VecEnv:
         self._last_states = out.states
         return out
 
+    def new_batch(self) -> StepBatch:
+        """Device output tensors for ``step_batch(actions, out=...)``."""
+        torch = self._torch
+        n, d, dev = self.n_copies, self.state_dim, self.device
+        return StepBatch(torch.empty((n, d), dtype=torch.float32, device=dev),
+                         torch.empty(n, dtype=torch.float64, device=dev),
+                         torch.empty(n, dtype=torch.bool, device=dev),
+                         torch.empty(n, dtype=torch.bool, device=dev),
+                         torch.empty((n, d), dtype=torch.float32, device=dev),
+                         torch.empty(n, dtype=torch.int8, device=dev))
+
     def host_buffers(self) -> "HostStep":
         """Page-locked host buffers for ``step_host``. The outputs are views into
         one flat block in ``sp_env_step_host``'s layout (include/sparrow.h)."""

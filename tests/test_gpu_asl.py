@@ -352,3 +352,65 @@ def test_update_from_samples_inside_the_graph():
         assert sg.loss == sh.loss and sg.version == sh.version
     for w, wh in zip(gl.online.weights + gl.online.biases, hl.online.weights + hl.online.biases):
         assert torch.equal(w, wh)
+
+
+@pytest.mark.parametrize("n,t_step,env0,n_envs", [(4096, 100, 0, 4096), (4096, 499_999, 0, 4096),
+                                                   (1000, 10**7, 3000, 4096), (37, 0, 0, 37)])
+def test_fused_actor_matches_reference(n, t_step, env0, n_envs):
+    """sp_actor_select (one launch: forward, device VEM epsilons, epsilon-greedy)
+    against the unmodified reference: net.forward (Q within 1e-5), VEM
+    epsilons of copies env0.. at t_step, select_actions on the same Philox
+    draws -- actions identical wherever the reference's top two Q-values are
+    not within fp32 summation-order noise (1e-5) of each other."""
+    ref()
+    import torch
+    from color_rl import net
+    from color_rl.asl.vem import VemSchedule as RV, select_actions as ref_select
+    from paper_2305_04180_b200.asl import QNet, VemSchedule, select_actions_fused
+    p_ref = net.init_params(np.random.default_rng(3), SIZES)
+    p = QNet.init(np.random.default_rng(3), SIZES)
+    x = np.random.default_rng(n + t_step).standard_normal((n, 37)).astype(np.float32)
+    kw = dict(or_init=min(16, n_envs), or_final=min(3, n_envs), decay_steps=500_000)
+    q_ref = net.forward(p_ref, x)
+    eps = RV(n_envs, **kw).epsilons(t_step)[env0:env0 + n]
+    want = ref_select(q_ref, eps, PhiloxStream(9, 0xAC, tag=3))
+    g = PhiloxStream(9, 0xAC, tag=3)
+    q = torch.empty((n, 5), dtype=torch.float32, device="cuda")
+    got = select_actions_fused(p, torch.from_numpy(x).cuda(), VemSchedule(n_envs, **kw), t_step, g,
+                               env0=env0, q_out=q).cpu().numpy()
+    assert g.ctr == 2 * n
+    np.testing.assert_allclose(q.cpu().numpy(), q_ref, rtol=1e-5, atol=1e-5)
+    top2 = np.sort(q_ref, axis=1)[:, -2:]
+    clear = (top2[:, 1] - top2[:, 0]) > 1e-5
+    assert clear.mean() > 0.99
+    assert np.array_equal(got[clear], want[clear])
+
+
+def test_fused_actor_equals_torch_path_and_explores():
+    """The fused kernel against this package's own torch path (QNet.forward +
+    select_actions with host epsilons): same draws, same actions away from
+    near-ties; at e_min = e_max = 1 every action is the random draw."""
+    import torch
+    from paper_2305_04180_b200.asl import QNet, VemSchedule, select_actions, select_actions_fused
+    from paper_2305_04180_b200.replay import PhiloxGenerator
+    p = QNet.init(np.random.default_rng(5), SIZES)
+    n = 65536
+    x = torch.randn((n, 37), generator=torch.Generator().manual_seed(0)).cuda()
+    vem = VemSchedule(n)
+    q = p.forward(x)
+    g1, g2 = PhiloxGenerator(4, 0xAC), PhiloxGenerator(4, 0xAC)
+    g1.tag = g2.tag = 3
+    want = select_actions(q, vem.epsilons(1234), g1).cpu().numpy()
+    got = select_actions_fused(p, x, vem, 1234, g2).cpu().numpy()
+    assert g1.ctr == g2.ctr
+    qs = torch.sort(q, dim=1).values
+    clear = ((qs[:, -1] - qs[:, -2]) > 1e-5).cpu().numpy()
+    assert np.array_equal(got[clear], want[clear])
+    allr = VemSchedule(n, e_min=1.0, e_max=1.0)
+    g3, g4 = PhiloxGenerator(4, 0xAC), PhiloxGenerator(4, 0xAC)
+    g3.tag = g4.tag = 3
+    got = select_actions_fused(p, x, allr, 0, g3).cpu().numpy()
+    from paper_2305_04180_b200.asl import philox_fill
+    philox_fill(n, g4, 0, 0.0, 1.0)
+    rnd = philox_fill(n, g4, 1, 0, 5).cpu().numpy()
+    assert np.array_equal(got, rnd)

@@ -49,6 +49,54 @@ def run_ours(seconds, eager=False, learner="fused"):
     return sharer, wall
 
 
+def run_actor(iters=300, fused=True):
+    """The actor's iteration alone (no learner): forward + VEM + selection,
+    env step, ring append, 4096 envs -- sp_actor_select (fused) against the
+    torch path (addmm forward, host VEM epsilons, philox draws, argmax)."""
+    import torch
+    from helpers import config, load_maps, ranges
+    from paper_2305_04180_b200 import ReplayBuffer, VecEnv
+    from paper_2305_04180_b200.asl import QNet, VemSchedule, select_actions, select_actions_fused
+    from paper_2305_04180_b200.replay import PhiloxGenerator
+    env = VecEnv(load_maps(16), N, ranges(0.3), config(32), check_actions=False)
+    states = env.reset_all(0)
+    p = QNet.init(np.random.default_rng(0), (37, 256, 128, 5))
+    rb = ReplayBuffer(CAP, 37)
+    vem = VemSchedule(N)
+    g = PhiloxGenerator(0, 0xAC)
+    g.tag = 3
+    outs = [env.new_batch(), env.new_batch()]
+    acts = [torch.empty(N, dtype=torch.int64, device=env.device) for _ in range(2)]
+    t_step = 0
+
+    def it(k):
+        nonlocal states, t_step
+        if fused:
+            a = select_actions_fused(p, states, vem, t_step, g, out=acts[k & 1])
+        else:
+            a = select_actions(p.forward(states), vem.epsilons(t_step), g)
+        b = outs[k & 1]
+        env.step_device(a.data_ptr(), b)
+        rb.append_batch(states, a, b.rewards, b.store_states, b.dones)
+        states = b.states
+        t_step += N
+    for k in range(20):
+        it(k)
+    torch.cuda.synchronize()
+    s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    s_.record()
+    for k in range(iters):
+        it(k)
+    e_.record()
+    e_.synchronize()
+    wall = time.perf_counter() - w0
+    dev_s = s_.elapsed_time(e_) / 1e3
+    return {"mode": "actor only (no learner), " + ("sp_actor_select" if fused else "torch path"),
+            "iters": iters, "us_per_iter_device": dev_s / iters * 1e6,
+            "us_per_iter_wall": wall / iters * 1e6, "env_steps_per_s": N * iters / wall}
+
+
 def run_reference(seconds):
     from oracle import oracle as O
     O.import_reference(37)
@@ -88,7 +136,13 @@ def main():
     ap.add_argument("--eager", action="store_true", help="learner updates without CUDA graph")
     ap.add_argument("--learner", default="fused", choices=["fused", "torch"],
                     help="fused sp_ddqn_update kernels or the torch update")
+    ap.add_argument("--actor-only", action="store_true",
+                    help="time the actor iteration alone, fused kernel vs the torch path")
     a = ap.parse_args()
+    if a.actor_only:
+        for fused in (True, False):
+            print(json.dumps(run_actor(fused=fused)))
+        return
     if a.impl == "ours":
         sharer, wall = run_ours(a.seconds, a.eager, a.learner)
     else:
