@@ -366,8 +366,25 @@ def replay_bench(dev, flush_l2, peak_gbs, reps=7):
             ms.append(s_.elapsed_time(e_))
         t = statistics.median(ms) / 1e3
         gbs = 2 * row_bytes * n / t / 1e9
-        res["append"].append({"rows_per_call": n, "us": t * 1e6, "rows_per_s": n / t,
-                              "achieved_gbs": gbs, "peak_gbs": peak_gbs, "frac": gbs / peak_gbs})
+        row = {"rows_per_call": n, "us": t * 1e6, "rows_per_s": n / t,
+               "achieved_gbs": gbs, "peak_gbs": peak_gbs, "frac": gbs / peak_gbs,
+               "timing": "one call between CUDA events (includes the launch latency)"}
+        if n >= 65_536:  # streaming: a full ring pass of back-to-back calls
+            calls = C // n
+            flush_l2(99)
+            s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s_.record(stream)
+            for _ in range(calls):
+                append()
+            e_.record(stream)
+            e_.synchronize()
+            ts = s_.elapsed_time(e_) / 1e3
+            sg = 2 * row_bytes * n * calls / ts / 1e9
+            row["stream"] = {"calls": calls, "rows": n * calls, "us_per_call": ts / calls * 1e6,
+                             "achieved_gbs": sg, "frac": sg / peak_gbs,
+                             "timing": "calls back to back between one pair of events "
+                                       "(a whole 1M-row ring pass; > L2)"}
+        res["append"].append(row)
     B = 256
     out = [torch.empty((B, D), device=dev), torch.empty(B, dtype=torch.int64, device=dev),
            torch.empty(B, device=dev), torch.empty((B, D), device=dev),

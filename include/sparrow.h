@@ -147,6 +147,10 @@ int sp_env_recent_returns_keyed(SpEnv* env, double* out256, uint64_t* keys256, i
 int sp_env_stats_reset(SpEnv* env, int clear_recent, void* stream);
 /* device totals {episodes, arrivals, return_sum} as 3 doubles (all-reduce payload) */
 int sp_env_stats_totals(SpEnv* env, double* dev_out3, void* stream);
+/* Lanes whose first episode since reset_all has not ended (first_event < 0;
+ * the latch behind first_episode_outcomes, vecenv.py:134-141): a device
+ * count and one 8-byte read; synchronizes `stream`. */
+int sp_env_first_pending(SpEnv* env, int64_t* host_count, void* stream);
 
 /* read one SoA field, external env order, into a host array of n_envs doubles.
  * field: 0 x, 1 y, 2 heading, 3 v_linear, 4 v_angular, 5 start_x, 6 start_y,

@@ -80,6 +80,7 @@ SIGNATURES = [
     ("sp_env_step_host", ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     ("sp_env_set_recording", ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     ("sp_env_read_fifo", ctypes.c_int, [c_vp, c_vp, c_vp]),
+    ("sp_env_first_pending", ctypes.c_int, [c_vp, c_vp, c_vp]),
     ("sp_env_check", ctypes.c_int, [c_vp, c_vp, c_i64p]),
     ("sp_env_any_needs_reset", ctypes.c_int, [c_vp, c_vp, c_i32p]),
     ("sp_env_stats_read", ctypes.c_int, [c_vp, c_i64p, c_i64p, c_dp, c_i8p, c_dp, c_i64p, c_vp]),

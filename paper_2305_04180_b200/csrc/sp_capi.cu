@@ -42,6 +42,10 @@ constexpr int kMaxWarps = SP_CTA_THREADS / 32;
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+int grid_for(int64_t n, int block) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + block - 1) / block, 148 * 16));
+}
+
 struct DevDeviceGuard {
   int prev = -1;
   explicit DevDeviceGuard(int dev) {
@@ -128,6 +132,7 @@ struct SpEnv {
   int32_t* rec_hit_store = nullptr;
   int32_t* rec_hit_state = nullptr;
   double* rec_scan_state = nullptr;
+  unsigned long long* d_count = nullptr;  // sp_env_first_pending scratch
   std::mutex mu;
 
   template <class T>
@@ -789,6 +794,28 @@ int sp_env_stats_reset(SpEnv* env, int clear_recent, void* stream) {
   return SP_OK;
 }
 
+int sp_env_first_pending(SpEnv* env, int64_t* host_count, void* stream) {
+  if (!env || !host_count) return fail(SP_EINVAL, "null argument");
+  DevDeviceGuard guard(env->device);
+  std::lock_guard<std::mutex> lk(env->mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!env->d_count) {
+    unsigned long long* p = nullptr;
+    const int rc = env->alloc(&p, 1);
+    if (rc != SP_OK) return rc;
+    env->d_count = p;
+  }
+  SP_CUDA(cudaMemsetAsync(env->d_count, 0, 8, st));
+  count_pending_kernel<<<grid_for(env->n, 256), 256, 0, st>>>(env->d.first_event, env->n,
+                                                              env->d_count);
+  SP_CUDA(cudaGetLastError());
+  unsigned long long h = 0;
+  SP_CUDA(cudaMemcpyAsync(&h, env->d_count, 8, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  *host_count = (int64_t)h;
+  return SP_OK;
+}
+
 int sp_env_stats_totals(SpEnv* env, double* dev_out3, void* stream) {
   if (!env || !dev_out3) return fail(SP_EINVAL, "null argument");
   DevDeviceGuard guard(env->device);
@@ -952,9 +979,6 @@ int sp_env_scan(SpEnv* env, int64_t n, const int64_t* query_offsets, const doubl
 }
 
 // ------------------------------------------------------------- op seam ----
-static int grid_for(int64_t n, int block) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>((n + block - 1) / block, 148 * 16));
-}
 
 int sp_cast_rays(const uint8_t* occ, const double* edt, int64_t n_maps, int64_t height,
                  int64_t width, const int64_t* map_idx, const double* px, const double* py,

@@ -294,6 +294,17 @@ __global__ void philox_fill_kernel(int64_t n, uint64_t seed, uint32_t lane, uint
   }
 }
 
+// Lanes whose first episode has not ended yet (first_event < 0), into *out.
+__global__ void count_pending_kernel(const int8_t* __restrict__ first_event, int64_t n,
+                                     unsigned long long* __restrict__ out) {
+  unsigned long long c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += first_event[i] < 0;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(SP_FULL, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
 // Deterministic single-CTA totals {episodes, arrivals, return_sum}.
 __global__ void stats_totals_kernel(const int64_t* __restrict__ eps,
                                     const int64_t* __restrict__ arr,

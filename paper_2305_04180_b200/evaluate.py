@@ -7,10 +7,10 @@ stay at their nominal values unless a randomization fraction is requested.
 Timeouts count as failures. The first-episode latch is kept by the step
 kernel (``first_event/first_return/first_steps``, ``vecenv.py:134-141``).
 
-The per-step loop runs on the device. The Q-net forward goes through cuBLAS,
-the greedy argmax through torch (ties resolve to the lowest index, as
-``np.argmax`` does), and the step is one fused launch. No host round trip
-happens except the done-check, which reads the latched first-event column
+The per-step loop runs on the device: the fused actor kernel (Q-net forward
++ argmax, ties to the lowest index as ``np.argmax``) and the fused env step,
+``check_every`` steps per CUDA graph replay. No host round trip happens
+except the done-check, which reads one count of still-running first episodes
 every ``check_every`` steps. Outcomes are latched, so stepping past the
 moment every copy has finished cannot change the report. The loop therefore
 gives the same report as the reference's check-every-step loop
@@ -117,19 +117,52 @@ def _map_seed(seed: int, mi: int) -> int:
     return int(np.random.SeedSequence((seed, mi)).generate_state(1)[0])  # evaluate.py:98
 
 
-def _rollout(env: VecEnv, net, seed: int, horizon: int, check_every: int):
+def _rollout(env: VecEnv, net, seed: int, horizon: int, check_every: int, graph: bool = True):
     """Greedy first-episode rollout of every copy (evaluate.py:98-106).
-    Returns the per-copy (first_event, first_return, first_steps) arrays."""
+    Returns the per-copy (first_event, first_return, first_steps) arrays.
+
+    With ``graph`` (default) a step is the fused actor kernel with exploration
+    off (sp_actor_select: forward + argmax, ties to the lowest index) and the
+    fused env step, and ``check_every`` (rounded up to even) such steps are
+    one CUDA graph replay, outputs alternating between two buffer sets inside
+    it.  Between replays the host reads one count (copies still in their first
+    episode).  Outcomes are latched, so the steps past the last finish change
+    nothing.  ``graph=False``: cuBLAS forward + torch argmax, one step at a
+    time."""
     import torch
     states = env.reset_all(seed)
-    done_steps = 0
-    for k in range(horizon):
-        with torch.no_grad():
-            actions = torch.argmax(net.forward(states), dim=1)
-        states = env.step_batch(actions).states
-        done_steps = k + 1
-        if done_steps % check_every == 0 and env.all_first_episodes_done:
-            break
+    if not graph:
+        for k in range(horizon):
+            with torch.no_grad():
+                actions = torch.argmax(net.forward(states), dim=1)
+            states = env.step_batch(actions).states
+            if (k + 1) % check_every == 0 and env.all_first_episodes_done:
+                break
+    else:
+        from .asl import VemSchedule, select_actions_fused
+        from .replay import PhiloxGenerator
+        n = env.n_copies
+        greedy = VemSchedule(n, or_init=1, or_final=1, e_min=0.0, e_max=0.0)
+        rng = PhiloxGenerator(0, 0)  # draws made but never used: eps = 0
+        outs = [env.new_batch(), env.new_batch()]
+        acts = torch.empty(n, dtype=torch.int64, device=env.device)
+        outs[1].states.copy_(states)
+        k_graph = check_every + (check_every & 1)
+        select_actions_fused(net, outs[1].states, greedy, 0, rng, out=acts)  # warm the kernel
+        side = torch.cuda.Stream(env.device)
+        side.wait_stream(torch.cuda.current_stream(env.device))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            for i in range(k_graph):
+                select_actions_fused(net, outs[(i + 1) & 1].states, greedy, 0, rng, out=acts)
+                env.step_device(acts.data_ptr(), outs[i & 1])
+        done = 0
+        while done < horizon:
+            g.replay()
+            done += k_graph
+            if env.first_pending() == 0:
+                break
+        torch.cuda.current_stream(env.device).wait_stream(side)
     st = env._per_copy_arrays()
     if (st["first_event"] < 0).any():
         raise RuntimeError("evaluation episodes did not finish within the timeout")
@@ -151,7 +184,8 @@ def _map_eval(name, events, returns, steps) -> MapEval:
 def evaluate_params(params, maps, names, episodes_per_map: int, seed: int,
                     config: EnvConfig | None = None, nominal: SimParams | None = None,
                     randomize_fraction: float = 0.0, kernel_backend=None, *,
-                    device=None, fused: bool = False, check_every: int = 8) -> EvalReport:
+                    device=None, fused: bool = False, check_every: int = 8,
+                    graph: bool = True) -> EvalReport:
     """evaluate.py:88-123. ``params`` is a QNet, or anything with the
     reference's ``weights``/``biases`` lists (MlpParams)."""
     config = config or EnvConfig()
@@ -167,7 +201,7 @@ def evaluate_params(params, maps, names, episodes_per_map: int, seed: int,
         midx = np.repeat(np.arange(len(maps)), episodes_per_map)
         env = VecEnv(maps, n, ranges, config, map_index=midx, kernel_backend=kernel_backend,
                      device=device, check_actions=False)
-        ev, rt, sp = _rollout(env, net, _map_seed(seed, 0), horizon, check_every)
+        ev, rt, sp = _rollout(env, net, _map_seed(seed, 0), horizon, check_every, graph)
         for mi, name in enumerate(names):
             sl = slice(mi * episodes_per_map, (mi + 1) * episodes_per_map)
             report.results.append(_map_eval(name, ev[sl], rt[sl], sp[sl]))
@@ -175,7 +209,7 @@ def evaluate_params(params, maps, names, episodes_per_map: int, seed: int,
     for mi, (grid_map, name) in enumerate(zip(maps, names)):
         env = VecEnv([grid_map], episodes_per_map, ranges, config,
                      kernel_backend=kernel_backend, device=device, check_actions=False)
-        ev, rt, sp = _rollout(env, net, _map_seed(seed, mi), horizon, check_every)
+        ev, rt, sp = _rollout(env, net, _map_seed(seed, mi), horizon, check_every, graph)
         report.results.append(_map_eval(name, ev, rt, sp))
     return report
 

@@ -575,7 +575,15 @@ class VecEnv:
 
     @property
     def all_first_episodes_done(self) -> bool:
-        return bool((self._per_copy_arrays()["first_event"] >= 0).all())
+        return self.first_pending() == 0
+
+    def first_pending(self) -> int:
+        """Copies whose first episode since reset_all is still running: a
+        device count and one 8-byte read (``sp_env_first_pending``)."""
+        c = ctypes.c_int64(0)
+        _lib.check(self._lib.sp_env_first_pending(self._h, ctypes.byref(c), self._stream()),
+                   "first_pending")
+        return int(c.value)
 
     @property
     def sim(self) -> SimView:

@@ -144,3 +144,19 @@ def test_fused_layout_matches_oracle_rollout():
         assert r.timeouts == int((fe[sl] == 3).sum())
         assert r.mean_steps == float(np.mean(fs[sl]))
         np.testing.assert_allclose(r.mean_return, np.mean(fr[sl]), rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_graphed_rollout_equals_stepwise(fused):
+    """The CUDA-graph rollout (fused actor kernel with exploration off + env
+    step, check_every steps per replay) gives the step-by-step cuBLAS/argmax
+    rollout's report."""
+    from paper_2305_04180_b200.evaluate import evaluate_params
+    from paper_2305_04180_b200.sim import EnvConfig, LidarConfig
+    maps = load_maps(4)
+    cfg = EnvConfig(lidar=LidarConfig(n_beams=32), timeout_steps=200)
+    p = _params(3, (37, 256, 128, 5))
+    kw = dict(config=cfg, fused=fused, check_every=5)
+    a = evaluate_params(p, maps, [f"m{i}" for i in range(4)], 64, seed=2, graph=True, **kw)
+    b = evaluate_params(p, maps, [f"m{i}" for i in range(4)], 64, seed=2, graph=False, **kw)
+    assert a.to_dict() == b.to_dict()

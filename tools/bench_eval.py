@@ -42,9 +42,23 @@ def run_ours(episodes, fused):
     rep = evaluate_params(p, maps, names, episodes, seed=1, config=cfg, fused=fused)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
-    return {"impl": "ours", "fused": fused, "episodes": rep.episodes, "wall_s": wall,
-            "episodes_per_s": rep.episodes / wall, "arrival_rate": rep.arrival_rate,
-            "mean_steps": float(np.mean([r.mean_steps for r in rep.results]))}
+    out = {"impl": "ours", "fused": fused, "episodes": rep.episodes, "wall_s": wall,
+           "episodes_per_s": rep.episodes / wall, "arrival_rate": rep.arrival_rate,
+           "mean_steps": float(np.mean([r.mean_steps for r in rep.results]))}
+    # share of the wall time spent in the step kernel (torch profiler / CUPTI)
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+        t0 = time.perf_counter()
+        evaluate_params(p, maps, names, episodes, seed=1, config=cfg, fused=fused)
+        torch.cuda.synchronize()
+        wall_p = time.perf_counter() - t0
+    step_us = sum(e.device_time_total for e in prof.key_averages()
+                  if "env_step_kernel" in e.key)
+    actor_us = sum(e.device_time_total for e in prof.key_averages() if "actor_kernel" in e.key)
+    out["step_kernel_share_of_wall"] = step_us / 1e6 / wall_p
+    out["actor_kernel_share_of_wall"] = actor_us / 1e6 / wall_p
+    out["profiled_wall_s"] = wall_p
+    return out
 
 
 def run_reference(episodes):
