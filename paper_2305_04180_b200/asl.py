@@ -125,47 +125,61 @@ class QNet:
         return self.forward_cached(states)[0][-1]
 
     # -- checkpoints (net.py:178-228) ----------------------------------------
+    # The COLORNET byte layout is the reference's (little-endian): magic,
+    # u32 format version, u32 layer count, u32 sizes, then per layer the f32
+    # weights (fan_in, fan_out) and f32 biases, then the u64 version.  Here the
+    # whole parameter payload crosses PCIe once each way: the device tensors
+    # are concatenated on the GPU and read back in one copy; loading validates
+    # the header and the exact payload length first, then uploads one buffer
+    # and splits it into per-layer views.
     def to_bytes(self) -> bytes:
-        buf = io.BytesIO()
-        buf.write(CHECKPOINT_MAGIC)
+        torch = _torch()
         sizes = self.sizes
-        buf.write(struct.pack("<II", CHECKPOINT_FORMAT_VERSION, len(sizes)))
-        buf.write(struct.pack(f"<{len(sizes)}I", *sizes))
-        for w, b in zip(self.weights, self.biases):
-            buf.write(np.ascontiguousarray(w.cpu().numpy(), dtype="<f4").tobytes())
-            buf.write(np.ascontiguousarray(b.cpu().numpy(), dtype="<f4").tobytes())
-        buf.write(struct.pack("<Q", self.version))
-        return buf.getvalue()
+        head = CHECKPOINT_MAGIC + np.array([CHECKPOINT_FORMAT_VERSION, len(sizes), *sizes],
+                                           dtype="<u4").tobytes()
+        flat = torch.cat([t.reshape(-1) for pair in zip(self.weights, self.biases) for t in pair])
+        return (head + flat.cpu().numpy().astype("<f4", copy=False).tobytes()
+                + np.array([self.version], dtype="<u8").tobytes())
 
     @classmethod
     def from_bytes(cls, data: bytes, expect_sizes=None, device=None) -> "QNet":
-        buf = io.BytesIO(data)
+        torch = _torch()
+        view = memoryview(data)
+        pos = 0
 
-        def read(n, what):
-            chunk = buf.read(n)
-            if len(chunk) != n:
+        def take(n, what):
+            nonlocal pos
+            if pos + n > len(view):
                 raise CheckpointError(f"truncated checkpoint while reading {what}")
-            return chunk
+            out = view[pos:pos + n]
+            pos += n
+            return out
 
-        if read(len(CHECKPOINT_MAGIC), "magic") != CHECKPOINT_MAGIC:
+        if bytes(take(len(CHECKPOINT_MAGIC), "magic")) != CHECKPOINT_MAGIC:
             raise CheckpointError("bad magic bytes; not a COLORNET checkpoint")
-        fmt, n_sizes = struct.unpack("<II", read(8, "header"))
+        fmt, n_sizes = (int(v) for v in np.frombuffer(take(8, "header"), dtype="<u4"))
         if fmt != CHECKPOINT_FORMAT_VERSION:
             raise CheckpointError(f"unsupported checkpoint format version {fmt}")
         if not 2 <= n_sizes <= 64:
             raise CheckpointError(f"implausible layer count {n_sizes}")
-        sizes = struct.unpack(f"<{n_sizes}I", read(4 * n_sizes, "layer sizes"))
-        if expect_sizes is not None and tuple(sizes) != tuple(expect_sizes):
-            raise CheckpointError(f"layer sizes {tuple(sizes)} do not match {tuple(expect_sizes)}")
-        ws, bs = [], []
-        for fan_in, fan_out in zip(sizes[:-1], sizes[1:]):
-            ws.append(np.frombuffer(read(4 * fan_in * fan_out, "weights"), "<f4")
-                      .reshape(fan_in, fan_out).copy())
-            bs.append(np.frombuffer(read(4 * fan_out, "biases"), "<f4").copy())
-        (version,) = struct.unpack("<Q", read(8, "version"))
-        if buf.read(1):
+        sizes = tuple(int(v) for v in np.frombuffer(take(4 * n_sizes, "layer sizes"), dtype="<u4"))
+        if expect_sizes is not None and sizes != tuple(expect_sizes):
+            raise CheckpointError(f"layer sizes {sizes} do not match {tuple(expect_sizes)}")
+        shapes = [(a, b) for a, b in zip(sizes[:-1], sizes[1:])]
+        n_floats = sum(a * b + b for a, b in shapes)
+        payload = np.frombuffer(take(4 * n_floats, "weights and biases"), dtype="<f4")
+        (version,) = (int(v) for v in np.frombuffer(take(8, "version"), dtype="<u8"))
+        if pos != len(view):
             raise CheckpointError("trailing bytes after checkpoint payload")
-        return cls.from_numpy(ws, bs, version, device)
+        dev = _lib.require_cuda(device)
+        flat = torch.from_numpy(payload.astype(np.float32)).to(dev)  # one upload
+        ws, bs, off = [], [], 0
+        for a, b in shapes:
+            ws.append(flat[off:off + a * b].view(a, b).clone())
+            off += a * b
+            bs.append(flat[off:off + b].clone())
+            off += b
+        return cls(ws, bs, version)
 
 
 def huber_residual_grad(residual):
@@ -665,6 +679,10 @@ def select_actions_fused(params: QNet, states, vem: VemSchedule, t_step: int, rn
 
 @dataclass(frozen=True)
 class TfmConfig:
+    """Time-feedback pacing targets (asl/tfm.py:15-29): n_envs interactions
+    per actor period, batch_size samples per learner update, and the target
+    transitions-per-sample ratio tps; rho = n_envs * tps / batch_size is the
+    learner updates one actor period should take."""
     n_envs: int
     tps: float
     batch_size: int
@@ -676,31 +694,47 @@ class TfmConfig:
             raise ValueError("n_envs, batch_size must be >= 1 and tps > 0")
 
     @property
-    def rho(self) -> float:  # tfm.py:27-29
+    def rho(self) -> float:
         return self.n_envs * self.tps / self.batch_size
 
 
-@dataclass
-class TfmState:  # tfm.py:32-77
-    ema_factor: float = 0.1
-    v_period_s: float | None = None
-    b_period_s: float | None = None
-    v_count: int = 0
-    b_count: int = 0
+class TfmState:
+    """Time-feedback modulation (asl/tfm.py:32-77, paper Alg. 1).
+
+    Keeps exponential moving averages (weight ``ema_factor`` on the newest
+    sample, the first sample taken as is) of the actor's interaction period
+    and the learner's update period.  Here the periods are device times: the
+    actor loop feeds the CUDA-event time between its iteration-end events
+    (``record_interaction_events``), so the pacing sees the GPU's work, not
+    the host's enqueue time.  With xi = rho * T_update - T_interaction, the
+    faster side sleeps: the actor for xi when xi > 0, the learner for
+    -xi / rho otherwise, each capped at max_sleep_s, and neither before both
+    averages hold warmup_samples samples."""
+
+    def __init__(self, ema_factor: float = 0.1):
+        self.ema_factor = float(ema_factor)
+        self.v_period_s = None  # actor interaction period (s), EMA
+        self.b_period_s = None  # learner update period (s), EMA
+        self.v_count = 0
+        self.b_count = 0
+
+    def _fold(self, avg, x):
+        return x if avg is None else (1.0 - self.ema_factor) * avg + self.ema_factor * x
 
     def record_interaction(self, seconds: float) -> None:
-        self.v_period_s = self._ema(self.v_period_s, seconds)
+        self.v_period_s = self._fold(self.v_period_s, seconds)
         self.v_count += 1
 
     def record_optimization(self, seconds: float) -> None:
-        self.b_period_s = self._ema(self.b_period_s, seconds)
+        self.b_period_s = self._fold(self.b_period_s, seconds)
         self.b_count += 1
 
-    def _ema(self, prev, sample):
-        return sample if prev is None else (1.0 - self.ema_factor) * prev + self.ema_factor * sample
+    def record_interaction_events(self, start, end) -> None:
+        """An interaction period measured on the device (two CUDA events)."""
+        self.record_interaction(start.elapsed_time(end) / 1e3)
 
     def ready(self, cfg: TfmConfig) -> bool:
-        return self.v_count >= cfg.warmup_samples and self.b_count >= cfg.warmup_samples
+        return min(self.v_count, self.b_count) >= cfg.warmup_samples
 
     def compute_xi(self, cfg: TfmConfig) -> float:
         if self.v_period_s is None or self.b_period_s is None:
@@ -848,7 +882,7 @@ def actor_loop(sharer: Sharer, vec_env, initial_states, params: QNet, vem: VemSc
                 if len(ends) >= 3:  # bounded run-ahead: wait for iteration k - 2
                     ends[-3].synchronize()
                 while len(ends) >= 2 and ends[1].query():
-                    sharer.tfm.record_interaction(ends[0].elapsed_time(ends[1]) / 1e3)
+                    sharer.tfm.record_interaction_events(ends[0], ends[1])
                     ends.popleft()
                 snap = sharer.fetch_params(version)
                 if snap is not None:

@@ -5,7 +5,7 @@ bordered square arena with rectangular obstacle blocks, a spawn square in the
 lower-left corner and a goal disc in the upper-right one. Map generation is
 offline, one-time CPU work, so it stays on the host (numpy + scipy) and feeds
 ``GridMap``. The device tables are built from the GridMap at VecEnv creation
-(block table + bitmap, ``sp_capi.cu build_block_table``).
+(per-cell free-box table + bitmap, ``sp_capi.cu build_cell_table``).
 
 Determinism contract: the same ``numpy.random.Generator`` consumes the same
 draws in the same order as the reference. Per block attempt that is

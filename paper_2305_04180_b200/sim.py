@@ -200,7 +200,7 @@ class GridMap:
     def edt_cells(self) -> np.ndarray:
         """Euclidean distance (cell units, centre to centre) to the nearest
         occupied cell (gridmap.py:62-71). The device path does not use it: the
-        marcher skips free space with its own chessboard block table. It is
+        marcher skips free space with its own per-cell free-box table. It is
         kept for API parity and computed once on first use."""
         if getattr(self, "_edt", None) is None:
             from scipy import ndimage
