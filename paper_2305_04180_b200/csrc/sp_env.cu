@@ -275,7 +275,10 @@ __device__ __forceinline__ double ray_end(const Ray& r, const MapView& mv, const
   const bool occ = ((const int8_t*)mv.blk)[r.v * r.ayw + r.u * r.ax + r.kb] < 0;
   hit = occ ? iy * d.W + ix : -1;
   if (!occ) return d.max_range;
-  const double te = fmax(((double)r.u - r.X) * r.IDX, ((double)r.v - r.Y) * r.IDY);
+  // plain selects, not fmax: no NaN handling needed (a 0 * inf entry term of
+  // an axis-parallel ray compares false and drops out, as fmax would drop it)
+  const double eu = ((double)r.u - r.X) * r.IDX, ev = ((double)r.v - r.Y) * r.IDY;
+  const double te = eu > ev ? eu : ev;
   return te > 0.0 ? te : 0.0;
 }
 
@@ -307,15 +310,24 @@ __device__ __forceinline__ bool ray_setup(Ray& r, double x0, double y0, double c
 // cap .. cap+extra-1 are post-reset scans of envs that finished this step.
 // A scan's R beams form up to 8 "beam groups" of gb = 2^gshift consecutive
 // beams (EnvDev::gshift); the ray queue dispatches (slot, group) entries.
+// One scan slot's record (80 B: every field at an immediate offset of one
+// base address, the 16-byte pairs loaded as 128-bit words; the 20-word stride
+// spreads 8 consecutive slots over disjoint banks).
+struct SlotRec {
+  double px, py;   // scan origin (cm)
+  double ch, sh;   // heading cos / sin
+  double sig;      // noise std (cm)
+  float* out0;     // the output row its scan fills (noise z parks there first)
+  float* out1;     // a second row that receives the same values, or null
+  uint64_t qacc;   // byte g = OR of 1 << step_level(steps) over group g's rays
+  uint64_t nctr;   // first Philox block of the slot's LiDAR noise
+  uint64_t qpred;  // the qacc bytes of the lane's last scan (dispatch prediction)
+};
+
 struct Chunk {
-  double *px, *py, *ch, *sh, *sig;  // per slot: scan origin, heading cos/sin, noise std
-  uint64_t* nctr;  // per slot: first Philox block of the slot's LiDAR noise
-  uint64_t* qacc;  // per slot: byte g = OR of 1 << step_level(steps) over group g's rays
-  uint64_t* qpred; // per slot: the same bytes from the lane's last scan (prediction)
+  SlotRec* rec;    // per slot
   double* retp;    // per env: episode return before this step (prefetched in phase A)
   double* part;    // per env: shaped reward without its proximity term
-  float** out0;    // per slot: the output row its scan fills (noise z parks there first)
-  float** out1;    // per slot: a second row that receives the same values, or null
   uint32_t* gid;   // per slot: the env's stream lane (global env id)
   int32_t* reg;    // slots in registration order
   int32_t* hwrite; // per slot: global slot whose history this scan refreshes, or -1
@@ -332,19 +344,10 @@ struct Chunk {
 
 __device__ __forceinline__ Chunk chunk_smem(uint8_t* base, int cap, int slots) {
   Chunk c;
-  c.px = (double*)base;
-  c.py = c.px + slots;
-  c.ch = c.py + slots;
-  c.sh = c.ch + slots;
-  c.sig = c.sh + slots;
-  c.nctr = (uint64_t*)(c.sig + slots);
-  c.qacc = c.nctr + slots;
-  c.qpred = c.qacc + slots;
-  c.retp = (double*)(c.qpred + slots);
+  c.rec = (SlotRec*)base;
+  c.retp = (double*)(c.rec + slots);
   c.part = c.retp + cap;
-  c.out0 = (float**)(c.part + cap);
-  c.out1 = c.out0 + slots;
-  c.gid = (uint32_t*)(c.out1 + slots);
+  c.gid = (uint32_t*)(c.part + cap);
   c.reg = (int32_t*)(c.gid + slots);
   c.hwrite = c.reg + slots;
   c.xslot = c.hwrite + slots;
@@ -446,7 +449,7 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
         const int my_b = base + na + __popc(ib & lt);
         if (fin_a && my_a < total && (ja = beam_of(c, my_a, gs, ea)) < R) {
           za = fin.pre(ea, ja);
-          if (ray_setup(ra, c.px[ea], c.py[ea], c.ch[ea], c.sh[ea], beam[ja], d)) {
+          if (ray_setup(ra, c.rec[ea].px, c.rec[ea].py, c.rec[ea].ch, c.rec[ea].sh, beam[ja], d)) {
             fin(ea, ja, 0.0, -1, 1, za);  // origin outside the grid: range 0 (_cy.pyx:37-39)
             ray_park(ra);
           } else {
@@ -456,7 +459,7 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
         }
         if (fin_b && my_b < total && (jb = beam_of(c, my_b, gs, eb)) < R) {
           zb = fin.pre(eb, jb);
-          if (ray_setup(rb, c.px[eb], c.py[eb], c.ch[eb], c.sh[eb], beam[jb], d)) {
+          if (ray_setup(rb, c.rec[eb].px, c.rec[eb].py, c.rec[eb].ch, c.rec[eb].sh, beam[jb], d)) {
             fin(eb, jb, 0.0, -1, 1, zb);
             ray_park(rb);
           } else {
@@ -493,7 +496,7 @@ __device__ __forceinline__ void store_history(const EnvDev& d, const Chunk& c, i
   for (int k = threadIdx.x; k < n_slots; k += blockDim.x) {
     const int slot = c.reg[k];
     const int hw = c.hwrite[slot];
-    if (hw >= 0) d.qhist[hw] = c.qacc[slot];
+    if (hw >= 0) d.qhist[hw] = c.rec[slot].qacc;
   }
 }
 
@@ -526,7 +529,7 @@ __device__ __forceinline__ void order_entries(const EnvDev& d, const Chunk& c, i
   for (int base = g.tid - lane; base < space; base += g.n) {  // warp-uniform trips
     const int k = base + lane;
     int b = 8;  // no entry
-    if (k < space && (k & 7) < G) b = group_bucket(c.qpred[c.reg[k >> 3]], k & 7);
+    if (k < space && (k & 7) < G) b = group_bucket(c.rec[c.reg[k >> 3]].qpred, k & 7);
     const unsigned peers = __match_any_sync(SP_FULL, b);
     if (b < 8 && (peers & lt) == 0) atomicAdd(&cnt[b], __popc(peers));
   }
@@ -546,7 +549,7 @@ __device__ __forceinline__ void order_entries(const EnvDev& d, const Chunk& c, i
     int slot = 0;
     if (k < space && (k & 7) < G) {
       slot = c.reg[k >> 3];
-      b = group_bucket(c.qpred[slot], k & 7);
+      b = group_bucket(c.rec[slot].qpred, k & 7);
     }
     const unsigned peers = __match_any_sync(SP_FULL, b);
     const int leader = __ffs(peers) - 1;
@@ -578,11 +581,11 @@ __device__ __forceinline__ int64_t row_of(const EnvDev& d, int m, int64_t mstart
 // Philox block, spread over the whole CTA; z parks in the slot's output row.
 // z ~ N(0,1) of one noise block (4 beams) of `slot` into its output row
 __device__ __forceinline__ void noise_block(const EnvDev& d, const Chunk& c, int slot, int b) {
-  const Block4 blk = stream_block(d.seed, c.gid[slot], 0u, c.nctr[slot] + (uint64_t)b);
+  const Block4 blk = stream_block(d.seed, c.gid[slot], 0u, c.rec[slot].nctr + (uint64_t)b);
   float z[4];
   draw_normals4(blk, z);
   SP_CHECK(slot >= 0 && slot < d.slot_cap && b >= 0 && b < d.nb);
-  float* row = c.out0[slot] + 5 + 4 * b;
+  float* row = c.rec[slot].out0 + 5 + 4 * b;
 #ifdef SP_EXP_NOZ  // experiment: no z stores (wrong noise), isolates their cost
   if (z[0] == 12345.0f)
 #endif
@@ -606,9 +609,9 @@ __device__ __forceinline__ void prenoise(const EnvDev& d, const StepArgs& a, con
   for (int k = (int)threadIdx.x - first; k < n; k += idle) {
     const int64_t s = s0 + k;
     const int64_t row = row_of(d, m, mstart, s);
-    c.nctr[k] = d.ctr[s];
+    c.rec[k].nctr = d.ctr[s];
     c.gid[k] = (uint32_t)(d.env_id_offset + row);
-    c.out0[k] = a.store_states + row * d.D;  // z parks in the store_states row
+    c.rec[k].out0 = a.store_states + row * d.D;  // z parks in the store_states row
   }
   asm volatile("bar.sync 1, %0;" ::"r"(idle) : "memory");
   for (int it = (int)threadIdx.x - first; it < n * nb; it += idle) {
@@ -704,20 +707,25 @@ struct FinObs {
   int d_slot_cap;           // SP_CHECKED bounds
   // z of beam j, parked in the output row by the noise pass: loaded when the
   // ray is dispatched so the L2 round trip overlaps its march
-  __device__ __forceinline__ float pre(int slot, int j) const { return c.out0[slot][5 + j]; }
+  __device__ __forceinline__ float pre(int slot, int j) const { return c.rec[slot].out0[5 + j]; }
   __device__ __forceinline__ void operator()(int slot, int j, double t, int hit, int steps,
                                              float zpre) const {
-    float* rowp = c.out0[slot];
+    float* rowp = c.rec[slot].out0;
     SP_CHECK(slot >= 0 && slot < d_slot_cap && j >= 0 && j < R);
     const double z = (double)zpre;
-    const double v = dclip(dadd(t, dadd(0.0, dmul(c.sig[slot], z))), 0.0, max_range);
+    // clip(raw + (0 + sigma z), 0, max) (core.py:240-241): the 0 + only turns
+    // a -0.0 into +0.0, which t + (.) absorbs for t >= 0; all finite, so
+    // plain selects replace the NaN-aware fmin/fmax
+    double v = dadd(t, dmul(c.rec[slot].sig, z));
+    v = v < 0.0 ? 0.0 : v;
+    v = v > max_range ? max_range : v;
     const float o = (float)div_by(v, max_range, inv_max_range);
     rowp[5 + j] = o;
-    float* r1 = c.out1[slot];
+    float* r1 = c.rec[slot].out1;
     if (r1) r1[5 + j] = o;
     if (t < proximity) c.prox[slot] = 1;
     const int grp = j >> gs;  // byte grp of the 64-bit word, as a 32-bit OR (native)
-    atomicOr((unsigned*)&c.qacc[slot] + (grp >> 2), 1u << (8 * (grp & 3) + step_level(steps)));
+    atomicOr((unsigned*)&c.rec[slot].qacc + (grp >> 2), 1u << (8 * (grp & 3) + step_level(steps)));
     if constexpr (kRec) {
       const int64_t k = (int64_t)(c.gid[slot] - gid0) * R + j;
       // post-step scans fill a store_states row (and the states row too when
@@ -765,14 +773,14 @@ __device__ __forceinline__ void add_slot(const EnvDev& d, const Chunk& c, int sl
                                          double y, double ch, double sh, double sig, uint32_t gid,
                                          uint64_t nctr, int32_t hwrite, float* o0, float* o1) {
   SP_CHECK(slot >= 0 && slot < d.slot_cap && c.ctl[1] < d.slot_cap);
-  c.out0[slot] = o0;
-  c.out1[slot] = o1;
+  c.rec[slot].out0 = o0;
+  c.rec[slot].out1 = o1;
   c.hwrite[slot] = hwrite;
-  c.px[slot] = x; c.py[slot] = y; c.ch[slot] = ch; c.sh[slot] = sh; c.sig[slot] = sig;
+  c.rec[slot].px = x; c.rec[slot].py = y; c.rec[slot].ch = ch; c.rec[slot].sh = sh; c.rec[slot].sig = sig;
   c.gid[slot] = gid;
-  c.nctr[slot] = nctr;
+  c.rec[slot].nctr = nctr;
   c.prox[slot] = 0;
-  c.qacc[slot] = 0;
+  c.rec[slot].qacc = 0;
   c.reg[atomicAdd(&c.ctl[1], 1)] = slot;
 }
 
@@ -815,7 +823,7 @@ __device__ __forceinline__ bool reset_env(const EnvDev& d, const MapView& mv, co
   for (int wi = 0; wi < ((delay + 15) >> 4); ++wi) d.hist[(int64_t)wi * d.n + s] = ~0ull;
   header_row(mc, x, y, bearing_error(x, y, th, mc.goal_x, mc.goal_y), c0, s0, 0.0, 0.0, vml, vma,
              orow, nullptr);
-  c.qpred[slot] = kNoHistory;  // a fresh spawn has no step history: ranks longest
+  c.rec[slot].qpred = kNoHistory;  // a fresh spawn has no step history: ranks longest
   add_slot(d, c, slot, x, y, c0, s0, sig, gid, ctr, (int32_t)s, orow, nullptr);
   ctr += d.nb;
   return true;
@@ -847,14 +855,6 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
                                           int64_t row, uint32_t gid, uint64_t& ctr, int64_t av,
                                           int cap, int slot_cap, uint64_t* mbar, int mpar) {
   StepA r;
-  // fields read late in the step (cross-track, obs header, noise sigma): an
-  // L2 prefetch now turns their later DRAM misses into L2 hits, without
-  // holding registers across the physics
-  prefetch_l2(d.sx + s);
-  prefetch_l2(d.sy + s);
-  prefetch_l2(d.c0 + s);
-  prefetch_l2(d.s0 + s);
-  prefetch_l2(d.psig + s);
   // the lane state is loaded before the action checks, so its DRAM round
   // trip overlaps the action load
   double x = d.x[s], y = d.y[s], h = d.h[s], vl = d.vl[s], va = d.va[s];
@@ -919,10 +919,15 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
     const bool timed_out = !coll && !arrived && step >= d.timeout;
     r.ev = coll ? 1 : (arrived ? 2 : (timed_out ? 3 : 0));
     r.ended = coll || arrived || timed_out;
+    // the episode constants read from here on arrived by cp.async into this
+    // env's (not yet registered) scan-slot words at chunk start
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    const double ep_sx = c.rec[e].px, ep_sy = c.rec[e].py, ep_c0 = c.rec[e].ch, ep_s0 = c.rec[e].sh;
+    const double ep_sig = c.rec[e].sig;
     // shaped reward without the proximity term (reward.py:55-73) + obs header
     const double alpha = bearing_error(x, y, h, mc.goal_x, mc.goal_y);
     if (r.ev == 0 || r.ev == 3) {
-      const double d2 = cross_track(x, y, d.sx[s], d.sy[s], mc.goal_x, mc.goal_y);
+      const double d2 = cross_track(x, y, ep_sx, ep_sy, mc.goal_x, mc.goal_y);
       const double r_d1 = dclip(dsub(1.0, div_by(d1, mc.plan_dist, mc.inv_plan)), 0.0, 1.0);
       const double r_d2 = dclip(dsub(1.0, div_by(d2, mc.plan_dist, mc.inv_plan)), 0.0, 1.0);
       const double r_v = vl > dmul(vml, 0.5) ? 1.0 : 0.0;  // vml / 2, exact
@@ -936,11 +941,11 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
     float* o_store = a.store_states + row * d.D;
     float* o_state = r.ended && d.auto_reset ? nullptr : a.states + row * d.D;
     SP_ESTAMP(42);
-    header_row(mc, x, y, alpha, d.c0[s], d.s0[s], vl, va, vml, vma, o_store, o_state);
+    header_row(mc, x, y, alpha, ep_c0, ep_s0, vl, va, vml, vma, o_store, o_state);
     SP_ESTAMP(43);
     // the post-step scan (core.py:203-206); cos/sin of h1 == of wrap(h1)
-    // (its dispatch prediction c.qpred[e] arrives by cp.async, see the kernel)
-    add_slot(d, c, e, x, y, cos1, sin1, d.psig[s], gid, ctr,
+    // (its dispatch prediction c.rec[e].qpred arrives by cp.async, see the kernel)
+    add_slot(d, c, e, x, y, cos1, sin1, ep_sig, gid, ctr,
              r.ended && d.auto_reset ? -1 : (int32_t)s, o_store, o_state);
     ctr += d.nb;
     d.x[s] = x; d.y[s] = y; d.h[s] = h; d.vl[s] = vl; d.va[s] = va;
@@ -1102,8 +1107,18 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
                          ? min(n, d.prenoise * max(0, (int)blockDim.x - first_idle) / d.nb)
                          : 0;
     if (act) c.rowi[e] = (int32_t)row;
-    if (act && a.mode == MODE_STEP)  // the post-step scan's step history, copied without
-      cp_async8(&c.qpred[e], &d.qhist[s]);  // registers; waited for before the ray order
+    if (act && a.mode == MODE_STEP) {
+      // copied without registers, waited for where used: the post-step scan's
+      // step history (before the ray order) and the episode constants phase A
+      // needs late, parked in this env's scan-slot words until add_slot
+      // overwrites them (cross-track start, obs-header start heading, sigma)
+      cp_async8(&c.rec[e].qpred, &d.qhist[s]);
+      cp_async8(&c.rec[e].px, d.sx + s);
+      cp_async8(&c.rec[e].py, d.sy + s);
+      cp_async8(&c.rec[e].ch, d.c0 + s);
+      cp_async8(&c.rec[e].sh, d.s0 + s);
+      cp_async8(&c.rec[e].sig, d.psig + s);
+    }
     __syncthreads();
     if (kpre > 0 && e >= first_idle) prenoise(d, a, c, kpre, first_idle, s0, m, mstart);
 
@@ -1273,10 +1288,10 @@ __global__ void __launch_bounds__(SP_SCAN_THREADS, SP_CTAS_PER_SM)
     for (int e = threadIdx.x; e < n; e += blockDim.x) {
       double sh_, ch_;
       sincos(q.h[s0 + e], &sh_, &ch_);
-      c.px[e] = q.x[s0 + e];
-      c.py[e] = q.y[s0 + e];
-      c.ch[e] = ch_;
-      c.sh[e] = sh_;
+      c.rec[e].px = q.x[s0 + e];
+      c.rec[e].py = q.y[s0 + e];
+      c.rec[e].ch = ch_;
+      c.rec[e].sh = sh_;
       for (int g = 0; g < d.n_groups; ++g) c.list[e * d.n_groups + g] = (uint16_t)((e << 3) | g);
     }
     __syncthreads();
