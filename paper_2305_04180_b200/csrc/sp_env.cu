@@ -189,16 +189,15 @@ struct Ray {
   int u, v, ax, ayw, kb, n;  // n: march steps taken (scheduling history)
 };
 
-// 1/v to within an ulp: fp32 seed + two fp64 Newton steps (no DDIV).
+// 1/v to within an ulp: the fp64 reciprocal approximation (full exponent
+// range) + two Newton steps, no branches and no DDIV.  v == 0 (an axis the
+// ray never crosses) and subnormal v give +-inf.
 __device__ __forceinline__ double recip(double v) {
-  if (v == 0.0) return __longlong_as_double(0x7ff0000000000000ll);  // +inf: never exits this axis
-  if (fabs(v) < 1e-30) return 1.0 / v;
-  float f;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(f) : "f"((float)v));
-  double r = (double)f;
-  r = r * (2.0 - v * r);
-  r = r * (2.0 - v * r);
-  return r;
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(v));
+  const double r1 = r * (2.0 - v * r);
+  const double r2 = r1 * (2.0 - v * r1);
+  return isinf(r) ? r : r2;
 }
 
 // Exact int <-> double conversions on the fp64 pipe instead of the slower
