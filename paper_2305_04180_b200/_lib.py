@@ -173,6 +173,42 @@ def load() -> ctypes.CDLL:
     return lib
 
 
+TORCH_EXT = os.path.join(HERE, "_lib", "sparrow_torch.so")
+_ops = None
+
+
+def torch_ops():
+    """torch.ops.sparrow: the PyTorch C++ extension (csrc/sp_torch.cpp) bound to
+    the loaded libsparrow.so -- the binding of the hot calls (env step, ring
+    append).  It checks tensors in C++ and takes the current CUDA stream from
+    ATen.  None when the extension was not built (then ctypes drives the same
+    C-ABI entry points)."""
+    global _ops
+    if _ops is None:
+        load()
+        import torch
+        if not os.path.exists(TORCH_EXT):
+            _ops = False
+        else:
+            torch.ops.load_library(TORCH_EXT)
+            torch.ops.sparrow.bind(os.path.abspath(LIB_PATH))
+            _ops = torch.ops.sparrow
+    return _ops or None
+
+
+def status_of(exc: BaseException) -> int:
+    """The SpStatus a torch.ops.sparrow call failed with (in its message); a
+    failed tensor check in the extension is a ValueError like the ctypes
+    path's argument checks."""
+    import re
+    m = re.search(r"\(status (\d+)\)", str(exc))
+    return int(m.group(1)) if m else SP_EINVAL
+
+
+def binding() -> str:
+    return "torch C++ extension (torch.ops.sparrow)" if torch_ops() else "ctypes"
+
+
 def last_error() -> str:
     return load().sp_last_error().decode(errors="replace")
 

@@ -77,6 +77,32 @@ def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()
     return out
 
 
+TORCH_EXT = os.path.join(HERE, "_lib", "sparrow_torch.so")
+
+
+def build_torch_ext(force: bool = False, verbose: bool = False) -> str:
+    """The PyTorch C++ extension (csrc/sp_torch.cpp: torch.ops.sparrow.*) over
+    the C-ABI, compiled in-tree next to libsparrow.so.  It resolves the C-ABI
+    with dlsym from the library the package loaded, so it does not link it."""
+    src = os.path.join(CSRC, "sp_torch.cpp")
+    hdr = os.path.join(HERE, "..", "include", "sparrow.h")
+    if (not force and os.path.exists(TORCH_EXT)
+            and os.path.getmtime(TORCH_EXT) >= max(os.path.getmtime(src), os.path.getmtime(hdr))):
+        return TORCH_EXT
+    import glob
+    from torch.utils.cpp_extension import load
+    bdir = os.path.join(HERE, "_lib", "torch_build")
+    os.makedirs(bdir, exist_ok=True)
+    load(name="sparrow_torch", sources=[src], build_directory=bdir, with_cuda=True,
+         is_python_module=False, extra_cflags=["-O2"], extra_ldflags=["-ldl"], verbose=verbose)
+    built = glob.glob(os.path.join(bdir, "sparrow_torch*.so"))
+    if not built:
+        raise RuntimeError("torch extension build produced no library")
+    shutil.copy2(built[0], TORCH_EXT + ".tmp")
+    os.replace(TORCH_EXT + ".tmp", TORCH_EXT)
+    return TORCH_EXT
+
+
 if __name__ == "__main__":
     args = [a for a in sys.argv[1:] if a != "--force"]
     if args:  # python -m paper_2305_04180_b200.build OUT.so DEF=1 ...

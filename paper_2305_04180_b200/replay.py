@@ -155,9 +155,18 @@ class ReplayBuffer:
             raise ValueError(f"state rows must have {self.state_dim} columns")
         with self._lock:
             self._order_after(self._last_sample)
-            _lib.check(self._lib.sp_rb_append(self._h, s.data_ptr(), a.data_ptr(), r.data_ptr(),
-                                              r64, s2.data_ptr(), d.data_ptr(), n,
-                                              _lib.stream_ptr(self.device)), "append_batch")
+            ops = _lib.torch_ops()
+            if ops is not None:
+                try:
+                    ops.rb_append(self._h.value, s, a, r, s2, d)
+                except RuntimeError as exc:
+                    _lib.check(_lib.status_of(exc), "append_batch")
+                    raise
+            else:
+                _lib.check(self._lib.sp_rb_append(self._h, s.data_ptr(), a.data_ptr(),
+                                                  r.data_ptr(), r64, s2.data_ptr(), d.data_ptr(),
+                                                  n, _lib.stream_ptr(self.device)),
+                           "append_batch")
             self._last_append = self._record()
 
     add = append_batch  # the paper's Sharer.buffer.add

@@ -347,13 +347,30 @@ class VecEnv:
                 torch.empty(n, dtype=torch.bool, device=dev),
                 torch.empty((n, d), dtype=torch.float32, device=dev),
                 torch.empty(n, dtype=torch.int8, device=dev))
-        rc = self._lib.sp_env_step(self._h, a.data_ptr(), out.states.data_ptr(),
-                                   out.store_states.data_ptr(), out.rewards.data_ptr(),
-                                   out.dones.data_ptr(), out.truncated.data_ptr(),
-                                   out.events.data_ptr(), self._stream())
-        _lib.check(rc, "step")
+        self._launch_step(a, out)
         self._last_states = out.states
         return out
+
+    def _launch_step(self, a, out: StepBatch) -> None:
+        """sp_env_step through the torch extension (tensor checks in C++,
+        ATen's current stream), or ctypes when it is not built."""
+        rb = out.states.numel() * out.states.element_size()
+        s0, s1 = out.states.data_ptr(), out.store_states.data_ptr()
+        if s0 < s1 + rb and s1 < s0 + rb:  # the C-ABI's own check, before the op's alias rules
+            raise ValueError("states and store_states must not overlap")
+        ops = _lib.torch_ops()
+        if ops is not None:
+            try:
+                ops.env_step(self._h.value, a, out.states, out.store_states, out.rewards,
+                             out.dones, out.truncated, out.events)
+            except RuntimeError as exc:  # the C-ABI status, mapped like ctypes calls
+                _lib.check(_lib.status_of(exc), "step")
+                raise
+            return
+        _lib.check(self._lib.sp_env_step(self._h, a.data_ptr(), out.states.data_ptr(),
+                                         out.store_states.data_ptr(), out.rewards.data_ptr(),
+                                         out.dones.data_ptr(), out.truncated.data_ptr(),
+                                         out.events.data_ptr(), self._stream()), "step")
 
     def new_batch(self) -> StepBatch:
         """Device output tensors for ``step_batch(actions, out=...)``."""

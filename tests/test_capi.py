@@ -5,6 +5,8 @@ import ctypes
 import os
 import re
 
+import pytest
+
 from paper_2305_04180_b200 import _lib
 
 HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
@@ -133,3 +135,22 @@ def test_env_create_validates_before_touching_the_device():
     d.occupancy = holed.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
     assert create(cfg(), [d]) == _lib.SP_EMAP
     assert b"border" in lib.sp_last_error()
+
+
+def test_torch_extension_registers_the_hot_ops():
+    """The PyTorch C++ extension (csrc/sp_torch.cpp) loads, binds the very
+    libsparrow.so the package loaded (dlsym) and registers torch.ops.sparrow
+    env_step / rb_append with the reference's argument shapes; with a CPU
+    tensor it raises (there is no CPU path) instead of computing."""
+    import torch
+    from paper_2305_04180_b200 import _lib
+    ops = _lib.torch_ops()
+    assert ops is not None, "build the extension: python -m paper_2305_04180_b200.build"
+    assert "torch C++ extension" in _lib.binding()
+    for name in ("env_step", "rb_append", "bind"):
+        assert hasattr(ops, name)
+    with pytest.raises(RuntimeError, match="CUDA"):
+        ops.env_step(0, torch.zeros(4, dtype=torch.int64), torch.zeros((4, 37)),
+                     torch.zeros((4, 37)), torch.zeros(4, dtype=torch.float64),
+                     torch.zeros(4, dtype=torch.bool), torch.zeros(4, dtype=torch.bool),
+                     torch.zeros(4, dtype=torch.int8))
