@@ -85,6 +85,7 @@ struct MapView {
   const uint8_t* blk;
   const uint32_t* bits;
   int W, H, Wb, WW;
+  uint32_t kbase;  // shared-window address of blk (tables in shared memory), else 0
   __device__ __forceinline__ uint32_t code(int ix, int iy) const {
     return blk[iy * Wb + ix];
   }
@@ -96,6 +97,20 @@ struct MapView {
     return bits[iy * WW + (ix >> 5)];
   }
 };
+
+// The signed cell byte at table offset `a` (+ kbase).  With the tables in
+// shared memory, rays carry the table's shared-window address in their kb, so
+// a march lookup is two IMADs and one LDS with no base add.
+template <bool kSmem>
+__device__ __forceinline__ int table_code(const MapView& mv, int a) {
+  if constexpr (kSmem) {
+    int v;
+    asm("ld.shared.s8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+  } else {
+    return ((const int8_t*)mv.blk)[a];
+  }
+}
 
 // disc_collides for one disc (_cy.pyx:109-158), exact fp64 test; the cell
 // table proves most discs free with one lookup.
@@ -178,14 +193,16 @@ __device__ __forceinline__ void sp_stamp_flush() {
 // Ray state, mirrored so that every ray moves toward +u, +v: on an axis the
 // ray travels in the negative direction, coordinates are negated (exactly)
 // and cell indices become u = -ix - 1, so cell u covers [u, u + 1).  In cell
-// units: origin (X, Y), |direction| / cell (DX, DY) and cell / |direction|
-// (IDX, IDY), so t = (face - X) * IDX is the reference's parameter in cm --
-// bit for bit the unmirrored ((double)face - x0) * idx, since negation is
-// exact.  The table address of cell (u, v) is v * ayw + u * ax + kb, with
-// (ax, bx) = (1, 0) or (-1, -1) per axis (ix = ax * u + bx), ayw = ay * W
-// and kb = by * W + bx.
+// units: origin (X, Y); cell / |direction| (IDX, IDY), so t = (face - X) * IDX
+// is the reference's parameter in cm -- bit for bit the unmirrored
+// ((double)face - x0) * idx, since negation is exact; slopes SY = |dy / dx|
+// (v gained per unit of u) and SX = |dx / dy|, which give the other axis at
+// a face crossing without the crossing's parameter.  The table address of
+// cell (u, v) is v * ayw + u * ax + kb, with (ax, bx) = (1, 0) or (-1, -1) per
+// axis (ix = ax * u + bx), ayw = ay * W and kb = by * W + bx (+ the table's
+// shared-window address).
 struct Ray {
-  double X, Y, DX, DY, IDX, IDY;
+  double X, Y, SX, SY, IDX, IDY;
   int u, v, ax, ayw, kb, n;  // n: march steps taken (scheduling history)
 };
 
@@ -222,24 +239,28 @@ __device__ __forceinline__ int floor_i(double v) {  // floor(v), |v| < 2^31
 // and the occupied cell it stopped in.  Every map has an occupied border
 // (GridMap's invariant, checked by sp_env_create), so no step can leave the
 // grid and there are no bounds tests.
+template <bool kSmem>
 __device__ __forceinline__ bool ray_step(Ray& r, const MapView& mv, const EnvDev& d) {
-  SP_CHECK((unsigned)(r.v * r.ayw + r.u * r.ax + r.kb) < (unsigned)(d.Wb * d.Hb));
-  const int code = (int)((const int8_t*)mv.blk)[r.v * r.ayw + r.u * r.ax + r.kb];
+  SP_CHECK((unsigned)(r.v * r.ayw + r.u * r.ax + r.kb - (int)mv.kbase) < (unsigned)(d.Wb * d.Hb));
+  const int code = table_code<kSmem>(mv, r.v * r.ayw + r.u * r.ax + r.kb);
   const bool occupied = code < 0;  // else the box radius
   // the free box's far faces: u + 1 + r (r = 0: this cell's own face)
   const int fu = r.u + 1 + code;
   const int fv = r.v + 1 + code;
-  const double tu = ((double)fu - r.X) * r.IDX;
-  const double tv = ((double)fv - r.Y) * r.IDY;
+  const double au = (double)fu - r.X, av = (double)fv - r.Y;
+  const double tu = au * r.IDX, tv = av * r.IDY;
   const bool xs = tu <= tv;  // ties exit through x, as tmx <= tmy (_cy.pyx:89)
-  const double t = xs ? tu : tv;
+  const bool over = tu > d.max_range && tv > d.max_range;  // min(tu, tv) > max (:97-99)
   // the cell on the other axis at the exit point, clamped between the current
-  // cell and the box's far cell (the ray moves monotonically)
-  const int c = floor_i(fma(t, xs ? r.DY : r.DX, xs ? r.Y : r.X));
+  // cell and the box's far cell (the ray moves monotonically): the crossing
+  // of the far x face is at v = Y + au SY, of the far y face at u = X + av SX,
+  // both independent of the face choice
+  const double pv = fma(au, r.SY, r.Y);
+  const double pu = fma(av, r.SX, r.X);
+  const int c = floor_i(xs ? pv : pu);
   const int lo = xs ? r.v : r.u;
   const int hi = (xs ? fv : fu) - 1;
   const int cc = min(max(c, lo), hi);
-  const bool over = t > d.max_range;  // :97-99
   const bool finished = occupied || over;
   if (!finished) {
     r.u = xs ? fu : cc;
@@ -251,14 +272,14 @@ __device__ __forceinline__ bool ray_step(Ray& r, const MapView& mv, const EnvDev
 
 // A parked ray: a finished fixed point for the lanes of a ray slot with no
 // ray (cell (0, 0) is a border cell, occupied).
-__device__ __forceinline__ void ray_park(Ray& r) {
+__device__ __forceinline__ void ray_park(Ray& r, const MapView& mv) {
   r.u = r.v = 0;
   r.ax = 1;
   r.ayw = 0;
-  r.kb = 0;
+  r.kb = (int)mv.kbase;
   r.n = 0;
   r.X = r.Y = 0.5;
-  r.DX = r.DY = 1.0;
+  r.SX = r.SY = 1.0;
   r.IDX = r.IDY = 1.0;
 }
 
@@ -266,40 +287,41 @@ __device__ __forceinline__ void ray_park(Ray& r) {
 // cell -- then its range is the parameter at which it entered that cell: the
 // later of the cell's two entry faces u, v (the march's last exit parameter,
 // bit for bit; 0 when the origin cell itself is occupied) -- or past
-// max_range (range max_range, no hit cell).
+// max_range (range max_range, no hit cell).  An axis the ray does not move
+// along (IDX = inf) has no entry face: its term is -inf, or NaN (0 * inf)
+// when the origin lies on that axis's cell boundary, and fmax drops a NaN.
+template <bool kSmem>
 __device__ __forceinline__ double ray_end(const Ray& r, const MapView& mv, const EnvDev& d,
                                           int& hit) {
   const int ix = r.ax * r.u + (r.ax < 0 ? -1 : 0);
   const int iy = r.ayw < 0 ? -r.v - 1 : r.v;
-  const bool occ = ((const int8_t*)mv.blk)[r.v * r.ayw + r.u * r.ax + r.kb] < 0;
+  const bool occ = table_code<kSmem>(mv, r.v * r.ayw + r.u * r.ax + r.kb) < 0;
   hit = occ ? iy * d.W + ix : -1;
   if (!occ) return d.max_range;
-  // plain selects, not fmax: no NaN handling needed (a 0 * inf entry term of
-  // an axis-parallel ray compares false and drops out, as fmax would drop it)
   const double eu = ((double)r.u - r.X) * r.IDX, ev = ((double)r.v - r.Y) * r.IDY;
-  const double te = eu > ev ? eu : ev;
-  return te > 0.0 ? te : 0.0;
+  return fmax(fmax(eu, ev), 0.0);
 }
 
 // Returns true if finished during setup (origin outside the grid -> 0).
 __device__ __forceinline__ bool ray_setup(Ray& r, double x0, double y0, double ch, double sh,
-                                          double2 cs, const EnvDev& d) {
+                                          double2 cs, const EnvDev& d, const MapView& mv) {
   const double dx = ch * cs.x - sh * cs.y;  // cos(h + o_j)
   const double dy = sh * cs.x + ch * cs.y;  // sin(h + o_j)
   const double xc = x0 * d.inv_cell, yc = y0 * d.inv_cell;
   const int ix = (int)floor(xc), iy = (int)floor(yc);
-  const bool px = dx >= 0.0, py = dy >= 0.0;  // dx == 0: IDX = +inf, x faces never taken
+  const bool px = dx >= 0.0, py = dy >= 0.0;  // dx == 0: SY = +inf, x faces never taken
   r.X = px ? xc : -xc;
   r.Y = py ? yc : -yc;
-  r.DX = fabs(dx * d.inv_cell);
-  r.DY = fabs(dy * d.inv_cell);
-  r.IDX = fabs(recip(dx) * d.cell);
-  r.IDY = fabs(recip(dy) * d.cell);
+  const double rx = recip(dx), ry = recip(dy);  // +-inf for a zero component
+  r.IDX = fabs(rx * d.cell);
+  r.IDY = fabs(ry * d.cell);
+  r.SY = fabs(dy * rx);  // |dy / dx|: +inf for dx == 0, 0 for dy == 0
+  r.SX = fabs(dx * ry);
   r.u = px ? ix : -ix - 1;
   r.v = py ? iy : -iy - 1;
   r.ax = px ? 1 : -1;
   r.ayw = py ? d.Wb : -d.Wb;
-  r.kb = (py ? 0 : -d.Wb) + (px ? 0 : -1);
+  r.kb = (int)mv.kbase + (py ? 0 : -d.Wb) + (px ? 0 : -1);
   r.n = 0;
   return (unsigned)ix >= (unsigned)d.W || (unsigned)iy >= (unsigned)d.H;  // :37-39
 }
@@ -394,7 +416,7 @@ __device__ __forceinline__ int beam_of(const Chunk& c, int q, int gs, int& slot)
 // other's.  A warp refills only when at least d.refill_min of its 64 ray
 // slots are idle (or the queue is drained); finished rays are retired in the
 // same branch, so per-ray setup/finish code runs at high SIMT occupancy.
-template <bool kHit, class Fin>
+template <bool kSmem, bool kHit, class Fin>
 __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, const Chunk& c,
                                           const double2* beam, int n_ent, const Fin& fin) {
   const int R = d.R;
@@ -409,8 +431,8 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
   int ea = 0, ja = 0, eb = 0, jb = 0;
   float za = 0.0f, zb = 0.0f;  // the slots' prefetched noise (Fin::pre)
   Ray ra, rb;
-  ray_park(ra);
-  ray_park(rb);
+  ray_park(ra, mv);
+  ray_park(rb, mv);
   for (;;) {
     const unsigned ia = __ballot_sync(SP_FULL, fin_a);
     const unsigned ib = __ballot_sync(SP_FULL, fin_b);
@@ -418,13 +440,13 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
     if (n_idle >= d.refill_min || drained) {
       if (busy_a && fin_a) {  // steps taken = moves + the finishing step
         int hit;
-        const double t = ray_end(ra, mv, d, hit);
+        const double t = ray_end<kSmem>(ra, mv, d, hit);
         fin(ea, ja, t, kHit ? hit : -1, ra.n + 1, za);
         busy_a = false;
       }
       if (busy_b && fin_b) {
         int hit;
-        const double t = ray_end(rb, mv, d, hit);
+        const double t = ray_end<kSmem>(rb, mv, d, hit);
         fin(eb, jb, t, kHit ? hit : -1, rb.n + 1, zb);
         busy_b = false;
       }
@@ -448,9 +470,9 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
         const int my_b = base + na + __popc(ib & lt);
         if (fin_a && my_a < total && (ja = beam_of(c, my_a, gs, ea)) < R) {
           za = fin.pre(ea, ja);
-          if (ray_setup(ra, c.rec[ea].px, c.rec[ea].py, c.rec[ea].ch, c.rec[ea].sh, beam[ja], d)) {
+          if (ray_setup(ra, c.rec[ea].px, c.rec[ea].py, c.rec[ea].ch, c.rec[ea].sh, beam[ja], d, mv)) {
             fin(ea, ja, 0.0, -1, 1, za);  // origin outside the grid: range 0 (_cy.pyx:37-39)
-            ray_park(ra);
+            ray_park(ra, mv);
           } else {
             busy_a = true;
             fin_a = false;
@@ -458,9 +480,9 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
         }
         if (fin_b && my_b < total && (jb = beam_of(c, my_b, gs, eb)) < R) {
           zb = fin.pre(eb, jb);
-          if (ray_setup(rb, c.rec[eb].px, c.rec[eb].py, c.rec[eb].ch, c.rec[eb].sh, beam[jb], d)) {
+          if (ray_setup(rb, c.rec[eb].px, c.rec[eb].py, c.rec[eb].ch, c.rec[eb].sh, beam[jb], d, mv)) {
             fin(eb, jb, 0.0, -1, 1, zb);
-            ray_park(rb);
+            ray_park(rb, mv);
           } else {
             busy_b = true;
             fin_b = false;
@@ -473,8 +495,8 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
     // per-cell steps); a finished ray stays put for the rest of the group
 #pragma unroll
     for (int u = 0; u < SP_MARCH_GROUP; ++u) {
-      fin_a = ray_step(ra, mv, d);
-      fin_b = ray_step(rb, mv, d);
+      fin_a = ray_step<kSmem>(ra, mv, d);
+      fin_b = ray_step<kSmem>(rb, mv, d);
     }
   }
 }
@@ -760,9 +782,11 @@ __device__ __forceinline__ MapView bind_map(const EnvDev& d, int m, uint8_t* sme
     phase ^= 1u;
     mv.blk = smem_maps;
     mv.bits = (const uint32_t*)(smem_maps + d.blk_bytes);
+    mv.kbase = smem_u32(smem_maps);
   } else {
     mv.blk = src;
     mv.bits = (const uint32_t*)(src + d.blk_bytes);
+    mv.kbase = 0;
   }
   return mv;
 }
@@ -1055,6 +1079,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
   if constexpr (kSmem) {
     mv.blk = smem;
     mv.bits = (const uint32_t*)(smem + d.blk_bytes);
+    mv.kbase = smem_u32(smem);
   }
   for (int64_t s0 = sb; s0 < se;) {
     if (!plan || s0 >= mend) {  // a further map (CTAs spanning maps): from the table
@@ -1186,7 +1211,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     noise_phase(d, c, n_slots, kpre, cta_grp());
     __syncthreads();
     SP_STAMP(4);
-    ray_phase<kRec>(mv, d, c, beam, c.ctl[20], fin);
+    ray_phase<kSmem, kRec>(mv, d, c, beam, c.ctl[20], fin);
     __syncthreads();
     SP_STAMP(5);
     store_history(d, c, n_slots);
@@ -1218,7 +1243,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       order_entries(d, c, n2, cta_grp());
       noise_phase(d, c, n2, 0, cta_grp());
       __syncthreads();
-      ray_phase<kRec>(mv, d, c, beam, c.ctl[20], fin);
+      ray_phase<kSmem, kRec>(mv, d, c, beam, c.ctl[20], fin);
       __syncthreads();
       store_history(d, c, n2);
     }
@@ -1271,6 +1296,7 @@ __global__ void __launch_bounds__(SP_SCAN_THREADS, SP_CTAS_PER_SM)
   if constexpr (kSmem) {
     mv.blk = smem;
     mv.bits = (const uint32_t*)(smem + d.blk_bytes);
+    mv.kbase = smem_u32(smem);
   }
   for (int64_t s0 = sb; s0 < se;) {
     while (q.qoff[m + 1] <= s0) ++m;
@@ -1295,7 +1321,7 @@ __global__ void __launch_bounds__(SP_SCAN_THREADS, SP_CTAS_PER_SM)
     }
     __syncthreads();
     const FinScan fin{q.ranges, q.hit_cell, s0, d.R};
-    ray_phase<true>(mv, d, c, beam, n * d.n_groups, fin);
+    ray_phase<kSmem, true>(mv, d, c, beam, n * d.n_groups, fin);
     s0 += n;
   }
 }

@@ -240,6 +240,20 @@ def test_lidar_scan_and_collision_helpers():  # test_env.py:301-329
     assert check_collision(m2, (5.0, 5.0), radius_cm=9.0)
 
 
+def test_axis_parallel_beam_from_a_cell_boundary():
+    """A beam exactly along +x (heading 0, centre beam offset 0.0) from a
+    row boundary (integer y, cell 1 cm) never crosses a y face: its range is
+    the x-face entry alone (the wall face at x = 30), from any origin."""
+    from paper_2305_04180_b200 import VecEnv
+    lc = LidarConfig(n_beams=27, max_range_cm=100.0)
+    j = int(np.flatnonzero(lc.beam_offsets() == 0.0)[0])
+    m = make_map(40, blocks=((30, 0, 32, 40),))
+    env = VecEnv([m], 1, fixed_ranges(), EnvConfig(lidar=lc))
+    xs, ys = [10.0, 10.0, 10.5, 12.0, 10.25], [20.0, 20.5, 20.0, 7.0, 33.0]
+    got = env.scan(xs, ys, np.zeros(5)).cpu().numpy()
+    assert np.array_equal(got[:, j], 30.0 - np.asarray(xs))
+
+
 # -- test_vecenv.py --------------------------------------------------------------
 
 def _rg(frac=0.3):
