@@ -248,7 +248,7 @@ static Plan plan_launch(SpEnv* env, const std::vector<int64_t>& off, bool stagin
   const size_t budget = std::min((size_t)env->smem_optin,
                                  sm_total / SP_CTAS_PER_SM) - 1024
 #ifdef SP_TIMING
-                        - 512  // the stamps' static shared memory
+                        - 1536  // the stamps' static shared memory
 #endif
       ;
   size_t map_bytes = align_up(d.map_bytes, 128);
@@ -1353,9 +1353,14 @@ int sp_actor_select(const SpMlp* net, const float* states, int64_t n, int64_t en
 
 #ifdef SP_TIMING
 // debug builds only (not part of include/sparrow.h): per-CTA phase stamps
+int sp_debug_read_lane(unsigned long long* out, int n_ctas) {
+  (void)n_ctas;
+  SP_CUDA(cudaMemcpyFromSymbol(out, g_sp_lane, sizeof(unsigned long long) * 5 * 148 * 768));
+  return SP_OK;
+}
 int sp_debug_read_ts(unsigned long long* out, int n_ctas) {
   SP_CUDA(cudaDeviceSynchronize());
-  SP_CUDA(cudaMemcpyFromSymbol(out, g_sp_ts, sizeof(unsigned long long) * 48 * (size_t)n_ctas));
+  SP_CUDA(cudaMemcpyFromSymbol(out, g_sp_ts, sizeof(unsigned long long) * kTs * (size_t)n_ctas));
   return SP_OK;
 }
 #endif

@@ -112,44 +112,109 @@ __device__ __forceinline__ int table_code(const MapView& mv, int a) {
   }
 }
 
-// disc_collides for one disc (_cy.pyx:109-158), exact fp64 test; the cell
-// table proves most discs free with one lookup.
-__device__ __forceinline__ bool disc_hits(const MapView& mv, const EnvDev& d, double x, double y) {
-  const double r = d.radius, cell = d.cell;
-  if (x - r < 0.0 || y - r < 0.0 || x + r > (double)d.W * cell || y + r > (double)d.H * cell)
-    return true;  // :124-126
-  const int cx = (int)floor(x * d.inv_cell), cy = (int)floor(y * d.inv_cell);
-  if (cx >= 0 && cx < d.W && cy >= 0 && cy < d.H) {
-    const uint32_t code = mv.code(cx, cy);  // free box of radius code covers the bbox?
-    if ((code & 0x80u) == 0u && code >= (uint32_t)d.need_k) return false;
-  }
-  int ix0 = (int)floor(ddiv(dsub(x, r), cell)); if (ix0 < 0) ix0 = 0;  // :128-135
-  int ix1 = (int)floor(ddiv(dadd(x, r), cell)); if (ix1 > d.W - 1) ix1 = d.W - 1;
-  int iy0 = (int)floor(ddiv(dsub(y, r), cell)); if (iy0 < 0) iy0 = 0;
-  int iy1 = (int)floor(ddiv(dadd(y, r), cell)); if (iy1 > d.H - 1) iy1 = d.H - 1;
-  const double r2 = dmul(r, r);
-  for (int iy = iy0; iy <= iy1; ++iy) {
-    const uint32_t* rowp = mv.bits + iy * mv.WW;
-    for (int w = ix0 >> 5; w <= (ix1 >> 5); ++w) {
-      uint32_t m = rowp[w];
-      const int lo = w << 5;
-      if (ix0 > lo) m &= ~0u << (ix0 - lo);
-      if (ix1 - lo < 31) m &= (2u << (ix1 - lo)) - 1u;
-      while (m) {
-        const int ix = lo + __ffs(m) - 1;
-        m &= m - 1;
-        const double clo = dmul((double)ix, cell), chi = dadd(clo, cell);  // :141-153
-        double nx = x > clo ? x : clo;
-        if (nx > chi) nx = chi;
-        const double rlo = dmul((double)iy, cell), rhi = dadd(rlo, cell);
-        double ny = y > rlo ? y : rlo;
-        if (ny > rhi) ny = rhi;
-        const double ddx = dsub(x, nx), ddy = dsub(y, ny);
-        if (dadd(dmul(ddx, ddx), dmul(ddy, ddy)) <= r2) return true;
+// The reference's nearest-point test of one occupied cell (_cy.pyx:141-153).
+__device__ __forceinline__ bool cell_within(double x, double y, int ix, int iy, double cell,
+                                            double r2) {
+  const double clo = dmul((double)ix, cell), chi = dadd(clo, cell);
+  double nx = x > clo ? x : clo;
+  if (nx > chi) nx = chi;
+  const double rlo = dmul((double)iy, cell), rhi = dadd(rlo, cell);
+  double ny = y > rlo ? y : rlo;
+  if (ny > rhi) ny = rhi;
+  const double ddx = dsub(x, nx), ddy = dsub(y, ny);
+  return dadd(dmul(ddx, ddx), dmul(ddy, ddy)) <= r2;
+}
+
+// Does bbox row iy ([ix0, ix1]) hold an occupied cell within r of (x, y)?
+// Along a row the computed distance term ddx^2 is V-shaped in ix (clo, chi
+// and the roundings are monotone), flat at 0 over the cell(s) holding x, so
+// the row's minimum is at the nearest occupied cell on either side of that
+// valley.  The valley is within one cell of cx = floor(x / cell), so the
+// candidates are the occupied cells among cx-1..cx+1 plus the nearest one
+// beyond each side -- the same answer as testing every occupied cell.
+__device__ __forceinline__ bool row_hits(const MapView& mv, double x, double y, int iy, int ix0,
+                                         int ix1, int cx, double cell, double r2) {
+  const uint32_t* rowp = mv.bits + iy * mv.WW;
+  const int width = ix1 - ix0 + 1;
+  if (width <= 32) {
+    // the row's bbox cells as one 32-bit window starting at ix0
+    const int w0 = ix0 >> 5, sh = ix0 & 31;
+    const uint32_t lo = rowp[w0], hi = w0 + 1 < mv.WW ? rowp[w0 + 1] : 0u;
+    uint32_t m = __funnelshift_r(lo, hi, sh);
+    if (width < 32) m &= (1u << width) - 1u;
+    if (!m) return false;
+    const int c = cx - ix0;  // the centre column in the window
+    const int a0 = max(c - 1, 0), a1 = min(c + 1, width - 1);
+    if (a0 <= a1) {  // occupied cells among c-1 .. c+1
+      uint32_t near = (m >> a0) & ((1u << (a1 - a0 + 1)) - 1u);
+      while (near) {
+        const int b = __ffs(near) - 1;
+        near &= near - 1;
+        if (cell_within(x, y, ix0 + a0 + b, iy, cell, r2)) return true;
       }
+    }
+    if (c - 1 > 0) {  // the nearest occupied cell left of c-1
+      const uint32_t left = m & ((1u << min(c - 1, 31)) - 1u);
+      if (left && cell_within(x, y, ix0 + 31 - __clz(left), iy, cell, r2)) return true;
+    }
+    if (c + 2 < width) {  // ... and right of c+1
+      const uint32_t right = c + 2 <= 0 ? m : (m & ~((1u << (c + 2)) - 1u));
+      if (right && cell_within(x, y, ix0 + __ffs(right) - 1, iy, cell, r2)) return true;
+    }
+    return false;
+  }
+  for (int w = ix0 >> 5; w <= (ix1 >> 5); ++w) {  // wide bboxes: every occupied cell
+    uint32_t m = rowp[w];
+    const int lo = w << 5;
+    if (ix0 > lo) m &= ~0u << (ix0 - lo);
+    if (ix1 - lo < 31) m &= (2u << (ix1 - lo)) - 1u;
+    while (m) {
+      const int ix = lo + __ffs(m) - 1;
+      m &= m - 1;
+      if (cell_within(x, y, ix, iy, cell, r2)) return true;
     }
   }
   return false;
+}
+
+// disc_collides for one disc (_cy.pyx:109-158), exact fp64 test, for every
+// calling lane of a warp: the cell table proves most discs free with one
+// lookup; each remaining disc is tested by all calling lanes together, one
+// bbox row per lane (a disc near a wall has ~2r/cell rows; one lane walking
+// them all kept its whole warp waiting for microseconds).
+__device__ __forceinline__ bool disc_hits(const MapView& mv, const EnvDev& d, double x, double y) {
+  const double r = d.radius, cell = d.cell;
+  bool res = false, decided = true;
+  if (x - r < 0.0 || y - r < 0.0 || x + r > (double)d.W * cell || y + r > (double)d.H * cell) {
+    res = true;  // :124-126
+  } else {
+    const int cx = (int)floor(x * d.inv_cell), cy = (int)floor(y * d.inv_cell);
+    decided = false;
+    if (cx >= 0 && cx < d.W && cy >= 0 && cy < d.H) {
+      const uint32_t code = mv.code(cx, cy);  // free box of radius code covers the bbox?
+      if ((code & 0x80u) == 0u && code >= (uint32_t)d.need_k) decided = true;
+    }
+  }
+  const unsigned act = __activemask();
+  unsigned pend = __ballot_sync(act, !decided);
+  const int nact = __popc(act), rank = __popc(act & lanemask_lt());
+  const double r2 = dmul(r, r);
+  while (pend) {
+    const int src = __ffs(pend) - 1;
+    pend &= pend - 1;
+    const double xs = __shfl_sync(act, x, src), ys = __shfl_sync(act, y, src);
+    int ix0 = (int)floor(ddiv(dsub(xs, r), cell)); if (ix0 < 0) ix0 = 0;  // :128-135
+    int ix1 = (int)floor(ddiv(dadd(xs, r), cell)); if (ix1 > d.W - 1) ix1 = d.W - 1;
+    int iy0 = (int)floor(ddiv(dsub(ys, r), cell)); if (iy0 < 0) iy0 = 0;
+    int iy1 = (int)floor(ddiv(dadd(ys, r), cell)); if (iy1 > d.H - 1) iy1 = d.H - 1;
+    const int cxs = (int)floor(xs * d.inv_cell);
+    bool hit = false;
+    for (int iy = iy0 + rank; iy <= iy1 && !hit; iy += nact)
+      hit = row_hits(mv, xs, ys, iy, ix0, ix1, cxs, cell, r2);
+    hit = __any_sync(act, hit);
+    if ((int)(threadIdx.x & 31) == src) res = hit;
+  }
+  return res;
 }
 
 // ---------------------------------------------- debug phase timestamps ---
@@ -158,8 +223,18 @@ __device__ __forceinline__ bool disc_hits(const MapView& mv, const EnvDev& d, do
 // memory (a global store could stall behind the CTA's queued row stores and
 // skew the stamps), copied out at the kernel's end.
 #ifdef SP_TIMING
-__device__ unsigned long long g_sp_ts[1024][48];
-__shared__ unsigned long long s_sp_ts[48];  // [12 + w]: warp w arrives at the end of phase A
+// [12 + w]: warp w arrives at the end of phase A; per warp w (lane 0, after
+// the barrier / phase named): [48 + w] leaves order_entries, [72 + w] enters
+// the ray phase, [96 + w] leaves it (before the barrier)
+constexpr int kTs = 160;
+__device__ unsigned long long g_sp_lane[5][148][768];  // per-lane debug clocks (points 0..4)
+// per-lane clock once `dep` is available (the add waits on it; in-order issue)
+#define SP_LSTAMP(p, dep) do { double t0_; \
+  asm volatile("add.f64 %0, %1, 0d0000000000000000;" : "=d"(t0_) : "d"((double)(dep))); \
+  unsigned long long t_; asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_) :: "memory"); \
+  if (blockIdx.x < 148) g_sp_lane[p][blockIdx.x][threadIdx.x] = t_ + (t0_ == 1.25e300 ? 1 : 0); } while (0)  // [120..127]: extra debug stamps, [128 + w]: warp w past its reset decisions
+__device__ unsigned long long g_sp_ts[1024][kTs];
+__shared__ unsigned long long s_sp_ts[kTs];
 __device__ __forceinline__ void sp_stamp(int k) {
   if (threadIdx.x == 0) {
     unsigned long long t;
@@ -175,15 +250,22 @@ __device__ __forceinline__ void sp_stamp_flush() {
     s_sp_ts[37] = g;
   }
   __syncthreads();
-  if (threadIdx.x < 48 && blockIdx.x < 1024) g_sp_ts[blockIdx.x][threadIdx.x] = s_sp_ts[threadIdx.x];
+  for (int k = threadIdx.x; k < kTs; k += blockDim.x)
+    if (blockIdx.x < 1024) g_sp_ts[blockIdx.x][k] = s_sp_ts[k];
 }
 #define SP_STAMP(k) sp_stamp(k)
+// lane 0 of every warp stamps slot base + warp
+#define SP_WSTAMP(base) do { if ((threadIdx.x & 31) == 0) { unsigned long long t_; \
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_)::"memory"); \
+  s_sp_ts[(base) + (threadIdx.x >> 5)] = t_; } } while (0)
 // env thread 0 inside step_env (slots 38..)
 #define SP_ESTAMP(k) do { if (threadIdx.x == 0) { unsigned long long t_; \
   asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_)::"memory"); s_sp_ts[k] = t_; } } while (0)
 #else
 #define SP_ESTAMP(k)
+#define SP_LSTAMP(p, dep)
 #define SP_STAMP(k)
+#define SP_WSTAMP(base)
 #endif
 
 // ---------------------------------------------------------------- rays ---
@@ -893,6 +975,7 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
     r.live = true;
     // delay queue (core.py:176-182): matured = action issued `delay` steps ago
     SP_ESTAMP(38);
+    SP_LSTAMP(0, x + vl + k + (double)delay + (double)step + (double)av);
     uint32_t code = (uint32_t)av;
     if (delay > 0) {
       const int q = delay - 1;
@@ -931,10 +1014,12 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
     h = wrap_angle(h1);
     // events (core.py:189-201)
     SP_ESTAMP(39);
+    SP_LSTAMP(1, x + y);
     if (mpar >= 0) mbar_wait(mbar, (uint32_t)mpar);  // the map tables (staged during the loads above)
     SP_ESTAMP(40);
     const bool coll = disc_hits(mv, d, x, y);
     SP_ESTAMP(41);
+    SP_LSTAMP(2, coll ? 1.0 : 0.0);
     const double gdx = dsub(mc.goal_x, x), gdy = dsub(mc.goal_y, y);
     const double d1 = __dsqrt_rn(dadd(dmul(gdx, gdx), dmul(gdy, gdy)));
     const bool arrived = !coll && d1 <= mc.goal_r;
@@ -942,6 +1027,7 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
     const bool timed_out = !coll && !arrived && step >= d.timeout;
     r.ev = coll ? 1 : (arrived ? 2 : (timed_out ? 3 : 0));
     r.ended = coll || arrived || timed_out;
+    SP_LSTAMP(3, (double)r.ev);
     // the episode constants read from here on arrived by cp.async into this
     // env's (not yet registered) scan-slot words at chunk start
     asm volatile("cp.async.wait_all;" ::: "memory");
@@ -1208,10 +1294,13 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     order_entries(d, c, n_slots, cta_grp());
 #endif
     SP_STAMP(11);
+    SP_WSTAMP(48);
     noise_phase(d, c, n_slots, kpre, cta_grp());
     __syncthreads();
     SP_STAMP(4);
+    SP_WSTAMP(72);
     ray_phase<kSmem, kRec>(mv, d, c, beam, c.ctl[20], fin);
+    SP_WSTAMP(96);
     __syncthreads();
     SP_STAMP(5);
     store_history(d, c, n_slots);
