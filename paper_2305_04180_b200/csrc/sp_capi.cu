@@ -224,11 +224,13 @@ static std::vector<int64_t> cta_ranges(const std::vector<int64_t>& off, int G) {
 // shared-memory bytes of a chunk with `cap` envs (layout of chunk_smem)
 static int extra_slots(int cap) { return std::max(32, cap / 8); }
 static size_t chunk_bytes(int cap, int D, int R) {
-  // layout of chunk_smem: 109 B per scan slot, 30 B per env, control words
-  const size_t slots = (size_t)cap + extra_slots(cap);
+  // layout of chunk_smem (chunk_offsets): 109 B per scan slot, 30 B per env,
+  // control words
   (void)R;
   (void)D;
-  return slots * 109 + 30 * (size_t)cap + 96 + 16;
+  uint32_t o[sp::CF_N];
+  sp::chunk_offsets(0, cap, cap + extra_slots(cap), o);
+  return (size_t)o[sp::CF_END] + 16;
 }
 
 static Plan plan_launch(SpEnv* env, const std::vector<int64_t>& off, bool staging = true) {
@@ -278,6 +280,7 @@ static void apply_plan(const Plan& p, EnvDev& d) {
   d.off_chunk = d.off_bar + 128;
   d.chunk_cap = p.chunk_cap;
   d.slot_cap = p.slot_cap;
+  chunk_offsets(d.off_chunk, p.chunk_cap, p.slot_cap, d.co);
   d.smem_maps = p.smem_maps;
 }
 

@@ -112,6 +112,17 @@ __device__ __forceinline__ int table_code(const MapView& mv, int a) {
   }
 }
 
+// atomicAdd(ctr, 1) for every calling lane of a warp with one shared-memory
+// atomic (consecutive values in lane order).
+__device__ __forceinline__ int warp_inc(int* ctr) {
+  const unsigned m = __activemask();
+  const int leader = __ffs(m) - 1;
+  int base = 0;
+  if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(ctr, __popc(m));
+  base = __shfl_sync(m, base, leader);
+  return base + __popc(m & lanemask_lt());
+}
+
 // The reference's nearest-point test of one occupied cell (_cy.pyx:141-153).
 __device__ __forceinline__ bool cell_within(double x, double y, int ix, int iy, double cell,
                                             double r2) {
@@ -437,6 +448,8 @@ struct Chunk {
   int32_t* xslot;  // per env: post-reset slot, -1 if none
   int* ctl;        // [0] ray-queue head [1] slots listed [2] extra slots used [3] overflow
                    // [4..11] bucket counts, [12..19] bucket offsets, [20] entries listed
+                   // late resets: [21] env lanes past their reset decision, [22] late
+                   // queue entries, [23] late slots claimed
   int32_t* rowi;   // per env: caller row
   int32_t* send;   // per env: episode length before any reset
   uint16_t* list;  // (slot << 3 | group) entries in dispatch order (longest predicted first)
@@ -445,22 +458,22 @@ struct Chunk {
   uint8_t* prox;   // per slot: some ray ended closer than the proximity range
 };
 
-__device__ __forceinline__ Chunk chunk_smem(uint8_t* base, int cap, int slots) {
+__device__ __forceinline__ Chunk chunk_smem(uint8_t* smem, const EnvDev& d) {
   Chunk c;
-  c.rec = (SlotRec*)base;
-  c.retp = (double*)(c.rec + slots);
-  c.part = c.retp + cap;
-  c.gid = (uint32_t*)(c.part + cap);
-  c.reg = (int32_t*)(c.gid + slots);
-  c.hwrite = c.reg + slots;
-  c.xslot = c.hwrite + slots;
-  c.ctl = c.xslot + cap;
-  c.rowi = c.ctl + 24;
-  c.send = c.rowi + cap;
-  c.list = (uint16_t*)(c.send + cap);
-  c.wmode = (uint8_t*)(c.list + 8 * slots);
-  c.evs = (int8_t*)(c.wmode + cap);
-  c.prox = (uint8_t*)(c.evs + cap);
+  c.rec = (SlotRec*)(smem + d.co[CF_REC]);
+  c.retp = (double*)(smem + d.co[CF_RETP]);
+  c.part = (double*)(smem + d.co[CF_PART]);
+  c.gid = (uint32_t*)(smem + d.co[CF_GID]);
+  c.reg = (int32_t*)(smem + d.co[CF_REG]);
+  c.hwrite = (int32_t*)(smem + d.co[CF_HWRITE]);
+  c.xslot = (int32_t*)(smem + d.co[CF_XSLOT]);
+  c.ctl = (int*)(smem + d.co[CF_CTL]);
+  c.rowi = (int32_t*)(smem + d.co[CF_ROWI]);
+  c.send = (int32_t*)(smem + d.co[CF_SEND]);
+  c.list = (uint16_t*)(smem + d.co[CF_LIST]);
+  c.wmode = smem + d.co[CF_WMODE];
+  c.evs = (int8_t*)(smem + d.co[CF_EVS]);
+  c.prox = smem + d.co[CF_PROX];
   return c;
 }
 
@@ -482,16 +495,23 @@ __device__ __forceinline__ int group_bucket(uint64_t pred, int g) {
 
 constexpr uint64_t kNoHistory = 0x8080808080808080ull;  // every group "longest"
 
-// queue index q -> (slot, beam) of its (slot, group) entry
-__device__ __forceinline__ int beam_of(const Chunk& c, int q, int gs, int& slot) {
-  SP_CHECK((q >> gs) < c.ctl[20]);
-  const uint32_t e = c.list[q >> gs];
+// List entries reserved ahead of the ordered ones for late-reset entries
+// (reset_late): at most every spare slot's groups.
+__device__ __forceinline__ int late_reserve(const EnvDev& d) {
+  return (d.slot_cap - d.chunk_cap) * d.n_groups;
+}
+
+// queue index q -> (slot, beam) of its (slot, group) entry in qlist
+__device__ __forceinline__ int beam_of(const uint16_t* qlist, int q, int gs, int n_ent, int& slot) {
+  SP_CHECK((q >> gs) < n_ent);
+  (void)n_ent;
+  const uint32_t e = qlist[q >> gs];
   slot = (int)(e >> 3);
   return (int)((e & 7u) << gs) + (q & ((1 << gs) - 1));
 }
 
-// CTA-wide ray queue over n_ent (slot, group) entries (c.list) x gb beams:
-// queue index q -> entry c.list[q >> gshift], beam (group << gshift) + (q & (gb - 1));
+// CTA-wide ray queue over n_ent (slot, group) entries (qlist) x gb beams:
+// queue index q -> entry qlist[q >> gshift], beam (group << gshift) + (q & (gb - 1));
 // beams >= R (a partial last group) are skipped.  fin(slot, j, t, hit).
 // Every thread of the CTA must call it.  Each lane marches two independent
 // rays (slots A and B) so one ray's fp64 dependency chain hides behind the
@@ -500,7 +520,8 @@ __device__ __forceinline__ int beam_of(const Chunk& c, int q, int gs, int& slot)
 // same branch, so per-ray setup/finish code runs at high SIMT occupancy.
 template <bool kSmem, bool kHit, class Fin>
 __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, const Chunk& c,
-                                          const double2* beam, int n_ent, const Fin& fin) {
+                                          const double2* beam, const uint16_t* qlist, int n_ent,
+                                          const Fin& fin) {
   const int R = d.R;
   const int gs = d.gshift;
   const int total = n_ent << gs;
@@ -550,7 +571,7 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
         }
         const int my_a = base + __popc(ia & lt);
         const int my_b = base + na + __popc(ib & lt);
-        if (fin_a && my_a < total && (ja = beam_of(c, my_a, gs, ea)) < R) {
+        if (fin_a && my_a < total && (ja = beam_of(qlist, my_a, gs, n_ent, ea)) < R) {
           za = fin.pre(ea, ja);
           if (ray_setup(ra, c.rec[ea].px, c.rec[ea].py, c.rec[ea].ch, c.rec[ea].sh, beam[ja], d, mv)) {
             fin(ea, ja, 0.0, -1, 1, za);  // origin outside the grid: range 0 (_cy.pyx:37-39)
@@ -560,7 +581,7 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
             fin_a = false;
           }
         }
-        if (fin_b && my_b < total && (jb = beam_of(c, my_b, gs, eb)) < R) {
+        if (fin_b && my_b < total && (jb = beam_of(qlist, my_b, gs, n_ent, eb)) < R) {
           zb = fin.pre(eb, jb);
           if (ray_setup(rb, c.rec[eb].px, c.rec[eb].py, c.rec[eb].ch, c.rec[eb].sh, beam[jb], d, mv)) {
             fin(eb, jb, 0.0, -1, 1, zb);
@@ -595,9 +616,11 @@ __device__ __forceinline__ void ray_phase(const MapView& mv, const EnvDev& d, co
 
 // Refresh the lanes' step-level history from this chunk's scans (after a ray
 // phase, before its slots are reused): the n_slots registered slots c.reg[].
-__device__ __forceinline__ void store_history(const EnvDev& d, const Chunk& c, int n_slots) {
-  for (int k = threadIdx.x; k < n_slots; k += blockDim.x) {
-    const int slot = c.reg[k];
+__device__ __forceinline__ void store_history(const EnvDev& d, const Chunk& c, int n_slots,
+                                              int n_late_slots = 0) {
+  for (int k = threadIdx.x; k < n_slots + n_late_slots; k += blockDim.x) {
+    // late-reset slots (reset_late; hwrite -1 after a failed spawn) follow
+    const int slot = k < n_slots ? c.reg[k] : d.chunk_cap + (k - n_slots);
     const int hw = c.hwrite[slot];
     if (hw >= 0) d.qhist[hw] = c.rec[slot].qacc;
   }
@@ -620,7 +643,7 @@ __device__ __forceinline__ Grp cta_grp() { return Grp{(int)threadIdx.x, (int)blo
 // predicted first; c.ctl[20] = entries listed.  Warp-aggregated atomics: one
 // shared atomic per bucket present in a warp's 32 entries.
 __device__ __forceinline__ void order_entries(const EnvDev& d, const Chunk& c, int n_slots,
-                                              const Grp& g) {
+                                              const Grp& g, uint16_t* out) {
   int* cnt = c.ctl + 4;
   int* off = c.ctl + 12;
   const int G = d.n_groups;
@@ -660,9 +683,9 @@ __device__ __forceinline__ void order_entries(const EnvDev& d, const Chunk& c, i
     if (b < 8 && lane == leader) pos = atomicAdd(&off[b], __popc(peers));
     pos = __shfl_sync(SP_FULL, pos, leader);
     SP_CHECK(b >= 8 || pos + __popc(peers & lt) < 8 * d.slot_cap);
-    if (b < 8) c.list[pos + __popc(peers & lt)] = (uint16_t)((slot << 3) | (k & 7));
+    if (b < 8) out[pos + __popc(peers & lt)] = (uint16_t)((slot << 3) | (k & 7));
   }
-  g.sync();  // c.list complete before anyone dispatches from it
+  g.sync();  // the list complete before anyone dispatches from it
 }
 
 __device__ __forceinline__ void set_error(const EnvDev& d, int code, int64_t row) {
@@ -876,7 +899,8 @@ __device__ __forceinline__ MapView bind_map(const EnvDev& d, int m, uint8_t* sme
 // Register a scan slot: origin, heading, noise stream position; queue it.
 __device__ __forceinline__ void add_slot(const EnvDev& d, const Chunk& c, int slot, double x,
                                          double y, double ch, double sh, double sig, uint32_t gid,
-                                         uint64_t nctr, int32_t hwrite, float* o0, float* o1) {
+                                         uint64_t nctr, int32_t hwrite, float* o0, float* o1,
+                                         bool reg = true) {
   SP_CHECK(slot >= 0 && slot < d.slot_cap && c.ctl[1] < d.slot_cap);
   c.rec[slot].out0 = o0;
   c.rec[slot].out1 = o1;
@@ -886,7 +910,7 @@ __device__ __forceinline__ void add_slot(const EnvDev& d, const Chunk& c, int sl
   c.rec[slot].nctr = nctr;
   c.prox[slot] = 0;
   c.rec[slot].qacc = 0;
-  c.reg[atomicAdd(&c.ctl[1], 1)] = slot;
+  if (reg) c.reg[atomicAdd(&c.ctl[1], 1)] = slot;  // else a late reset: queued by reset_late
 }
 
 // core.py:114-156 for one lane (stream bound to gid): resample, spawn, write
@@ -894,7 +918,7 @@ __device__ __forceinline__ void add_slot(const EnvDev& d, const Chunk& c, int sl
 // noise blocks follow the reset draws, core.py:159-160).  false = no spawn.
 __device__ __forceinline__ bool reset_env(const EnvDev& d, const MapView& mv, const MapConst& mc,
                                           int64_t s, uint32_t gid, uint64_t& ctr, const Chunk& c,
-                                          int slot, float* orow) {
+                                          int slot, float* orow, bool reg = true) {
   const double* rg = d.ranges + (d.ranges_shared ? 0 : 12 * s);
   // DiversityRanges.sample (params.py:112-121): U U I U U U
   const double k = draw_uniform(stream_block(d.seed, gid, 0u, ctr++), rg[0], rg[1]);
@@ -929,7 +953,7 @@ __device__ __forceinline__ bool reset_env(const EnvDev& d, const MapView& mv, co
   header_row(mc, x, y, bearing_error(x, y, th, mc.goal_x, mc.goal_y), c0, s0, 0.0, 0.0, vml, vma,
              orow, nullptr);
   c.rec[slot].qpred = kNoHistory;  // a fresh spawn has no step history: ranks longest
-  add_slot(d, c, slot, x, y, c0, s0, sig, gid, ctr, (int32_t)s, orow, nullptr);
+  add_slot(d, c, slot, x, y, c0, s0, sig, gid, ctr, (int32_t)s, orow, nullptr, reg);
   ctr += d.nb;
   return true;
 }
@@ -950,6 +974,7 @@ enum : uint8_t {
 // ctr advances past the draws used; the caller stores it.
 struct StepA {
   bool live = false, ended = false;
+  bool handed = false;  // the reset warp owns the env's state from the decision on
   int8_t ev = 0;
   int32_t step_end = 0;  // episode length before any reset
   double partial = 0.0;  // shaped reward minus the proximity term
@@ -958,7 +983,8 @@ struct StepA {
 __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, const MapView& mv,
                                           const MapConst& mc, const Chunk& c, int e, int64_t s,
                                           int64_t row, uint32_t gid, uint64_t& ctr, int64_t av,
-                                          int cap, int slot_cap, uint64_t* mbar, int mpar) {
+                                          int cap, int slot_cap, uint64_t* mbar, int mpar,
+                                          bool late) {
   StepA r;
   // the lane state is loaded before the action checks, so its DRAM round
   // trip overlaps the action load
@@ -969,8 +995,10 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
   const uint8_t nr = d.needs_reset[s];
   if (av < 0 || av >= d.n_actions) {
     set_error(d, SP_EACTION, row);
+    if (late) warp_inc(&c.ctl[21]);
   } else if (nr) {
     set_error(d, SP_EEPISODE, row);
+    if (late) warp_inc(&c.ctl[21]);
   } else {
     r.live = true;
     // delay queue (core.py:176-182): matured = action issued `delay` steps ago
@@ -1027,6 +1055,36 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
     const bool timed_out = !coll && !arrived && step >= d.timeout;
     r.ev = coll ? 1 : (arrived ? 2 : (timed_out ? 3 : 0));
     r.ended = coll || arrived || timed_out;
+    // fused auto-reset (vecenv.py:113-114) into a spare scan slot, else the
+    // overflow pass.  With `late`, the reset is handed to the reset warp
+    // (reset_late) here, at the decision: it runs beside the rest of phase A
+    // and the ordering instead of after this lane's reward and header, and
+    // this lane leaves the episode state to it (no pose / step / counter
+    // writes below).
+    int xs = -1;
+    c.wmode[e] = W_KEEP;
+    if (r.ended && d.auto_reset) {
+      const int k2 = atomicAdd(&c.ctl[2], 1);
+      if (k2 < slot_cap - cap) {
+        xs = cap + k2;
+        if (late) {
+          // parked in the spare slot's record until reset_env fills it
+          c.rec[xs].nctr = ctr + (uint64_t)d.nb;  // after this step's post-step scan blocks
+          c.rec[xs].qpred = (uint64_t)e;
+          c.xslot[e] = xs;
+          c.wmode[e] = W_RESET_X;
+          r.handed = true;
+        }
+      } else {
+        c.wmode[e] = W_RESET_OV;  // extra slots exhausted: second pass below
+        atomicAdd(&c.ctl[3], 1);
+      }
+    }
+    if (late) {
+      __threadfence_block();  // the hand-off is visible before the count
+      __syncwarp(__activemask());
+      warp_inc(&c.ctl[21]);
+    }
     SP_LSTAMP(3, (double)r.ev);
     // the episode constants read from here on arrived by cp.async into this
     // env's (not yet registered) scan-slot words at chunk start
@@ -1057,27 +1115,86 @@ __device__ __forceinline__ StepA step_env(const EnvDev& d, const StepArgs& a, co
     add_slot(d, c, e, x, y, cos1, sin1, ep_sig, gid, ctr,
              r.ended && d.auto_reset ? -1 : (int32_t)s, o_store, o_state);
     ctr += d.nb;
-    d.x[s] = x; d.y[s] = y; d.h[s] = h; d.vl[s] = vl; d.va[s] = va;
-    d.step[s] = step;
     r.step_end = step;
-    c.wmode[e] = W_KEEP;
-    if (r.ended && d.auto_reset) {  // fused auto-reset (vecenv.py:113-114)
-      const int k2 = atomicAdd(&c.ctl[2], 1);
-      if (k2 < slot_cap - cap) {
-        const int xs = cap + k2;
-        if (reset_env(d, mv, mc, s, gid, ctr, c, xs, a.states + row * d.D)) {
-          c.xslot[e] = xs;
-          c.wmode[e] = W_RESET_X;
-        } else {
-          set_error(d, SP_EMAP, row);
-        }
+    if (!r.handed) {
+      d.x[s] = x; d.y[s] = y; d.h[s] = h; d.vl[s] = vl; d.va[s] = va;
+      d.step[s] = step;
+    }
+    if (xs >= 0 && !late) {  // inline reset (no reset warp in this chunk)
+      if (reset_env(d, mv, mc, s, gid, ctr, c, xs, a.states + row * d.D)) {
+        c.xslot[e] = xs;
+        c.wmode[e] = W_RESET_X;
       } else {
-        c.wmode[e] = W_RESET_OV;  // extra slots exhausted: second pass below
-        atomicAdd(&c.ctl[3], 1);
+        set_error(d, SP_EMAP, row);
       }
     }
   }
   return r;
+}
+
+// The late auto-resets of a chunk (step_env with `late`), by the reset warp:
+// once every env lane is past its reset decision, reset each handed-off env
+// into its spare slot (SIMT across them; the hand-off -- env, stream
+// position -- is parked in the slot's record), draw their scans' LiDAR noise,
+// and list their (slot, group) entries right-aligned in the list's reserved
+// prefix, just before the ordered entries -- while the other warps finish
+// phase A and order the chunk's post-step scans.  So the ray queue starts
+// with the fresh spawns (no step history: they rank longest).  ctl[22] =
+// entries listed, ctl[23] = slots claimed; a failed spawn (SP_EMAP) gets
+// hwrite -1 and no entries (its rows keep the post-step values).
+__device__ __forceinline__ void reset_late(const EnvDev& d, const StepArgs& a, const MapView& mv,
+                                           const MapConst& mc, const Chunk& c, int n, int64_t s0,
+                                           uint64_t* bar, int map_par) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0)
+    while (*(volatile int*)&c.ctl[21] < n) __nanosleep(64);
+  __syncwarp();
+  __threadfence_block();
+  const int cap = d.chunk_cap;
+  const int nres = min(*(volatile int*)&c.ctl[2], d.slot_cap - cap);
+  if (nres > 0) {
+    if (map_par >= 0) mbar_wait(bar, (uint32_t)map_par);
+    for (int k = lane; k < nres; k += 32) {
+      const int slot = cap + k;
+      const int e = (int)c.rec[slot].qpred;
+      uint64_t ctr = c.rec[slot].nctr;
+      const int64_t s = s0 + e;
+      const int64_t row = c.rowi[e];
+      if (!reset_env(d, mv, mc, s, (uint32_t)(d.env_id_offset + row), ctr, c, slot,
+                     a.states + row * d.D, false)) {
+        set_error(d, SP_EMAP, row);
+        c.hwrite[slot] = -1;
+      }
+      d.ctr[s] = ctr;
+    }
+    __syncwarp();
+    // LiDAR noise of the reset scans (every slot's blocks over the warp)
+    for (int it = lane; it < nres * d.nb; it += 32) {
+      const int k = it / d.nb;
+      if (c.hwrite[cap + k] >= 0) noise_block(d, c, cap + k, it - k * d.nb);
+    }
+  }
+  // the spawned slots' entries, groups in order, ending at the reserved prefix
+  const int G = d.n_groups;
+  int good_n = 0;
+  for (int k0 = 0; k0 < nres; k0 += 32)
+    good_n += __popc(__ballot_sync(SP_FULL, k0 + lane < nres && c.hwrite[cap + k0 + lane] >= 0));
+  uint16_t* dst = c.list + late_reserve(d) - good_n * G;
+  int pos = 0;
+  for (int k0 = 0; k0 < nres; k0 += 32) {
+    const int k = k0 + lane;
+    const bool good = k < nres && c.hwrite[cap + k] >= 0;
+    const unsigned m = __ballot_sync(SP_FULL, good);
+    if (good) {
+      const int at = pos + __popc(m & lanemask_lt());
+      for (int g = 0; g < G; ++g) dst[at * G + g] = (uint16_t)(((cap + k) << 3) | g);
+    }
+    pos += __popc(m);
+  }
+  if (lane == 0) {
+    c.ctl[22] = good_n * G;
+    c.ctl[23] = nres;
+  }
 }
 
 // The per-env outputs and VecEnv statistics of one live env in MODE_STEP
@@ -1130,7 +1247,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
 #endif
   double2* beam = (double2*)(smem + d.off_beam);
   uint64_t* bar = (uint64_t*)(smem + d.off_bar);
-  const Chunk c = chunk_smem(smem + d.off_chunk, d.chunk_cap, d.slot_cap);
+  const Chunk c = chunk_smem(smem, d);
   const bool plan = blockIdx.x < (unsigned)d.plan_n;
   // prologue: the beam table and the first map's constants, copied by
   // cp.async (one global round trip, no registers held)
@@ -1207,14 +1324,25 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     const int64_t av = act && a.mode == MODE_STEP ? a.actions[row] : 0;
     __syncthreads();  // the previous chunk is fully written out
     if (threadIdx.x < 4) c.ctl[threadIdx.x] = 0;
+    if (threadIdx.x >= 21 && threadIdx.x < 24) c.ctl[threadIdx.x] = 0;
     // the warps without an env pre-noise the first kpre env slots during phase
     // A, d.prenoise blocks per thread (what fits in phase A's latency: more
     // would make them its tail); every thread does the rest after phase A.
     // Only whole idle warps: a warp mixing env and noise threads runs both
     // paths one after the other and became phase A's slowest warp
     const int first_idle = (n + 31) & ~31;
+    // late resets: the first warp without an env becomes the reset warp
+    // (reset_late) when another idle warp is left for the pre-noise; the other
+    // warps then run phase A's end and the ordering on barrier 2 without it
+#ifdef SP_EXP_NOLATE  // experiment: inline resets
+    const bool late = false;
+#else
+    const bool late = a.mode == MODE_STEP && d.auto_reset && (int)blockDim.x - first_idle >= 64;
+#endif
+    const int first_pre = first_idle + (late ? 32 : 0);
+    const bool rw = late && e >= first_idle && e < first_pre;
     const int kpre = a.mode == MODE_STEP
-                         ? min(n, d.prenoise * max(0, (int)blockDim.x - first_idle) / d.nb)
+                         ? min(n, d.prenoise * max(0, (int)blockDim.x - first_pre) / d.nb)
                          : 0;
     if (act) c.rowi[e] = (int32_t)row;
     if (act && a.mode == MODE_STEP) {
@@ -1230,7 +1358,8 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       cp_async8(&c.rec[e].sig, d.psig + s);
     }
     __syncthreads();
-    if (kpre > 0 && e >= first_idle) prenoise(d, a, c, kpre, first_idle, s0, m, mstart);
+    if (kpre > 0 && e >= first_pre) prenoise(d, a, c, kpre, first_pre, s0, m, mstart);
+    if (rw) reset_late(d, a, mv, mc, c, n, s0, bar, map_par);
 
     // ---- A: physics, collision, events, reward partial, resets -----------
     if (act) {
@@ -1256,8 +1385,8 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     } else if (act) {
       const double ret_prev = d.ret[s];  // issued early: only the outputs wait on it
       const StepA r = step_env(d, a, mv, mc, c, e, s, row, gid, ctr, av, d.chunk_cap, d.slot_cap,
-                               bar, map_par);
-      d.ctr[s] = ctr;
+                               bar, map_par, late);
+      if (!r.handed) d.ctr[s] = ctr;
       if (r.live) {
         if (r.ev == 1 || r.ev == 2) {  // terminal reward: no scan needed
           finish_env(d, a, c, e, s, row, r.ev, 0.0, r.step_end, ret_prev);
@@ -1281,29 +1410,30 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       s_sp_ts[12 + (threadIdx.x >> 5)] = t;
     }
 #endif
-    __syncthreads();
-    SP_STAMP(3);
-    const int n_slots = c.ctl[1];
     // ---- N: LiDAR noise + longest-first ray order; B: LiDAR rays ------------
-#ifdef SP_EXP_SYNC2  // experiment: a bare barrier pair instead of the ordering
-    __syncthreads();
-    SP_STAMP(10);
-    if (threadIdx.x == 0) c.ctl[20] = 0;
-    __syncthreads();
-#else
-    order_entries(d, c, n_slots, cta_grp());
-#endif
-    SP_STAMP(11);
-    SP_WSTAMP(48);
-    noise_phase(d, c, n_slots, kpre, cta_grp());
+    // (all threads but the reset warp, which joins at the ray phase)
+    const int reserve = late ? late_reserve(d) : 0;
+    if (!rw) {
+      const Grp main = late ? Grp{(int)threadIdx.x - (e >= first_pre ? 32 : 0), (int)blockDim.x - 32, 2}
+                            : cta_grp();
+      main.sync();
+      SP_STAMP(3);
+      const int n_main = c.ctl[1];
+      order_entries(d, c, n_main, main, c.list + reserve);
+      SP_STAMP(11);
+      SP_WSTAMP(48);
+      noise_phase(d, c, n_main, kpre, main);
+    }
     __syncthreads();
     SP_STAMP(4);
     SP_WSTAMP(72);
-    ray_phase<kSmem, kRec>(mv, d, c, beam, c.ctl[20], fin);
+    const int n_slots = c.ctl[1];
+    const int n_late = c.ctl[22];  // late-reset entries, right before the ordered ones
+    ray_phase<kSmem, kRec>(mv, d, c, beam, c.list + reserve - n_late, c.ctl[20] + n_late, fin);
     SP_WSTAMP(96);
     __syncthreads();
     SP_STAMP(5);
-    store_history(d, c, n_slots);
+    store_history(d, c, n_slots, c.ctl[23]);
     // ---- C: reward, outputs, statistics of running / timed-out envs --------
     if (act && c.evs[e] >= 0)
       finish_env(d, a, c, e, s, c.rowi[e], c.evs[e], c.part[e], c.send[e], c.retp[e]);
@@ -1329,10 +1459,10 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
       }
       __syncthreads();
       const int n2 = c.ctl[1];
-      order_entries(d, c, n2, cta_grp());
+      order_entries(d, c, n2, cta_grp(), c.list);
       noise_phase(d, c, n2, 0, cta_grp());
       __syncthreads();
-      ray_phase<kSmem, kRec>(mv, d, c, beam, c.ctl[20], fin);
+      ray_phase<kSmem, kRec>(mv, d, c, beam, c.list, c.ctl[20], fin);
       __syncthreads();
       store_history(d, c, n2);
     }
@@ -1372,7 +1502,7 @@ __global__ void __launch_bounds__(SP_SCAN_THREADS, SP_CTAS_PER_SM)
   extern __shared__ __align__(128) uint8_t smem[];
   double2* beam = (double2*)(smem + d.off_beam);
   uint64_t* bar = (uint64_t*)(smem + d.off_bar);
-  const Chunk c = chunk_smem(smem + d.off_chunk, d.chunk_cap, d.slot_cap);
+  const Chunk c = chunk_smem(smem, d);
   for (int j = threadIdx.x; j < d.R; j += blockDim.x) beam[j] = d.beam_cs[j];
   if (threadIdx.x == 0 && kSmem) mbar_init(bar, 1);
   __syncthreads();
@@ -1410,7 +1540,7 @@ __global__ void __launch_bounds__(SP_SCAN_THREADS, SP_CTAS_PER_SM)
     }
     __syncthreads();
     const FinScan fin{q.ranges, q.hit_cell, s0, d.R};
-    ray_phase<kSmem, true>(mv, d, c, beam, n * d.n_groups, fin);
+    ray_phase<kSmem, true>(mv, d, c, beam, c.list, n * d.n_groups, fin);
     s0 += n;
   }
 }

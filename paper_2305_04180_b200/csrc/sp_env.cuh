@@ -25,6 +25,33 @@ struct MapConst {
   double inv_plan;  // 1 / plan_dist (correctly rounded; quotients use div_by)
 };
 
+// Byte offsets (from the dynamic shared-memory base) of the chunk's arrays
+// (Chunk in sp_env.cu): SlotRec rec[slots] (80 B) | double retp[cap], part[cap]
+// | u32 gid[slots] | i32 reg[slots], hwrite[slots] | i32 xslot[cap] |
+// i32 ctl[24] | i32 rowi[cap], send[cap] | u16 list[8 slots] | u8 wmode[cap],
+// evs[cap] | u8 prox[slots].  Kernel parameters, so every array address is
+// one constant-bank operand away (nothing to keep in registers).
+enum ChunkField { CF_REC, CF_RETP, CF_PART, CF_GID, CF_REG, CF_HWRITE, CF_XSLOT, CF_CTL, CF_ROWI,
+                  CF_SEND, CF_LIST, CF_WMODE, CF_EVS, CF_PROX, CF_END, CF_N };
+__host__ __device__ inline void chunk_offsets(uint32_t base, int cap, int slots, uint32_t* o) {
+  const uint32_t c = (uint32_t)cap, s = (uint32_t)slots;
+  o[CF_REC] = base;
+  o[CF_RETP] = o[CF_REC] + 80u * s;
+  o[CF_PART] = o[CF_RETP] + 8u * c;
+  o[CF_GID] = o[CF_PART] + 8u * c;
+  o[CF_REG] = o[CF_GID] + 4u * s;
+  o[CF_HWRITE] = o[CF_REG] + 4u * s;
+  o[CF_XSLOT] = o[CF_HWRITE] + 4u * s;
+  o[CF_CTL] = o[CF_XSLOT] + 4u * c;
+  o[CF_ROWI] = o[CF_CTL] + 96u;
+  o[CF_SEND] = o[CF_ROWI] + 4u * c;
+  o[CF_LIST] = o[CF_SEND] + 4u * c;
+  o[CF_WMODE] = o[CF_LIST] + 16u * s;
+  o[CF_EVS] = o[CF_WMODE] + c;
+  o[CF_PROX] = o[CF_EVS] + c;
+  o[CF_END] = o[CF_PROX] + s;
+}
+
 // Everything the step kernel reads, by value (kernel parameter).
 struct EnvDev {
   int64_t n;              // lanes (slots)
@@ -74,6 +101,7 @@ struct EnvDev {
   int32_t nb, nb_shift;   // Philox blocks of LiDAR noise per scan (ceil(R/4)); log2 or -1
   double inv_max_range;
   uint32_t off_beam, off_bar, off_chunk;  // smem offsets
+  uint32_t co[CF_N];      // chunk array offsets (chunk_offsets)
   int32_t smem_maps;      // 1: tables staged in shared memory via TMA bulk copy
   int32_t refill_min;     // ray queue: refill a warp once this many lanes idle
   int32_t prenoise;       // LiDAR noise blocks each idle thread draws during phase A
