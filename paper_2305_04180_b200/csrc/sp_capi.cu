@@ -508,7 +508,7 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
     const char* rm = std::getenv("SPARROW_REFILL_MIN");
     d.refill_min = rm ? std::max(1, std::min(64, std::atoi(rm))) : 40;
     const char* pn = std::getenv("SPARROW_PRENOISE");
-    d.prenoise = pn ? std::max(0, std::min(64, std::atoi(pn))) : 12;
+    d.prenoise = pn ? std::max(0, std::min(64, std::atoi(pn))) : 24;
   }
   Plan plan = plan_launch(env, env->map_off);
   apply_plan(plan, d);
