@@ -240,10 +240,14 @@ __device__ __forceinline__ bool disc_hits(const MapView& mv, const EnvDev& d, do
 constexpr int kTs = 160;
 __device__ unsigned long long g_sp_lane[5][148][768];  // per-lane debug clocks (points 0..4)
 // per-lane clock once `dep` is available (the add waits on it; in-order issue)
+#ifdef SP_TIMING_LANES  // per-lane clocks (perturb phase A: a global store per lane and point)
 #define SP_LSTAMP(p, dep) do { double t0_; \
   asm volatile("add.f64 %0, %1, 0d0000000000000000;" : "=d"(t0_) : "d"((double)(dep))); \
   unsigned long long t_; asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_) :: "memory"); \
-  if (blockIdx.x < 148) g_sp_lane[p][blockIdx.x][threadIdx.x] = t_ + (t0_ == 1.25e300 ? 1 : 0); } while (0)  // [120..127]: extra debug stamps, [128 + w]: warp w past its reset decisions
+  if (blockIdx.x < 148) g_sp_lane[p][blockIdx.x][threadIdx.x] = t_ + (t0_ == 1.25e300 ? 1 : 0); } while (0)
+#else
+#define SP_LSTAMP(p, dep)
+#endif
 __device__ unsigned long long g_sp_ts[1024][kTs];
 __shared__ unsigned long long s_sp_ts[kTs];
 __device__ __forceinline__ void sp_stamp(int k) {

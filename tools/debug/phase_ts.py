@@ -60,15 +60,17 @@ for n in (int(os.environ.get("N", "65536")),):
     ln = ln.astype(np.int64)
     if os.environ.get("LANES"):
         np.save(os.environ["LANES"], ln)
-    rows = []  # per env warp: the last lane past each step_env point (ns from the CTA start)
+    rows = []  # per env warp: the last lane past each step_env point (ns from the CTA start;
+    # a build with -DSP_TIMING_LANES, else all zero)
     for b in range(148):
         nb_ = int(ts[b, 8])
         for w in range((nb_ + 31) // 32):
             sl = slice(w * 32, min(nb_, (w + 1) * 32))
             rows.append([((ln[p, b, sl] - ts[b, 0]) * cyc).max() for p in range(4)])
     rows = np.array(rows)
-    print("   env warps, last lane past loads / physics / disc / events (ns, median): %s; p90: %s"
-          % (np.median(rows, 0).round().tolist(), np.percentile(rows, 90, 0).round().tolist()))
+    if ln.any():
+        print("   env warps, last lane past loads / physics / disc / events (ns, median): %s; p90: %s"
+              % (np.median(rows, 0).round().tolist(), np.percentile(rows, 90, 0).round().tolist()))
     wa = ts[:, 12:36].copy()  # per-warp phase-A arrivals (cycles), relative to the CTA start
     wa = (wa - ts[:, :1]) * (1000.0 / 1.965) / 1e6  # -> us
     ts = ts[:, :12]
