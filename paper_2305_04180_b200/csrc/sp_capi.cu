@@ -509,6 +509,8 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
     d.refill_min = rm ? std::max(1, std::min(64, std::atoi(rm))) : 40;
     const char* pn = std::getenv("SPARROW_PRENOISE");
     d.prenoise = pn ? std::max(0, std::min(64, std::atoi(pn))) : 24;
+    const char* lr = std::getenv("SPARROW_LATE_RESETS");  // tests / A/B: 0 = inline resets
+    d.late_resets = lr && lr[0] == '0' ? 0 : 1;
   }
   Plan plan = plan_launch(env, env->map_off);
   apply_plan(plan, d);

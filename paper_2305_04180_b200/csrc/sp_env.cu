@@ -1338,11 +1338,8 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
     // late resets: the first warp without an env becomes the reset warp
     // (reset_late) when another idle warp is left for the pre-noise; the other
     // warps then run phase A's end and the ordering on barrier 2 without it
-#ifdef SP_EXP_NOLATE  // experiment: inline resets
-    const bool late = false;
-#else
-    const bool late = a.mode == MODE_STEP && d.auto_reset && (int)blockDim.x - first_idle >= 64;
-#endif
+    const bool late = a.mode == MODE_STEP && d.auto_reset && d.late_resets &&
+                      (int)blockDim.x - first_idle >= 64;
     const int first_pre = first_idle + (late ? 32 : 0);
     const bool rw = late && e >= first_idle && e < first_pre;
     const int kpre = a.mode == MODE_STEP

@@ -105,6 +105,7 @@ struct EnvDev {
   int32_t smem_maps;      // 1: tables staged in shared memory via TMA bulk copy
   int32_t refill_min;     // ray queue: refill a warp once this many lanes idle
   int32_t prenoise;       // LiDAR noise blocks each idle thread draws during phase A
+  int32_t late_resets;    // 1: auto-resets by the reset warp (reset_late), 0: inline
   int32_t gshift;         // beams per dispatch group = 2^gshift (<= 8 groups per scan)
   int32_t n_groups;       // groups per scan: ceil(R / 2^gshift)
   uint64_t d_magic;       // ceil(2^40 / D): f / D for f < 2^21 (row writes)

@@ -112,3 +112,12 @@ def test_cfg3_reset_heavy():
     """Timeout 6 steps: after step 6 every env resets, far more resets per
     chunk than spare scan slots -> the overflow pass runs in every CTA."""
     _run(CFG3, 14, seed=5, timeout=6)
+
+
+@pytest.mark.parametrize("timeout", [None, 6])
+def test_inline_resets_match(monkeypatch, timeout):
+    """The inline auto-reset path (the env lane resets after its own header;
+    used when a chunk leaves no spare idle warp for the reset warp), forced
+    with SPARROW_LATE_RESETS=0, against the oracle at cfg3 and reset-heavy."""
+    monkeypatch.setenv("SPARROW_LATE_RESETS", "0")
+    _run(CFG3, 12, seed=31, timeout=timeout, check_every=3)
