@@ -95,6 +95,20 @@ def ncu_metrics():
     return d
 
 
+def smem_issued(nm: dict, n_sm: int, mhz: float) -> dict:
+    """Shared-memory wavefronts per launch (all phases, bank conflicts included)
+    over the capture's kernel duration, against one wavefront per clock per SM
+    at this run's sampled SM clock."""
+    wf, dur = nm.get("smem_wavefronts"), nm.get("duration_us")
+    if not (wf and dur and mhz):
+        return {"source": nm.get("stale") or "no capture"}
+    rate = wf / (dur * 1e-6)
+    peak = n_sm * mhz * 1e6
+    return {"wavefronts_per_launch": wf, "bank_conflicts_per_launch": nm.get("smem_bank_conflicts"),
+            "wavefronts_per_s": rate, "peak_wavefronts_per_s": peak, "frac": rate / peak,
+            "source": nm.get("source")}
+
+
 def numa_bind(local_rank: int) -> dict:
     """Bind this process to the CPUs of the GPU's NUMA node (pinned host
     buffers allocated afterwards are first-touched there), so the e2e copies
@@ -635,7 +649,11 @@ def run_ours(args, rank, world, local_rank):
                          "achieved_basis": "ray-cells per launch (N scans x R rays x pure-DDA "
                                            "cells per ray, counted from a recorded step in this "
                                            "run; reset scans not credited) x 4 B / mean launch",
-                         "kernel": "env_step_kernel", "mean_launch_ms": mean_launch * 1e3},
+                         "kernel": "env_step_kernel", "mean_launch_ms": mean_launch * 1e3,
+                         # SURVEY 8(d)'s alternative: the SMEM wavefronts the kernel
+                         # actually issues (the free-box march looks up far fewer
+                         # cells than a pure DDA enters), from the ncu capture
+                         "smem_issued": smem_issued(nm, n_sm, mhz)},
             "roofline_hbm": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak,
                              "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
