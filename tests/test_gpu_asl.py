@@ -121,6 +121,41 @@ def test_ddqn_updates_match_reference(mode):
             np.testing.assert_allclose(w.cpu().numpy(), wr, rtol=1e-4, atol=1e-6)
 
 
+@pytest.mark.parametrize("mode", ["fused", "fused_graph"])
+def test_fused_updates_chained_against_reference(mode):
+    """The fused learner run chained for 20 updates (no restarts) against the
+    reference learner on the same batches.  Adam's early steps are about
+    lr * sign(g), so an element whose gradient is within fp32 rounding of 0
+    may step the other way; every weight must therefore be within 1e-4
+    relative or 2 lr per update of the reference, and at least 99.9 % of the
+    elements of every tensor within 1e-4 relative (+1e-6 absolute).  Losses
+    and |td| agree to 1e-4 at every update."""
+    ref()
+    from color_rl import net
+    from color_rl.ddqn import DdqnConfig as RC, DdqnLearner as RL
+    from color_rl.replay import TransitionBatch as RTB
+    from paper_2305_04180_b200.asl import DdqnConfig, DdqnLearner, QNet
+    lr, n_up = 1e-4, 20
+    rl = RL(net.init_params(np.random.default_rng(5), SIZES), RC(target_sync_period=7))
+    gl = DdqnLearner(QNet.init(np.random.default_rng(5), SIZES), DdqnConfig(target_sync_period=7),
+                     **LEARNER_MODES[mode])
+    rng = np.random.default_rng(17)
+    for k in range(n_up):
+        arrs = _batch(rng, 256)
+        sr = rl.update(RTB(*arrs))
+        sg = gl.update(_tb(arrs))
+        assert sg.version == sr.version and sg.target_synced == sr.target_synced
+        np.testing.assert_allclose(sg.loss, sr.loss, rtol=1e-4)
+        np.testing.assert_allclose(sg.mean_abs_td, sr.mean_abs_td, rtol=1e-4)
+    for mine, theirs in ((gl.online.weights + gl.online.biases, rl.online.weights + rl.online.biases),
+                         (gl.target.weights + gl.target.biases, rl.target.weights + rl.target.biases)):
+        for w, wr in zip(mine, theirs):
+            a = w.cpu().numpy()
+            dev = np.abs(a - wr)
+            assert (dev <= 1e-4 * np.abs(wr) + 2 * lr * n_up).all(), float(dev.max())
+            assert (dev > 1e-4 * np.abs(wr) + 1e-6).mean() <= 1e-3, int((dev > 1e-4 * np.abs(wr) + 1e-6).sum())
+
+
 def test_fused_adam_bit_exact_vs_reference():
     """sp_adam_step over all six tensors == net.py:151-161 adam_step (numpy
     fp32, weak Python-float scalars) bit for bit, over several steps."""
