@@ -123,9 +123,12 @@ int sp_env_set_recording(SpEnv* env, int32_t* hit_store, int32_t* hit_state,
  * block of sp_env_host_out_bytes(env) bytes laid out as
  *   rewards f64[N] | states f32[N][5+R] | store_states f32[N][5+R] |
  *   dones u8[N] | truncated u8[N] | events i8[N].
- * One H2D copy of the actions, the fused step, one D2H copy of the block, all
- * on `stream` (device staging owned by the handle); returns after the stream
- * synchronized.  Page-locked host memory lets the copies run at full PCIe
+ * One H2D copy of the actions, the fused step, the D2H copy of the block
+ * (device staging owned by the handle); returns after everything synchronized.
+ * From 16,384 envs (default map assignment) the step runs as row parts: part
+ * p's launch, then its obs rows' copy on a second stream while part p + 1
+ * steps (SPARROW_HOST_PARTS sets the count, 1 = one launch and one copy on
+ * `stream`).  Page-locked host memory lets the copies run at full PCIe
  * bandwidth.  Invalid actions are reported by sp_env_check as after sp_env_step. */
 int64_t sp_env_host_out_bytes(SpEnv* env);
 int sp_env_step_host(SpEnv* env, const int64_t* h_actions, void* h_out, void* stream);

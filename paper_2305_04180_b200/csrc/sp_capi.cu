@@ -133,6 +133,13 @@ struct SpEnv {
   int32_t* rec_hit_state = nullptr;
   double* rec_scan_state = nullptr;
   unsigned long long* d_count = nullptr;  // sp_env_first_pending scratch
+  // sp_env_step_host row parts: part p's rows are stepped by a launch with the
+  // launch plan of dpart[p] (only its plan fields are used) and copied back
+  // while the next part steps
+  std::vector<EnvDev> dpart;
+  std::vector<int64_t> part_rows;  // parts + 1 row cuts
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t part_done[8] = {};
   std::mutex mu;
 
   template <class T>
@@ -148,6 +155,9 @@ struct SpEnv {
   ~SpEnv() {
     for (void* p : allocs) cudaFree(p);
     if (h_err) cudaFreeHost(h_err);
+    for (cudaEvent_t e : part_done)
+      if (e) cudaEventDestroy(e);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     if (h_scan) cudaFreeHost(h_scan);
     if (scan_copied) cudaEventDestroy(scan_copied);
   }
@@ -394,7 +404,16 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   d.bits_bytes = (uint32_t)align_up((size_t)H * d.WW * 4, 16);
   d.map_bytes = d.blk_bytes + d.bits_bytes;
   d.env_id_offset = env_id_offset;
-  d.row_affine = map_index ? 0 : 1;  // default assignment: rows follow from slots
+  // default assignment (map = (env_id_offset + row) % n_maps, also when the
+  // caller passes it explicitly, as VecEnv does): rows follow from slots
+  // arithmetically, so the kernel never loads env_of_slot
+  bool affine = true;
+  if (map_index) {
+    const int64_t om = ((env_id_offset % n_maps) + n_maps) % n_maps;
+    for (int64_t i = 0; i < n_envs && affine; ++i)
+      affine = map_index[i] == (int32_t)((om + i) % n_maps);
+  }
+  d.row_affine = affine ? 1 : 0;
   d.off_mod = (int32_t)(((env_id_offset % n_maps) + n_maps) % n_maps);
 
   // slot order: stable sort by map (map-major)
@@ -526,6 +545,7 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   if (plan.grid <= SP_PLAN_MAX && n_envs < (int64_t)1 << 31) {  // the plan rides in the params
     d.plan_n = plan.grid;
     for (int b = 0; b <= plan.grid; ++b) d.plan_begin[b] = (int32_t)plan.cta_begin[b];
+    for (int b = 0; b < plan.grid; ++b) d.plan_end[b] = (int32_t)plan.cta_begin[b + 1];
     for (int b = 0; b < plan.grid; ++b) {
       int m = 0;
       while (env->map_off[m + 1] <= plan.cta_begin[b] && m + 1 < n_maps) ++m;
@@ -538,6 +558,59 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   env->grid = plan.grid;
   env->threads = plan.threads;
   env->smem = plan.smem;
+  // sp_env_step_host row parts (default 4 from 16,384 envs; SPARROW_HOST_PARTS
+  // sets the count, 1 = off): for the default map assignment a row range holds,
+  // per map, one contiguous slot range, so each part gets its own launch plan
+  {
+    const char* hp = std::getenv("SPARROW_HOST_PARTS");
+    int parts = hp ? std::max(1, std::min(8, std::atoi(hp))) : (n_envs >= 16384 ? 4 : 1);
+    if (!(d.plan_n > 0 && d.row_affine && d.smem_maps)) parts = 1;
+    if (parts > 1) {
+      const int M = n_maps;
+      std::vector<int64_t> rows(parts + 1);
+      for (int p = 0; p <= parts; ++p) rows[p] = n_envs * p / parts;
+      std::vector<EnvDev> dps;
+      bool ok = true;
+      for (int p = 0; p < parts && ok; ++p) {
+        // per map m: slots [lo[m], hi[m]) have rows in [rows[p], rows[p + 1])
+        std::vector<int64_t> lo(M), hi(M), voff(M + 1, 0);
+        for (int m = 0; m < M; ++m) {
+          const int64_t i0 = m >= d.off_mod ? m - d.off_mod : m - d.off_mod + M;
+          const int64_t nm = env->map_off[m + 1] - env->map_off[m];
+          auto first_j = [&](int64_t r) {  // first j with i0 + j * M >= r
+            return std::min(nm, std::max<int64_t>(0, (r - i0 + M - 1) / M));
+          };
+          lo[m] = env->map_off[m] + first_j(rows[p]);
+          hi[m] = env->map_off[m] + first_j(rows[p + 1]);
+          voff[m + 1] = voff[m] + (hi[m] - lo[m]);
+        }
+        const std::vector<int64_t> vc = cta_ranges(voff, plan.grid);
+        const int G = (int)vc.size() - 1;
+        EnvDev dp = d;
+        dp.plan_n = G;
+        for (int b = 0; b < G && ok; ++b) {
+          int m = 0;
+          while (m + 1 < M && voff[m + 1] <= vc[b]) ++m;
+          if (vc[b + 1] > voff[m + 1]) ok = false;  // a CTA would span two maps
+          dp.plan_begin[b] = (int32_t)(lo[m] + (vc[b] - voff[m]));
+          dp.plan_end[b] = (int32_t)(lo[m] + (vc[b + 1] - voff[m]));
+          if (dp.plan_end[b] - dp.plan_begin[b] > d.chunk_cap) ok = false;
+          dp.plan_map[b] = (int16_t)m;
+          dp.plan_mstart[b] = (int32_t)env->map_off[m];
+          dp.plan_mend[b] = (int32_t)env->map_off[m + 1];
+        }
+        dps.push_back(dp);
+      }
+      if (ok && cudaStreamCreateWithFlags(&env->copy_stream, cudaStreamNonBlocking) == cudaSuccess) {
+        for (int p = 0; p < parts && ok; ++p)
+          ok = cudaEventCreateWithFlags(&env->part_done[p], cudaEventDisableTiming) == cudaSuccess;
+        if (ok) {
+          env->dpart = dps;
+          env->part_rows = rows;
+        }
+      }
+    }
+  }
   const void* kernels_[] = {(const void*)env_step_kernel<true, false>,
                             (const void*)env_step_kernel<false, false>,
                             (const void*)env_step_kernel<true, true>,
@@ -568,21 +641,23 @@ int sp_env_destroy(SpEnv* env) {
   return SP_OK;
 }
 
-static int launch_env(SpEnv* env, StepArgs a, cudaStream_t st) {
+static int launch_env(SpEnv* env, StepArgs a, cudaStream_t st, const EnvDev* dp = nullptr) {
+  const EnvDev& d = dp ? *dp : env->d;
+  const int grid = dp ? dp->plan_n : env->grid;
   a.hit_store = env->rec_hit_store;
   a.hit_state = env->rec_hit_state;
   a.scan_state = env->rec_scan_state;
   const bool rec = a.hit_store || a.hit_state || a.scan_state;
-  if (env->d.smem_maps) {
+  if (d.smem_maps) {
     if (rec)
-      env_step_kernel<true, true><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
+      env_step_kernel<true, true><<<grid, env->threads, env->smem, st>>>(d, a);
     else
-      env_step_kernel<true, false><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
+      env_step_kernel<true, false><<<grid, env->threads, env->smem, st>>>(d, a);
   } else {
     if (rec)
-      env_step_kernel<false, true><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
+      env_step_kernel<false, true><<<grid, env->threads, env->smem, st>>>(d, a);
     else
-      env_step_kernel<false, false><<<env->grid, env->threads, env->smem, st>>>(env->d, a);
+      env_step_kernel<false, false><<<grid, env->threads, env->smem, st>>>(d, a);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(SP_ECUDA, std::string("env_step_kernel: ") + cudaGetErrorString(e));
@@ -677,11 +752,85 @@ int sp_env_step_host(SpEnv* env, const int64_t* h_actions, void* h_out, void* st
   float* states = (float*)(o + 8 * n);
   float* store = states + n * D;
   uint8_t* dones = (uint8_t*)(store + n * D);
-  const int rc = step_locked(env, (const int64_t*)dev_act, states, store, rewards, dones,
-                             dones + n, (int8_t*)(dones + 2 * n), st);
-  if (rc != SP_OK) return rc;
-  SP_CUDA(cudaMemcpyAsync(h_out, o, out_bytes, cudaMemcpyDeviceToHost, st));
+  const int parts = (int)env->dpart.size();
+  if (parts < 2) {
+    const int rc = step_locked(env, (const int64_t*)dev_act, states, store, rewards, dones,
+                               dones + n, (int8_t*)(dones + 2 * n), st);
+    if (rc != SP_OK) return rc;
+    SP_CUDA(cudaMemcpyAsync(h_out, o, out_bytes, cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaStreamSynchronize(st));
+    return SP_OK;
+  }
+  // row parts: part p's launch, then its rows' copies on the copy stream
+  // while part p + 1 steps (the PCIe read-back is most of a host step)
+  StepArgs a{};
+  a.mode = MODE_STEP;
+  a.step_index = ++env->step_index;  // one step for every part (ring keys)
+  a.actions = (const int64_t*)dev_act;
+  a.states = states;
+  a.store_states = store;
+  a.rewards = rewards;
+  a.dones = dones;
+  a.truncated = dones + n;
+  a.events = (int8_t*)(dones + 2 * n);
+  uint8_t* h = (uint8_t*)h_out;
+#ifdef SP_HOST_TIMING  // debug: timeline of the parts (stderr)
+  cudaEvent_t tev[20];
+  for (auto& e : tev) cudaEventCreate(&e);
+  int ti = 0;
+  cudaEventRecord(tev[ti++], st);
+#endif
+  for (int p = 0; p < parts; ++p) {
+    // the handle's current parameters (seed etc.) with part p's launch plan
+    EnvDev dp = env->d;
+    const EnvDev& pp = env->dpart[p];
+    dp.plan_n = pp.plan_n;
+    std::memcpy(dp.plan_begin, pp.plan_begin, sizeof(dp.plan_begin));
+    std::memcpy(dp.plan_end, pp.plan_end, sizeof(dp.plan_end));
+    std::memcpy(dp.plan_map, pp.plan_map, sizeof(dp.plan_map));
+    std::memcpy(dp.plan_mstart, pp.plan_mstart, sizeof(dp.plan_mstart));
+    std::memcpy(dp.plan_mend, pp.plan_mend, sizeof(dp.plan_mend));
+    const int rc = launch_env(env, a, st, &dp);
+    if (rc != SP_OK) return rc;
+    SP_CUDA(cudaEventRecord(env->part_done[p], st));
+#ifdef SP_HOST_TIMING
+    cudaEventRecord(tev[ti++], st);
+#endif
+    SP_CUDA(cudaStreamWaitEvent(env->copy_stream, env->part_done[p], 0));
+    // the part's obs rows (the bulk: 2 x 148 B per row at R = 32) now; the
+    // small per-row columns once, after the last part (every copy costs ~3.5 us)
+    const int64_t r0 = env->part_rows[p], r1 = env->part_rows[p + 1], k = r1 - r0;
+    const size_t row_f = 4 * (size_t)D;
+    const size_t so = 8 * (size_t)n + row_f * r0, ro = 8 * (size_t)n + row_f * (n + r0);
+    SP_CUDA(cudaMemcpyAsync(h + so, o + so, row_f * k, cudaMemcpyDeviceToHost, env->copy_stream));
+    SP_CUDA(cudaMemcpyAsync(h + ro, o + ro, row_f * k, cudaMemcpyDeviceToHost, env->copy_stream));
+#ifdef SP_HOST_TIMING
+    cudaEventRecord(tev[ti++], env->copy_stream);
+#endif
+  }
+  {
+    const size_t row_f = 4 * (size_t)D, tail = 8 * (size_t)n + 2 * row_f * n;
+    SP_CUDA(cudaMemcpyAsync(h, o, 8 * (size_t)n, cudaMemcpyDeviceToHost, env->copy_stream));
+    SP_CUDA(cudaMemcpyAsync(h + tail, o + tail, 3 * (size_t)n, cudaMemcpyDeviceToHost,
+                            env->copy_stream));
+  }
+#ifdef SP_HOST_TIMING
+  cudaEventRecord(tev[ti++], env->copy_stream);
+#endif
+  SP_CUDA(cudaStreamSynchronize(env->copy_stream));
   SP_CUDA(cudaStreamSynchronize(st));
+#ifdef SP_HOST_TIMING
+  {
+    float ms;
+    fprintf(stderr, "parts timeline (us from start):");
+    for (int i = 1; i < ti; ++i) {
+      cudaEventElapsedTime(&ms, tev[0], tev[i]);
+      fprintf(stderr, " %.1f", ms * 1e3f);
+    }
+    fprintf(stderr, "\n");
+    for (auto& e : tev) cudaEventDestroy(e);
+  }
+#endif
   return SP_OK;
 }
 

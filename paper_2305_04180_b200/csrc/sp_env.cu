@@ -1274,7 +1274,7 @@ __global__ void __launch_bounds__(SP_CTA_THREADS, SP_CTAS_PER_SM)
   uint32_t phase = 0;
   if (threadIdx.x == 0) bar[1] = (uint64_t)clock64();  // CTA start (kept in smem, not a register)
   const int64_t sb = plan ? d.plan_begin[blockIdx.x] : d.cta_begin[blockIdx.x];
-  const int64_t se = plan ? d.plan_begin[blockIdx.x + 1] : d.cta_begin[blockIdx.x + 1];
+  const int64_t se = plan ? d.plan_end[blockIdx.x] : d.cta_begin[blockIdx.x + 1];
   const int D = d.D;
   const FinObs<kRec> fin{c, D, d.max_range, d.inv_max_range, d.proximity, a.hit_store,
                          a.hit_state, a.scan_state, a.store_states,

@@ -117,7 +117,8 @@ struct EnvDev {
   // launch plan in the parameters (constant bank): a CTA starts without a
   // global-memory round trip.  plan_n == 0: read cta_begin / map_off instead
   int32_t plan_n;
-  int32_t plan_begin[SP_PLAN_MAX + 1];  // slot range of CTA b: [begin[b], begin[b+1])
+  int32_t plan_begin[SP_PLAN_MAX + 1];  // slot range of CTA b: [begin[b], end[b])
+  int32_t plan_end[SP_PLAN_MAX];        // = begin[b + 1], except in a part plan (row parts)
   int32_t plan_mstart[SP_PLAN_MAX];     // map_off[map of the CTA's first slot]
   int32_t plan_mend[SP_PLAN_MAX];       // map_off[that map + 1]
   int16_t plan_map[SP_PLAN_MAX];        // that map

@@ -479,6 +479,31 @@ def test_step_host_matches_device_step():
         b_env.step_host(np.full(n, 7))
 
 
+@pytest.mark.parametrize("n,parts", [(65_536, None), (4_096, "3"), (3_000, "8")])
+def test_step_host_row_parts_match_device_step(monkeypatch, n, parts):
+    """sp_env_step_host in row parts (a launch per part, each part's rows read
+    back while the next part steps; 2 parts by default from 16,384 envs,
+    SPARROW_HOST_PARTS otherwise) gives the device step's StepBatch, and the
+    two handles' episode statistics agree."""
+    from paper_2305_04180_b200 import VecEnv
+    if parts:
+        monkeypatch.setenv("SPARROW_HOST_PARTS", parts)
+    maps = load_maps(16)
+    a_env = VecEnv(maps, n, ranges(0.3), config(32, timeout_steps=9))
+    b_env = VecEnv(maps, n, ranges(0.3), config(32, timeout_steps=9))
+    a_env.reset_all(5)
+    b_env.reset_all(5)
+    for t in range(12):
+        acts = random_actions(5, np.arange(n), t)
+        x = a_env.step_batch(acts)
+        y = b_env.step_host(acts)
+        for f in ("states", "store_states", "rewards", "dones", "truncated", "events"):
+            assert np.array_equal(getattr(x, f).cpu().numpy(), getattr(y, f)), (t, f)
+    sa, sb = a_env.snapshot_stats(), b_env.snapshot_stats()
+    assert (sa.episodes, sa.arrivals) == (sb.episodes, sb.arrivals)
+    assert list(sa.recent_returns) == list(sb.recent_returns)
+
+
 def test_reset_clears_terminal_flag_and_velocity():  # test_env.py:282-296
     env = make_env(40, cfg=EnvConfig(timeout_steps=3))
     env.reset(17)
