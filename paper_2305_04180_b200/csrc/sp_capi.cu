@@ -133,6 +133,13 @@ struct SpEnv {
   int32_t* rec_hit_state = nullptr;
   double* rec_scan_state = nullptr;
   unsigned long long* d_count = nullptr;  // sp_env_first_pending scratch
+  // one-shot re-plan (replan_by_cost): the CTA cycles of the third step launch,
+  // read back asynchronously, give each map's cost; CTAs are then allocated
+  // to maps by cost instead of by lane count
+  int replan_state = 0;  // 0 waiting, 1 cycles in flight, 2 done (or off)
+  uint64_t step_launches = 0;
+  uint32_t* cyc_host = nullptr;  // pinned, grid
+  cudaEvent_t cyc_ready = nullptr;
   // sp_env_step_host row parts: part p's rows are stepped by a launch with the
   // launch plan of dpart[p] (only its plan fields are used) and copied back
   // while the next part steps
@@ -155,6 +162,8 @@ struct SpEnv {
   ~SpEnv() {
     for (void* p : allocs) cudaFree(p);
     if (h_err) cudaFreeHost(h_err);
+    if (cyc_host) cudaFreeHost(cyc_host);
+    if (cyc_ready) cudaEventDestroy(cyc_ready);
     for (cudaEvent_t e : part_done)
       if (e) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
@@ -185,9 +194,11 @@ struct Plan {
 };
 
 // CTA slot ranges: every CTA stays inside one map when there are at most as
-// many non-empty maps as CTAs (CTAs per map proportional to its lanes,
-// largest remainder); otherwise equal contiguous splits.
-static std::vector<int64_t> cta_ranges(const std::vector<int64_t>& off, int G) {
+// many non-empty maps as CTAs (CTAs per map proportional to its lanes -- or
+// to the map's measured cost `w` when given -- largest remainder); otherwise
+// equal contiguous splits.
+static std::vector<int64_t> cta_ranges(const std::vector<int64_t>& off, int G,
+                                       const std::vector<double>* w = nullptr) {
   const int M = (int)off.size() - 1;
   const int64_t N = off[M] - off[0];
   std::vector<int64_t> b;
@@ -198,26 +209,34 @@ static std::vector<int64_t> cta_ranges(const std::vector<int64_t>& off, int G) {
     for (int c = 0; c <= G; ++c) b.push_back(off[0] + N * c / G);
     return b;
   }
+  // a map's load: its lanes, or its measured cost (zero for an empty map)
+  std::vector<double> ld(M);
+  double L = 0.0;
+  for (int m = 0; m < M; ++m) {
+    const int64_t nm = off[m + 1] - off[m];
+    ld[m] = nm == 0 ? 0.0 : (w ? std::max((*w)[m], 1e-9) : (double)nm);
+    L += ld[m];
+  }
   std::vector<int> g(M, 0);
   int used = 0;
   for (int m = 0; m < M; ++m) {
     const int64_t nm = off[m + 1] - off[m];
     if (nm == 0) continue;
-    g[m] = std::max<int>(1, (int)(nm * G / N));
+    g[m] = std::max<int>(1, (int)(ld[m] * G / L));
     used += g[m];
   }
   while (used > G) {  // too many after the min-1 rule: trim the best-served map
     int best = -1;
     for (int m = 0; m < M; ++m)
-      if (g[m] > 1 && (best < 0 || (off[m + 1] - off[m]) * g[best] < (off[best + 1] - off[best]) * g[m])) best = m;
+      if (g[m] > 1 && (best < 0 || ld[m] * g[best] < ld[best] * g[m])) best = m;
     if (best < 0) break;
     --g[best];
     --used;
   }
-  while (used < G) {  // hand spare CTAs to the map with the most lanes per CTA
+  while (used < G) {  // hand spare CTAs to the map with the most load per CTA
     int best = -1;
     for (int m = 0; m < M; ++m)
-      if (g[m] > 0 && (best < 0 || (off[m + 1] - off[m]) * g[best] > (off[best + 1] - off[best]) * g[m])) best = m;
+      if (g[m] > 0 && (best < 0 || ld[m] * g[best] > ld[best] * g[m])) best = m;
     const int64_t nm = off[best + 1] - off[best];
     if (g[best] >= nm) break;
     ++g[best];
@@ -555,6 +574,14 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
     }
     if (n_maps > 32767) d.plan_n = 0;
   }
+  {
+    const char* rpe = std::getenv("SPARROW_REPLAN");  // 0: keep the lane-count plan
+    env->replan_state = 2;
+    if (d.plan_n > 0 && !(rpe && rpe[0] == '0') &&
+        cudaMallocHost(&env->cyc_host, 4 * (size_t)d.plan_n) == cudaSuccess &&
+        cudaEventCreateWithFlags(&env->cyc_ready, cudaEventDisableTiming) == cudaSuccess)
+      env->replan_state = 0;
+  }
   env->grid = plan.grid;
   env->threads = plan.threads;
   env->smem = plan.smem;
@@ -641,7 +668,76 @@ int sp_env_destroy(SpEnv* env) {
   return SP_OK;
 }
 
+// Allocate the step's CTAs to maps by measured cost (one CTA's time = a fixed
+// part, ~40 % of the median, + its envs' variable cost): the maps' costs
+// differ by +-5 % and the pattern persists from step to step, so the extra
+// CTAs go to the costliest maps.  Cuts inside a map stay equal-count; results
+// do not depend on the plan (every lane's computation is its own).
+static void replan_by_cost(SpEnv* env) {
+  EnvDev& d = env->d;
+  const int G = d.plan_n, M = env->n_maps;
+  std::vector<double> y(env->cyc_host, env->cyc_host + G), ys = y;
+  std::nth_element(ys.begin(), ys.begin() + G / 2, ys.end());
+  const double F = 0.4 * ys[G / 2];
+  std::vector<double> w(M, 0.0);
+  for (int b = 0; b < G; ++b) w[d.plan_map[b]] += std::max(y[b] - F, 0.05 * y[b]);
+  // per map cost per lane (normalised by its lanes: the maps' lane counts may
+  // differ), then only the spare CTAs move: every map keeps the count the
+  // lane plan gives the smallest-served map, the G % M extra ones go to the
+  // costliest maps (one step's estimate is noisy, so never fewer CTAs than a
+  // lane-count plan would give)
+  std::vector<int> g(M, 0);
+  for (int b = 0; b < G; ++b) ++g[d.plan_map[b]];
+  int base = G;
+  for (int m = 0; m < M; ++m)
+    if (env->map_off[m + 1] > env->map_off[m]) base = std::min(base, g[m]);
+  int used = 0;
+  for (int m = 0; m < M; ++m) {
+    g[m] = env->map_off[m + 1] > env->map_off[m] ? base : 0;
+    used += g[m];
+  }
+  while (used < G) {  // the spare CTAs, one at a time, to the highest cost per CTA
+    int best = -1;
+    for (int m = 0; m < M; ++m)
+      if (g[m] > 0 && (best < 0 || w[m] * g[best] > w[best] * g[m])) best = m;
+    if (best < 0) return;
+    ++g[best];
+    ++used;
+  }
+  std::vector<int64_t> cuts{env->map_off[0]};
+  for (int m = 0; m < M; ++m) {
+    const int64_t nm = env->map_off[m + 1] - env->map_off[m];
+    for (int c = 1; c <= g[m]; ++c) cuts.push_back(env->map_off[m] + nm * c / g[m]);
+  }
+  if ((int)cuts.size() != G + 1) return;
+  for (int b = 0; b < G; ++b) {
+    if (cuts[b + 1] - cuts[b] > d.chunk_cap) return;  // keep the lane-count plan
+    int m = 0;
+    while (env->map_off[m + 1] <= cuts[b] && m + 1 < M) ++m;
+    if (cuts[b + 1] > env->map_off[m + 1]) return;
+  }
+  for (int b = 0; b <= G; ++b) d.plan_begin[b] = (int32_t)cuts[b];
+  for (int b = 0; b < G; ++b) {
+    int m = 0;
+    while (env->map_off[m + 1] <= cuts[b] && m + 1 < M) ++m;
+    d.plan_end[b] = (int32_t)cuts[b + 1];
+    d.plan_map[b] = (int16_t)m;
+    d.plan_mstart[b] = (int32_t)env->map_off[m];
+    d.plan_mend[b] = (int32_t)env->map_off[m + 1];
+  }
+}
+
 static int launch_env(SpEnv* env, StepArgs a, cudaStream_t st, const EnvDev* dp = nullptr) {
+  // the one-shot re-plan: step launches of the main plan outside graph capture
+  bool rp = !dp && env->replan_state < 2 && a.mode == MODE_STEP;
+  if (rp) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    rp = cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
+  }
+  if (rp && env->replan_state == 1 && cudaEventQuery(env->cyc_ready) == cudaSuccess) {
+    replan_by_cost(env);
+    env->replan_state = 2;
+  }
   const EnvDev& d = dp ? *dp : env->d;
   const int grid = dp ? dp->plan_n : env->grid;
   a.hit_store = env->rec_hit_store;
@@ -661,6 +757,12 @@ static int launch_env(SpEnv* env, StepArgs a, cudaStream_t st, const EnvDev* dp 
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(SP_ECUDA, std::string("env_step_kernel: ") + cudaGetErrorString(e));
+  if (rp && env->replan_state == 0 && ++env->step_launches == 3) {
+    SP_CUDA(cudaMemcpyAsync(env->cyc_host, env->d.cta_cyc, 4 * (size_t)env->d.plan_n,
+                            cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaEventRecord(env->cyc_ready, st));
+    env->replan_state = 1;
+  }
   return SP_OK;
 }
 
