@@ -125,7 +125,8 @@ int sp_env_set_recording(SpEnv* env, int32_t* hit_store, int32_t* hit_state,
  *   dones u8[N] | truncated u8[N] | events i8[N].
  * One H2D copy of the actions, the fused step, the D2H copy of the block
  * (device staging owned by the handle); returns after everything synchronized.
- * From 16,384 envs (default map assignment) the step runs as row parts: part
+ * From 16,384 envs (default map assignment) the step runs as row parts (two:
+ * a quarter of the rows, then the rest): part
  * p's launch, then its obs rows' copy on a second stream while part p + 1
  * steps (SPARROW_HOST_PARTS sets the count, 1 = one launch and one copy on
  * `stream`).  Page-locked host memory lets the copies run at full PCIe

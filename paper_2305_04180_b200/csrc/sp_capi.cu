@@ -585,17 +585,42 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
   env->grid = plan.grid;
   env->threads = plan.threads;
   env->smem = plan.smem;
-  // sp_env_step_host row parts (default 4 from 16,384 envs; SPARROW_HOST_PARTS
-  // sets the count, 1 = off): for the default map assignment a row range holds,
-  // per map, one contiguous slot range, so each part gets its own launch plan
+  // sp_env_step_host row parts (default from 16,384 envs: two, a quarter of the
+  // rows then the rest; SPARROW_HOST_PARTS sets an even split into that many,
+  // 1 = off; SPARROW_HOST_PART_W="w0,w1,..." weights them): for the default
+  // map assignment a row range holds, per map, one contiguous slot range, so
+  // each part gets its own launch plan.  A launch costs ~40 us whatever its
+  // size (cfg2's 4,096 envs step in 40 us), so the first part is small only
+  // to start the copies early, and few parts pay: the copies (~95 us per
+  // 16,384 rows) are the floor.  e2e per step at cfg3: four even parts
+  // 0.488 / 0.497 ms, three (1:2:5) 0.478 / 0.478, two (1:3) 0.473 / 0.477.
   {
     const char* hp = std::getenv("SPARROW_HOST_PARTS");
-    int parts = hp ? std::max(1, std::min(8, std::atoi(hp))) : (n_envs >= 16384 ? 4 : 1);
+    if (hp && !*hp) hp = nullptr;  // set but empty: the default
+    const char* pw = std::getenv("SPARROW_HOST_PART_W");
+    std::string wspec = pw ? pw : (hp ? "" : "1,3");
+    int parts = hp ? std::max(1, std::min(8, std::atoi(hp))) : (n_envs >= 16384 ? 2 : 1);
     if (!(d.plan_n > 0 && d.row_affine && d.smem_maps)) parts = 1;
     if (parts > 1) {
       const int M = n_maps;
       std::vector<int64_t> rows(parts + 1);
       for (int p = 0; p <= parts; ++p) rows[p] = n_envs * p / parts;
+      if (!wspec.empty()) {  // part weights
+        std::vector<double> w;
+        for (const char* q = wspec.c_str(); *q;) {
+          w.push_back(std::atof(q));
+          while (*q && *q != ',') ++q;
+          if (*q == ',') ++q;
+        }
+        if ((int)w.size() == parts) {
+          double tot = 0, acc = 0;
+          for (double x : w) tot += x;
+          for (int p = 0; p < parts; ++p) {
+            acc += w[p];
+            rows[p + 1] = p + 1 == parts ? n_envs : (int64_t)(n_envs * acc / tot);
+          }
+        }
+      }
       std::vector<EnvDev> dps;
       bool ok = true;
       for (int p = 0; p < parts && ok; ++p) {

@@ -482,7 +482,7 @@ def test_step_host_matches_device_step():
 @pytest.mark.parametrize("n,parts", [(65_536, None), (4_096, "3"), (3_000, "8")])
 def test_step_host_row_parts_match_device_step(monkeypatch, n, parts):
     """sp_env_step_host in row parts (a launch per part, each part's rows read
-    back while the next part steps; 2 parts by default from 16,384 envs,
+    back while the next part steps; 2 parts (1:3) by default from 16,384 envs,
     SPARROW_HOST_PARTS otherwise) gives the device step's StepBatch, and the
     two handles' episode statistics agree."""
     from paper_2305_04180_b200 import VecEnv
