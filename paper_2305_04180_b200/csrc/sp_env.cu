@@ -386,6 +386,8 @@ __device__ __forceinline__ void ray_park(Ray& r, const MapView& mv) {
 // max_range (range max_range, no hit cell).  An axis the ray does not move
 // along (IDX = inf) has no entry face: its term is -inf, or NaN (0 * inf)
 // when the origin lies on that axis's cell boundary, and fmax drops a NaN.
+// (Compare-selects instead of fmax, with the NaN case kept out by moving such
+// an origin to its cell's centre or tested for, measured +1 % -- dropped.)
 template <bool kSmem>
 __device__ __forceinline__ double ray_end(const Ray& r, const MapView& mv, const EnvDev& d,
                                           int& hit) {
@@ -487,6 +489,17 @@ __device__ __forceinline__ int step_level(int steps) {
   const int msb = 31 - __clz(s);
   const int lv = 2 * msb + ((s >> (msb - 1)) & 1) - 3;
   return lv < 0 ? 0 : (lv > 7 ? 7 : lv);
+}
+
+// step_level of a retiring ray: its step count is 1 + a multiple of
+// SP_MARCH_GROUP (steps are counted per group, ray_phase), so with groups of
+// four the level is a nibble table on steps / 4: 1, 5, 9, .., 33+ -> 0 1 3 4 5 5 6 6 7
+__device__ __forceinline__ int retire_level(int steps) {
+#if SP_MARCH_GROUP == 4
+  return (int)(0x766554310ull >> (4 * min(steps >> 2, 8))) & 15;
+#else
+  return step_level(steps);
+#endif
 }
 
 // predicted bucket of a beam group (0 = longest): 7 - its highest level
@@ -859,7 +872,7 @@ struct FinObs {
     if (r1) r1[5 + j] = o;
     if (t < proximity) c.prox[slot] = 1;
     const int grp = j >> gs;  // byte grp of the 64-bit word, as a 32-bit OR (native)
-    atomicOr((unsigned*)&c.rec[slot].qacc + (grp >> 2), 1u << (8 * (grp & 3) + step_level(steps)));
+    atomicOr((unsigned*)&c.rec[slot].qacc + (grp >> 2), 1u << (8 * (grp & 3) + retire_level(steps)));
     if constexpr (kRec) {
       const int64_t k = (int64_t)(c.gid[slot] - gid0) * R + j;
       // post-step scans fill a store_states row (and the states row too when
