@@ -28,7 +28,9 @@ the fp32 numerics follow the numpy reference to ~1e-6.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
+import gc
 import io
 import math
 import struct
@@ -54,6 +56,20 @@ class CheckpointError(ValueError):
 
 class TrainingDiverged(RuntimeError):
     """A non-finite loss appeared during optimization (ddqn.py:68-71)."""
+
+
+@contextlib.contextmanager
+def no_gc():
+    """Cyclic garbage collection off for a CUDA graph capture: a collected
+    handle of an earlier env or buffer would cudaFree mid-capture, which
+    invalidates the capture (torch.cuda.graph collects once before it begins)."""
+    was = gc.isenabled()
+    gc.disable()
+    try:
+        yield
+    finally:
+        if was:
+            gc.enable()
 
 
 def _torch():
@@ -341,7 +357,7 @@ class _GraphedUpdate:
         self.t.fill_(float(ad.step))
         self.graph = torch.cuda.CUDAGraph()
         # thread_local: the actor thread keeps syncing its own stream meanwhile
-        with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
+        with no_gc(), torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
             self._body()
 
     def _body(self) -> None:
@@ -436,7 +452,7 @@ class _FusedUpdate:
             if self.d_ctr is not None:
                 self.d_ctr.fill_(int(sampler[1].ctr))
             self.graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
+            with no_gc(), torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
                 self._launch()
 
     @property

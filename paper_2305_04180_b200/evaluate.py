@@ -139,7 +139,7 @@ def _rollout(env: VecEnv, net, seed: int, horizon: int, check_every: int, graph:
             if (k + 1) % check_every == 0 and env.all_first_episodes_done:
                 break
     else:
-        from .asl import VemSchedule, select_actions_fused
+        from .asl import VemSchedule, no_gc, select_actions_fused
         from .replay import PhiloxGenerator
         n = env.n_copies
         greedy = VemSchedule(n, or_init=1, or_final=1, e_min=0.0, e_max=0.0)
@@ -152,7 +152,7 @@ def _rollout(env: VecEnv, net, seed: int, horizon: int, check_every: int, graph:
         side = torch.cuda.Stream(env.device)
         side.wait_stream(torch.cuda.current_stream(env.device))
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=side):
+        with no_gc(), torch.cuda.graph(g, stream=side):  # no cudaFree by a collection mid-capture
             for i in range(k_graph):
                 select_actions_fused(net, outs[(i + 1) & 1].states, greedy, 0, rng, out=acts)
                 env.step_device(acts.data_ptr(), outs[i & 1])
