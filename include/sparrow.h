@@ -123,7 +123,7 @@ int sp_env_set_recording(SpEnv* env, int32_t* hit_store, int32_t* hit_state,
  * block of sp_env_host_out_bytes(env) bytes laid out as
  *   rewards f64[N] | states f32[N][5+R] | store_states f32[N][5+R] |
  *   dones u8[N] | truncated u8[N] | events i8[N].
- * One H2D copy of the actions, the fused step, the D2H copy of the block
+ * The H2D copy of the actions, the fused step, the D2H copy of the block
  * (device staging owned by the handle); returns after everything synchronized.
  * From 16,384 envs (default map assignment) the step runs as row parts (two:
  * a quarter of the rows, then the rest): part

@@ -147,6 +147,7 @@ struct SpEnv {
   std::vector<int64_t> part_rows;  // parts + 1 row cuts
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t part_done[8] = {};
+  cudaEvent_t acts_rest = nullptr;  // the actions of parts 1.. landed (copy stream)
   std::mutex mu;
 
   template <class T>
@@ -166,6 +167,7 @@ struct SpEnv {
     if (cyc_ready) cudaEventDestroy(cyc_ready);
     for (cudaEvent_t e : part_done)
       if (e) cudaEventDestroy(e);
+    if (acts_rest) cudaEventDestroy(acts_rest);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (h_scan) cudaFreeHost(h_scan);
     if (scan_copied) cudaEventDestroy(scan_copied);
@@ -656,6 +658,7 @@ int sp_env_create(const SpConfig* cfg, const SpMapDesc* maps, int32_t n_maps, in
       if (ok && cudaStreamCreateWithFlags(&env->copy_stream, cudaStreamNonBlocking) == cudaSuccess) {
         for (int p = 0; p < parts && ok; ++p)
           ok = cudaEventCreateWithFlags(&env->part_done[p], cudaEventDisableTiming) == cudaSuccess;
+        ok = ok && cudaEventCreateWithFlags(&env->acts_rest, cudaEventDisableTiming) == cudaSuccess;
         if (ok) {
           env->dpart = dps;
           env->part_rows = rows;
@@ -874,13 +877,13 @@ int sp_env_step_host(SpEnv* env, const int64_t* h_actions, void* h_out, void* st
   cudaStream_t st = (cudaStream_t)stream;
   uint8_t* dev_act = env->d_host_stage;
   uint8_t* o = env->d_host_stage + 8 * n;  // output block, 8-byte aligned
-  SP_CUDA(cudaMemcpyAsync(dev_act, h_actions, 8 * n, cudaMemcpyHostToDevice, st));
   double* rewards = (double*)o;
   float* states = (float*)(o + 8 * n);
   float* store = states + n * D;
   uint8_t* dones = (uint8_t*)(store + n * D);
   const int parts = (int)env->dpart.size();
   if (parts < 2) {
+    SP_CUDA(cudaMemcpyAsync(dev_act, h_actions, 8 * n, cudaMemcpyHostToDevice, st));
     const int rc = step_locked(env, (const int64_t*)dev_act, states, store, rewards, dones,
                                dones + n, (int8_t*)(dones + 2 * n), st);
     if (rc != SP_OK) return rc;
@@ -907,7 +910,17 @@ int sp_env_step_host(SpEnv* env, const int64_t* h_actions, void* h_out, void* st
   int ti = 0;
   cudaEventRecord(tev[ti++], st);
 #endif
+  // the first part's actions on the step stream, the rest beside its launch
+  // on the copy stream (idle until the first part's rows are ready)
+  {
+    const int64_t r1 = env->part_rows[1];
+    SP_CUDA(cudaMemcpyAsync(dev_act, h_actions, 8 * r1, cudaMemcpyHostToDevice, st));
+    SP_CUDA(cudaMemcpyAsync(dev_act + 8 * r1, h_actions + r1, 8 * (n - r1), cudaMemcpyHostToDevice,
+                            env->copy_stream));
+    SP_CUDA(cudaEventRecord(env->acts_rest, env->copy_stream));
+  }
   for (int p = 0; p < parts; ++p) {
+    if (p == 1) SP_CUDA(cudaStreamWaitEvent(st, env->acts_rest, 0));
     // the handle's current parameters (seed etc.) with part p's launch plan
     EnvDev dp = env->d;
     const EnvDev& pp = env->dpart[p];
