@@ -633,7 +633,9 @@ def run_ours(args, rank, world, local_rank):
                     "d2h_probe_gbs": d2h_gbs,
                     "pcie_share": (d2h / d2h_gbs / 1e9) / (e2e_t / Ke),
                     "numa": numa,
-                    "path": "VecEnv.step_host: pinned host actions in, every StepBatch field out as numpy"},
+                    "path": "VecEnv.step_host: pinned host actions in (range-checked on the host "
+                            "before any launch, as the reference's step_all), every StepBatch "
+                            "field out as numpy"},
             "roofline": {"bound": "smem", "achieved": smem_ach, "peak": smem_peak, "unit": "GB/s",
                          "frac": smem_ach / smem_peak,
                          "traffic": nm.get("traffic_bytes_per_launch"),

@@ -125,6 +125,9 @@ int sp_env_set_recording(SpEnv* env, int32_t* hit_store, int32_t* hit_state,
  *   dones u8[N] | truncated u8[N] | events i8[N].
  * The H2D copy of the actions, the fused step, the D2H copy of the block
  * (device staging owned by the handle); returns after everything synchronized.
+ * The actions are checked on the host while their copy is in flight: one
+ * outside [0, n_actions) returns SP_EACTION before anything is launched, so
+ * nothing steps (core.py:169-170).
  * From 16,384 envs (default map assignment) the step runs as row parts (two:
  * a quarter of the rows, then the rest): part
  * p's launch, then its obs rows' copy on a second stream while part p + 1

@@ -863,6 +863,17 @@ int64_t sp_env_host_out_bytes(SpEnv* env) {
   return env->n * (8 + 2 * 4 * (int64_t)env->D + 3);
 }
 
+// The first action outside [0, n_actions) (core.py:169-170), or -1: one
+// branch-free pass (a maximum of the unsigned values), then the index.
+static int64_t first_bad_action(const int64_t* a, int64_t n, int64_t n_actions) {
+  uint64_t mx = 0;
+  for (int64_t i = 0; i < n; ++i) mx = std::max(mx, (uint64_t)a[i]);
+  if (mx < (uint64_t)n_actions) return -1;
+  for (int64_t i = 0; i < n; ++i)
+    if ((uint64_t)a[i] >= (uint64_t)n_actions) return i;
+  return -1;
+}
+
 int sp_env_step_host(SpEnv* env, const int64_t* h_actions, void* h_out, void* stream) {
   if (!env || !h_actions || !h_out) return fail(SP_EINVAL, "null argument");
   DevDeviceGuard guard(env->device);
@@ -882,14 +893,35 @@ int sp_env_step_host(SpEnv* env, const int64_t* h_actions, void* h_out, void* st
   float* store = states + n * D;
   uint8_t* dones = (uint8_t*)(store + n * D);
   const int parts = (int)env->dpart.size();
+  // the actions are checked on the host while their copy is in flight, before
+  // any launch: an invalid one raises before anything steps, as in the
+  // reference (core.py:169-170), and costs no extra PCIe round trip
+  auto check_actions = [&]() -> int {
+    const int64_t bad = first_bad_action(h_actions, n, env->d.n_actions);
+    if (bad < 0) return SP_OK;
+    cudaStreamSynchronize(st);
+    if (env->copy_stream) cudaStreamSynchronize(env->copy_stream);
+    return fail(SP_EACTION, "action index out of range (env " + std::to_string(bad) + ")");
+  };
   if (parts < 2) {
     SP_CUDA(cudaMemcpyAsync(dev_act, h_actions, 8 * n, cudaMemcpyHostToDevice, st));
+    if (const int rc = check_actions()) return rc;
     const int rc = step_locked(env, (const int64_t*)dev_act, states, store, rewards, dones,
                                dones + n, (int8_t*)(dones + 2 * n), st);
     if (rc != SP_OK) return rc;
     SP_CUDA(cudaMemcpyAsync(h_out, o, out_bytes, cudaMemcpyDeviceToHost, st));
     SP_CUDA(cudaStreamSynchronize(st));
     return SP_OK;
+  }
+  // the first part's actions on the step stream, the rest beside its launch
+  // on the copy stream (idle until the first part's rows are ready)
+  {
+    const int64_t r1 = env->part_rows[1];
+    SP_CUDA(cudaMemcpyAsync(dev_act, h_actions, 8 * r1, cudaMemcpyHostToDevice, st));
+    SP_CUDA(cudaMemcpyAsync(dev_act + 8 * r1, h_actions + r1, 8 * (n - r1), cudaMemcpyHostToDevice,
+                            env->copy_stream));
+    SP_CUDA(cudaEventRecord(env->acts_rest, env->copy_stream));
+    if (const int rc = check_actions()) return rc;
   }
   // row parts: part p's launch, then its rows' copies on the copy stream
   // while part p + 1 steps (the PCIe read-back is most of a host step)
@@ -910,15 +942,6 @@ int sp_env_step_host(SpEnv* env, const int64_t* h_actions, void* h_out, void* st
   int ti = 0;
   cudaEventRecord(tev[ti++], st);
 #endif
-  // the first part's actions on the step stream, the rest beside its launch
-  // on the copy stream (idle until the first part's rows are ready)
-  {
-    const int64_t r1 = env->part_rows[1];
-    SP_CUDA(cudaMemcpyAsync(dev_act, h_actions, 8 * r1, cudaMemcpyHostToDevice, st));
-    SP_CUDA(cudaMemcpyAsync(dev_act + 8 * r1, h_actions + r1, 8 * (n - r1), cudaMemcpyHostToDevice,
-                            env->copy_stream));
-    SP_CUDA(cudaEventRecord(env->acts_rest, env->copy_stream));
-  }
   for (int p = 0; p < parts; ++p) {
     if (p == 1) SP_CUDA(cudaStreamWaitEvent(st, env->acts_rest, 0));
     // the handle's current parameters (seed etc.) with part p's launch plan

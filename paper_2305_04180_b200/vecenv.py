@@ -421,7 +421,11 @@ class VecEnv:
             if a.shape != (self.n_copies,):
                 raise ValueError(f"expected {self.n_copies} actions, got shape {a.shape}")
             np.copyto(bufs.actions.numpy(), a, casting="same_kind")
-        if self.check_actions:
+        # sp_env_step_host checks the actions on the host before it launches
+        # (SP_EACTION -> ValueError, nothing stepped: core.py:169-170); the
+        # no-auto-reset path checks them here too, because the reference
+        # raises for bad actions before it raises for lanes awaiting a reset
+        if self.check_actions and not self.auto_reset:
             av = bufs.actions.numpy()
             if av.min() < 0 or av.max() >= self.n_actions:  # core.py:169-170
                 raise ValueError("action index out of range")

@@ -479,6 +479,29 @@ def test_step_host_matches_device_step():
         b_env.step_host(np.full(n, 7))
 
 
+@pytest.mark.parametrize("n", [257, 20_000])
+def test_step_host_bad_action_steps_nothing(n):
+    """core.py:169-170: one action out of range raises ValueError before any
+    lane steps -- sp_env_step_host checks on the host while the actions'
+    copy is in flight (one part and the row-part path): the next valid step
+    equals a twin env's that never saw the bad call."""
+    from paper_2305_04180_b200 import VecEnv
+    maps = load_maps(16)
+    a_env = VecEnv(maps, n, ranges(0.3), config(32))
+    b_env = VecEnv(maps, n, ranges(0.3), config(32))
+    a_env.reset_all(11)
+    b_env.reset_all(11)
+    acts = np.ascontiguousarray(random_actions(11, np.arange(n), 0), np.int64)
+    bad = acts.copy()
+    bad[n // 2] = 5
+    with pytest.raises(ValueError, match="out of range"):
+        b_env.step_host(bad)
+    x, y = a_env.step_host(acts), b_env.step_host(acts)
+    for f in ("states", "store_states", "rewards", "dones", "truncated", "events"):
+        assert np.array_equal(getattr(x, f), getattr(y, f)), f
+    b_env.check()  # no sticky device error
+
+
 @pytest.mark.parametrize("n,parts", [(65_536, None), (4_096, "3"), (3_000, "8")])
 def test_step_host_row_parts_match_device_step(monkeypatch, n, parts):
     """sp_env_step_host in row parts (a launch per part, each part's rows read
